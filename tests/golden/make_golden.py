@@ -1,0 +1,285 @@
+"""Generate golden vectors by running the REFERENCE package itself.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports `gnnio` read-only from /root/reference/pkg/src and writes
+sampler.npz / cache.npz / ordering.npz next to this file. The fixtures are
+committed; nothing on the GPU box reads /root/reference.
+
+What is pinned (the reference ships no golden arrays):
+  * sampler: per-hop frontiers + parent_idx of `_sample_hop` chained exactly
+    as `sample_batch` does (sampler.py:97-116), `sample_batch`'s distinct set,
+    and `simulate_epoch` traces + EpochCommReport (sampler.py:119-167);
+  * cache: per-batch counters, per-node outcome codes and the ring contents +
+    tail of every level after every batch (cachesim.py:81-107, 461-549);
+  * ordering: `generate_bfs_sequences`, `proximity_schedule`,
+    `random_shuffle_schedule` (ordering.py:57-207).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from packing import put  # noqa: E402
+
+from gnnio import cachesim as cs  # noqa: E402
+from gnnio import ordering as od  # noqa: E402
+from gnnio import sampler as sp  # noqa: E402
+from gnnio.graph import build_graph, generate_power_law  # noqa: E402
+from gnnio.partition import random_partition  # noqa: E402
+from gnnio.sampler import AccessTrace  # noqa: E402
+
+
+def make_graph(edges, n, train=None):
+    g = build_graph(np.array(edges, dtype=np.int64).reshape(-1, 2), n, undirected=True)
+    if train is not None:
+        g.train_mask[:] = False
+        g.train_mask[list(train)] = True
+    return g
+
+
+def graphs():
+    gs = {}
+    gs["planted"] = generate_power_law(2000, 8, seed=4, train_fraction=0.1, num_labels=8)
+    gs["star6"] = make_graph([(0, i) for i in range(1, 6)], 6, train=range(6))
+    gs["path5"] = make_graph([(0, 1), (1, 2), (2, 3), (3, 4)], 5, train=range(5))
+    gs["isolated"] = make_graph([(0, 1), (1, 2), (3, 4)], 8, train=[0, 2, 5, 6, 7])
+    gs["dense"] = generate_power_law(3000, 40, seed=3, train_fraction=0.2, num_labels=4)
+    return gs
+
+
+def store_graph(out, name, g):
+    out[f"g_{name}_off"] = g.row_offsets.astype(np.int64)
+    out[f"g_{name}_col"] = g.col_indices.astype(np.int64)
+    out[f"g_{name}_train"] = g.train_mask.astype(np.uint8)
+
+
+def sampler_cases(gs):
+    rng = np.random.default_rng(2024)
+    cases = []
+    pl = gs["planted"]
+    dn = gs["dense"]
+    cases.append(("star6", [0], (3, 3), 7, 0))
+    cases.append(("star6", [0, 0, 3], (10, 2), 1, 5))
+    cases.append(("isolated", [5, 2, 5, 0], (4, 4), 0, 0))
+    cases.append(("path5", [2], (1, 1, 1), 3, 9))
+    for i in range(6):
+        seeds = pl.train_nodes()[rng.integers(pl.num_train(), size=int(rng.integers(1, 80)))]
+        fan = tuple(int(x) for x in rng.integers(1, 16, size=int(rng.integers(1, 4))))
+        cases.append(("planted", seeds.tolist(), fan, int(rng.integers(100)), int(rng.integers(1000))))
+    # high fanouts (> 32 and >= hub degrees) exercise the wide-k path
+    for fan in ((40,), (64, 3), (200,), (15, 10, 5)):
+        seeds = dn.train_nodes()[rng.integers(dn.num_train(), size=24)]
+        cases.append(("dense", seeds.tolist(), fan, int(rng.integers(100)), int(rng.integers(1000))))
+    return cases
+
+
+def make_sampler(gs):
+    out = {}
+    for name, g in gs.items():
+        store_graph(out, name, g)
+    cases = sampler_cases(gs)
+    meta, seeds_l, fan_l, fr_l, pi_l, dist_l = [], [], [], [], [], []
+    hop_count = []
+    for gname, seeds, fan, seed, bseed in cases:
+        g = gs[gname]
+        cfg = sp.SamplingConfig(fanouts=fan, seed=seed)
+        rng = sp._batch_rng(cfg, bseed)
+        parents = np.asarray(seeds, dtype=np.int64)
+        for f in fan:
+            ids, pidx = sp._sample_hop(g, parents, f, rng)
+            fr_l.append(ids)
+            pi_l.append(pidx)
+            parents = ids
+        frontiers, distinct = sp.sample_batch(g, np.asarray(seeds), cfg, batch_seed=bseed)
+        for a, b in zip(frontiers, fr_l[-len(fan):]):
+            assert np.array_equal(a, b)
+        dist_l.append(distinct)
+        seeds_l.append(seeds)
+        fan_l.append(fan)
+        hop_count.append(len(fan))
+        meta.append((list(gs).index(gname), seed, bseed))
+    out["graph_names"] = np.array(list(gs))
+    out["case_meta"] = np.array(meta, dtype=np.int64)
+    put(out, "case_seeds", seeds_l)
+    put(out, "case_fanouts", fan_l)
+    put(out, "hop_ids", fr_l)
+    put(out, "hop_pidx", pi_l)
+    put(out, "distinct", dist_l)
+
+    # epochs: simulate_epoch over two schedules and two partitionings
+    pl = gs["planted"]
+    ep_meta, ep_trace, ep_batches = [], [], []
+    ep_report = []
+    for k, sched_kind, fan, seed in ((4, "prox", (5, 5), 7), (1, "rand", (10, 5), 0), (3, "rand", (15, 10, 5), 2)):
+        part = random_partition(pl, k, seed=seed)
+        if sched_kind == "prox":
+            sched = od.proximity_schedule(pl, 2, 40, seed=0)
+        else:
+            sched = od.random_shuffle_schedule(pl, 64, seed=seed)
+        trace, rep = sp.simulate_epoch(pl, part, sched, sp.SamplingConfig(fanouts=fan, seed=seed))
+        ep_meta.append((k, seed, len(sched.batches)))
+        ep_batches.append(sched.batches)
+        ep_trace.append(trace.batches)
+        ep_report.append((rep.local_accesses, rep.remote_accesses, rep.seed_load, rep.request_load, part.part_of))
+        out[f"epoch{len(ep_meta) - 1}_fanouts"] = np.array(fan, dtype=np.int64)
+    out["epoch_meta"] = np.array(ep_meta, dtype=np.int64)
+    for e, (batches, trace, rep) in enumerate(zip(ep_batches, ep_trace, ep_report)):
+        put(out, f"epoch{e}_batches", batches)
+        put(out, f"epoch{e}_trace", trace)
+        out[f"epoch{e}_local_remote"] = np.array(rep[:2], dtype=np.int64)
+        out[f"epoch{e}_seed_load"] = rep[2]
+        out[f"epoch{e}_request_load"] = rep[3]
+        out[f"epoch{e}_part_of"] = rep[4].astype(np.int64)
+    np.savez_compressed(os.path.join(HERE, "sampler.npz"), **out)
+
+
+def cache_case_batches(rng, kind):
+    universe = int(rng.integers(8, 300))
+    batches = []
+    remaining = int(rng.integers(50, 3000))
+    while remaining > 0:
+        size = int(min(remaining, rng.integers(1, min(universe, 64) + 1)))
+        b = rng.choice(universe, size=size, replace=False)
+        if kind == "sorted":
+            b = np.sort(b)
+        elif kind == "dups":
+            b = np.concatenate([b, b[: max(1, size // 3)]])
+            rng.shuffle(b)
+        batches.append(b)
+        remaining -= size
+    return batches
+
+
+def make_cache():
+    rng = np.random.default_rng(42)
+    out = {}
+    specs = []
+    all_batches, all_codes, all_counters = [], [], []
+    dev_slots, dev_tails, host_slots, host_tails = [], [], [], []
+    kinds = ["sorted"] * 40 + ["unsorted"] * 10 + ["dups"] * 10
+    for ci, kind in enumerate(kinds):
+        batches = cache_case_batches(rng, kind)
+        d = int(rng.choice([1, 2, 4, 8]))
+        cap = int(rng.integers(0, 65))
+        hcap = int(rng.choice([0, 1, 8, 64]))
+        use_bd = ci % 5 == 4
+        bd = [int(x) for x in rng.integers(d, size=len(batches))] if use_bd else None
+        cfg = cs.CacheConfig(device_capacity=cap, host_capacity=hcap, num_devices=d, policy="fifo",
+                             feature_bytes_per_node=400)
+        state = cs.cold_state(cfg)
+        codes_case, cnt_case = [], []
+        ds, dt, hs, ht = [], [], [], []
+        for i, b in enumerate(batches):
+            rep = cs.simulate(AccessTrace(batches=[np.asarray(b, dtype=np.int64)]), cfg,
+                              batch_devices=[bd[i] if bd else i % d], state=state, record_outcomes=True)
+            codes_case.append(np.array(["DPHM".index(c) for c in rep.outcomes[0]], dtype=np.int64))
+            cnt_case.append([rep.batch_queries[0], rep.batch_own_hits[0], rep.batch_peer_hits[0],
+                             rep.batch_host_hits[0], rep.batch_misses[0], rep.batch_insertions[0],
+                             rep.batch_evictions[0], rep.batch_metadata_updates[0]])
+            ds.append(np.stack([lv.slots for lv in state.devices]).ravel())
+            dt.append([lv.tail for lv in state.devices])
+            hs.append(state.host.slots.copy())
+            ht.append(state.host.tail)
+        # the whole-trace call must agree with the batch-at-a-time replay
+        whole = cs.simulate(AccessTrace(batches=[np.asarray(b, dtype=np.int64) for b in batches]), cfg,
+                            batch_devices=bd, record_outcomes=True)
+        assert whole.batch_misses == [c[4] for c in cnt_case]
+        specs.append((d, cap, hcap, len(batches), int(use_bd), ["sorted", "unsorted", "dups"].index(kind)))
+        all_batches.extend(batches)
+        all_codes.extend(codes_case)
+        all_counters.extend(cnt_case)
+        dev_slots.extend(ds)
+        dev_tails.extend(dt)
+        host_slots.extend(hs)
+        host_tails.append(ht)
+        out[f"bd_{ci}"] = np.array(bd if bd else [], dtype=np.int64)
+    out["specs"] = np.array(specs, dtype=np.int64)
+    put(out, "batches", all_batches)
+    put(out, "codes", all_codes, np.int8)
+    out["counters"] = np.array(all_counters, dtype=np.int64)
+    put(out, "dev_slots", dev_slots)
+    put(out, "dev_tails", dev_tails)
+    put(out, "host_slots", host_slots)
+    put(out, "host_tails", host_tails)
+
+    # a sampler-produced trace at desk scale (acceptance-style, 10% capacity)
+    g = generate_power_law(5000, 10, seed=1, train_fraction=0.1, num_labels=16)
+    sched = od.proximity_schedule(g, 4, 100, seed=1)
+    trace, _ = sp.simulate_epoch(g, random_partition(g, 1, seed=0), sched,
+                                 sp.SamplingConfig(fanouts=(10, 5), seed=1))
+    put(out, "real_trace", trace.batches)
+    real = []
+    for d in (1, 2, 4, 8):
+        rep = cs.simulate(trace, cs.CacheConfig(device_capacity=500 // d, host_capacity=250,
+                                                num_devices=d, policy="fifo"), record_outcomes=True)
+        real.append([rep.batch_queries, rep.batch_own_hits, rep.batch_peer_hits, rep.batch_host_hits,
+                     rep.batch_misses, rep.batch_insertions, rep.batch_evictions])
+    out["real_counters"] = np.array(real, dtype=np.int64)   # [4 d-values, 7, nb]
+    np.savez_compressed(os.path.join(HERE, "cache.npz"), **out)
+
+
+def make_ordering(gs):
+    out = {}
+    for name, g in gs.items():
+        store_graph(out, name, g)
+    out["graph_names"] = np.array(list(gs))
+    seq_meta, seqs, scheds, sched_meta = [], [], [], []
+    for gname, S, seed in (("planted", 1, 0), ("planted", 3, 1), ("planted", 4, 2), ("planted", 7, 5),
+                           ("dense", 4, 3), ("path5", 1, 4), ("star6", 2, 6), ("isolated", 2, 1),
+                           ("isolated", 5, 8)):
+        g = gs[gname]
+        res = od.generate_bfs_sequences(g, S, seed=seed)
+        seq_meta.append((list(gs).index(gname), S, seed))
+        seqs.extend(res)
+    # random small (mostly disconnected) graphs exercise restarts
+    rng = np.random.default_rng(77)
+    rnd_graphs = []
+    for i in range(12):
+        n = int(rng.integers(20, 400))
+        m = int(rng.integers(n // 2, 2 * n))
+        g = build_graph(rng.integers(n, size=(m, 2)), n)
+        g.train_mask[rng.random(n) < 0.4] = True
+        if g.num_train() < 6:
+            g.train_mask[:6] = True
+        store_graph(out, f"rnd{i}", g)
+        S = int(rng.integers(1, 6))
+        seed = int(rng.integers(1000))
+        res = od.generate_bfs_sequences(g, S, seed=seed)
+        seq_meta.append((100 + i, S, seed))
+        seqs.extend(res)
+        b = int(rng.integers(1, 30))
+        sched = od.proximity_schedule(g, S, b, seed=seed)
+        sched_meta.append((100 + i, S, b, seed, len(sched.batches), 0))
+        scheds.extend(sched.batches)
+        rs = od.random_shuffle_schedule(g, b, seed=seed)
+        sched_meta.append((100 + i, 0, b, seed, len(rs.batches), 1))
+        scheds.extend(rs.batches)
+    for gname, S, b, seed in (("planted", 4, 64, 2), ("dense", 4, 100, 1), ("planted", 2, 40, 0)):
+        g = gs[gname]
+        sched = od.proximity_schedule(g, S, b, seed=seed)
+        sched_meta.append((list(gs).index(gname), S, b, seed, len(sched.batches), 0))
+        scheds.extend(sched.batches)
+    out["seq_meta"] = np.array(seq_meta, dtype=np.int64)
+    put(out, "seqs", seqs)
+    out["sched_meta"] = np.array(sched_meta, dtype=np.int64)
+    put(out, "sched_batches", scheds)
+    np.savez_compressed(os.path.join(HERE, "ordering.npz"), **out)
+
+
+if __name__ == "__main__":
+    gs = graphs()
+    make_sampler(gs)
+    make_cache()
+    make_ordering(gs)
+    for f in ("sampler.npz", "cache.npz", "ordering.npz"):
+        print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -1,0 +1,180 @@
+"""Pin the CPU oracle against golden vectors produced by the reference itself
+(tests/golden/make_golden.py). CPU only."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_graph
+from packing import get
+
+from oracle import cache_oracle as co
+from oracle import features_oracle as fo
+from oracle import ordering_oracle as oo
+from oracle import pcg64
+from oracle import sampler_oracle as so
+
+
+def _cases(npz):
+    meta = npz["case_meta"]
+    seeds = get(npz, "case_seeds")
+    fans = get(npz, "case_fanouts")
+    ids = get(npz, "hop_ids")
+    pidx = get(npz, "hop_pidx")
+    dist = get(npz, "distinct")
+    names = list(npz["graph_names"])
+    h = 0
+    for c in range(len(meta)):
+        gi, seed, bseed = (int(x) for x in meta[c])
+        nh = len(fans[c])
+        yield names[gi], seeds[c], tuple(int(f) for f in fans[c]), seed, bseed, ids[h:h + nh], pidx[h:h + nh], dist[c]
+        h += nh
+
+
+@pytest.mark.parametrize("hop", [so.sample_hop, so.sample_hop_topk], ids=["segsort", "topk"])
+def test_sampler_matches_reference(golden, hop):
+    npz = golden("sampler")
+    n = 0
+    for gname, seeds, fans, seed, bseed, ids, pidx, dist in _cases(npz):
+        off, col, _ = golden_graph(npz, gname)
+        fr, pi, distinct, inverse = so.sample_batch(off, col, seeds, fans, seed, bseed, hop=hop)
+        for a, b in zip(fr, ids):
+            assert np.array_equal(a, b)
+        for a, b in zip(pi, pidx):
+            assert np.array_equal(a, b)
+        assert np.array_equal(distinct, dist)
+        allk = np.concatenate([seeds] + fr)
+        assert np.array_equal(distinct[inverse], allk)
+        n += 1
+    assert n >= 14
+
+
+def test_epochs_match_reference(golden):
+    npz = golden("sampler")
+    off, col, _ = golden_graph(npz, "planted")
+    for e, (k, seed, nb) in enumerate(npz["epoch_meta"]):
+        batches = get(npz, f"epoch{e}_batches")
+        fans = tuple(int(x) for x in npz[f"epoch{e}_fanouts"])
+        trace, local, remote, sl, rl = so.simulate_epoch(off, col, npz[f"epoch{e}_part_of"], int(k), batches, fans, int(seed))
+        ref = get(npz, f"epoch{e}_trace")
+        assert len(trace) == nb == len(ref)
+        assert all(np.array_equal(a, b) for a, b in zip(trace, ref))
+        assert [local, remote] == npz[f"epoch{e}_local_remote"].tolist()
+        assert np.array_equal(sl, npz[f"epoch{e}_seed_load"])
+        assert np.array_equal(rl, npz[f"epoch{e}_request_load"])
+
+
+def test_pcg64_restatement_matches_numpy():
+    st, inc = pcg64.stream_state((7, 3))
+    ref = np.random.default_rng((7, 3)).random(2000)
+    for i in (0, 1, 2, 5, 999, 1999):
+        assert pcg64.draw_u53(st, inc, i) * 2.0 ** -53 == ref[i]
+    table = pcg64.jump_table(st, inc)
+    assert table.shape == (65, 4)
+    # composing 2^k jumps equals advance()
+    s = st
+    for k in (0, 3, 10):
+        a = (int(table[1 + k, 0]) << 64) | int(table[1 + k, 1])
+        c = (int(table[1 + k, 2]) << 64) | int(table[1 + k, 3])
+        s = (a * s + c) & pcg64.MASK128
+    assert s == pcg64.advance(st, inc, 1 + 8 + 1024)
+
+
+def _cache_cases(npz):
+    specs = npz["specs"]
+    batches = get(npz, "batches")
+    codes = get(npz, "codes")
+    dslots = get(npz, "dev_slots")
+    dtails = get(npz, "dev_tails")
+    hslots = get(npz, "host_slots")
+    htails = get(npz, "host_tails")
+    cnt = npz["counters"]
+    b0 = 0
+    for ci, (d, cap, hcap, nb, use_bd, kind) in enumerate(specs):
+        bd = npz[f"bd_{ci}"].tolist() if use_bd else None
+        sl = slice(b0, b0 + nb)
+        yield (int(d), int(cap), int(hcap), bd, batches[sl], codes[sl], cnt[sl], dslots[sl], dtails[sl],
+               hslots[sl], htails[ci], int(kind))
+        b0 += nb
+
+
+def test_fifo_sequential_oracle_matches_reference(golden):
+    npz = golden("cache")
+    for d, cap, hcap, bd, batches, codes, cnt, dsl, dtl, hsl, htl, _ in _cache_cases(npz):
+        eng = co.FifoEngine(cap, hcap, d)
+        for i, b in enumerate(batches):
+            c, cd = eng.run([b], [bd[i] if bd else i % d])
+            assert np.array_equal(cd[0], codes[i])
+            assert np.array_equal(c[0], cnt[i][:7])
+            assert cnt[i][7] == 0   # FIFO never updates metadata (cachesim.py:240-241)
+            assert np.array_equal(np.concatenate([r.slots for r in eng.devices]) if cap else np.empty(0), dsl[i])
+            assert [r.tail for r in eng.devices] == dtl[i].tolist()
+            assert np.array_equal(eng.host.slots, hsl[i])
+            assert eng.host.tail == htl[i]
+
+
+def test_fifo_batched_oracle_matches_reference(golden):
+    npz = golden("cache")
+    for d, cap, hcap, bd, batches, codes, cnt, dsl, dtl, hsl, htl, _ in _cache_cases(npz):
+        state = None
+        for i, b in enumerate(batches):
+            kw = {} if state is None else dict(dev_slots=state[0], dev_tails=state[1], host_slots=state[2], host_tail=state[3])
+            c, cd, state = co.simulate_batched([b], cap, hcap, d, [bd[i] if bd else i % d], **kw)
+            assert np.array_equal(cd[0], codes[i])
+            assert np.array_equal(c[0], cnt[i][:7])
+            assert np.array_equal(state[0].ravel(), dsl[i])
+            assert state[1].tolist() == dtl[i].tolist()
+            assert np.array_equal(state[2], hsl[i])
+            assert state[3] == htl[i]
+
+
+def test_fifo_real_trace(golden):
+    npz = golden("cache")
+    trace = get(npz, "real_trace")
+    for j, d in enumerate((1, 2, 4, 8)):
+        c, _, _ = co.simulate_batched(trace, 500 // d, 250, d)
+        assert np.array_equal(c.T, npz["real_counters"][j])
+
+
+def test_ordering_matches_reference(golden):
+    npz = golden("ordering")
+    names = list(npz["graph_names"])
+    seqs = get(npz, "seqs")
+    s0 = 0
+    for gi, S, seed in npz["seq_meta"]:
+        gname = names[gi] if gi < 100 else f"rnd{gi - 100}"
+        off, col, train = golden_graph(npz, gname)
+        res = oo.bfs_sequences(off, col, train, int(S), int(seed))
+        assert len(res) == S
+        for a, b in zip(res, seqs[s0:s0 + S]):
+            assert np.array_equal(a, b)
+        s0 += S
+    batches = get(npz, "sched_batches")
+    b0 = 0
+    for gi, S, b, seed, nb, kind in npz["sched_meta"]:
+        gname = names[gi] if gi < 100 else f"rnd{gi - 100}"
+        off, col, train = golden_graph(npz, gname)
+        if kind == 0:
+            got = oo.proximity_schedule(off, col, train, int(S), int(b), int(seed))
+        else:
+            got = oo.random_schedule(train, int(b), int(seed))
+        assert len(got) == nb
+        for x, y in zip(got, batches[b0:b0 + nb]):
+            assert np.array_equal(x, y)
+        b0 += nb
+
+
+def test_interleave_hand_cases():
+    # ordering tests test_form_batches_* (test_ordering.py:113-128 of the reference)
+    assert [b.tolist() for b in oo.interleave([np.arange(7)], 3)[1]] == [[0, 1, 2], [3, 4, 5], [6]]
+    assert [b.tolist() for b in oo.interleave([np.array([1, 2]), np.array([3, 4])], 2)[1]] == [[1, 3], [2, 4]]
+    assert oo.interleave([np.array([1, 2, 5]), np.array([3])], 2)[1][0].tolist() == [1, 3]
+    with pytest.raises(ValueError):
+        oo.interleave([np.array([1])], 0)
+
+
+def test_feature_hash_properties():
+    a = fo.synthetic_features(np.array([0, 1, 123456789]), 100, seed=3)
+    assert a.dtype == np.float32 and a.shape == (3, 100)
+    assert np.all(a >= -0.5) and np.all(a < 0.5)
+    assert np.array_equal(a, fo.synthetic_features(np.array([0, 1, 123456789]), 100, seed=3))
+    assert not np.array_equal(a, fo.synthetic_features(np.array([0, 1, 123456789]), 100, seed=4))
