@@ -1,0 +1,200 @@
+/*
+ * bgl_b200.h -- C ABI of the B200-native BGL per-mini-batch preprocessing path.
+ *
+ * Drop-in boundary. The reference (`gnnio`, /root/reference/pkg/src/gnnio) is a
+ * pure-Python package, so its "FFI" for this path is the set of Python module
+ * functions it exports; each entry point below replaces the arithmetic of one
+ * of them and cites the reference interface (file:line) it stands in for. The
+ * Python host layer `paper_2112_08541_b200/{sampler,cachesim,ordering,
+ * features}.py` keeps the reference signatures and calls these through ctypes
+ * (INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *   - All functions return an int status (BGL_OK = 0) and never throw; the
+ *     message of the last failure on the calling thread is bgl_last_error().
+ *   - Pointers are device pointers unless the name says host. Node IDs are
+ *     int32 (n < 2^31), CSR offsets int64. Sizes named `max_*` are host-known
+ *     upper bounds used for launch geometry; the true counts live on the
+ *     device (`*_dev` scalars) so a whole mini-batch runs without a host sync
+ *     and can be captured in a CUDA graph.
+ *   - `stream` is a cudaStream_t passed as void*. No function allocates device
+ *     memory except bgl_cache_create; workspaces are caller-owned.
+ *   - Handles are not thread-safe; order every call by stream.
+ */
+#ifndef BGL_B200_H
+#define BGL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    BGL_OK = 0,
+    BGL_EINVAL = 1,      /* bad argument (ValueError on the Python side) */
+    BGL_ECUDA = 2,       /* CUDA runtime / launch failure */
+    BGL_ENOMEM = 3,      /* device allocation failed */
+    BGL_EUNSUPPORTED = 4 /* shape outside what the kernels implement */
+};
+
+const char* bgl_last_error(void);
+int bgl_abi_version(void);
+
+/* ---------------------------------------------------------------- host memory */
+/* Device-usable alias of a pinned host buffer (zero-copy miss path). */
+int bgl_host_device_pointer(void* host_ptr, void** dev_ptr);
+/* Page-lock + map an existing host buffer (cudaHostRegister Mapped|Portable). */
+int bgl_host_register(void* host_ptr, size_t bytes);
+int bgl_host_unregister(void* host_ptr);
+
+/* ---------------------------------------------------------------- PCG64 replay
+ * Replaces the numpy stream `np.random.default_rng((cfg.seed, batch_seed))`
+ * drawn by `Generator.random` in gnnio/sampler.py:61-62,90.
+ * states: uint64[nb][4] = (state_hi, state_lo, inc_hi, inc_lo) taken from
+ *         numpy's bit_generator.state (the host keeps SeedSequence).
+ * tables: uint64[nb][65][4]; row 0 = the state, row 1+k = (A_hi, A_lo, C_hi,
+ *         C_lo) of the affine map advancing the LCG by 2^k steps. */
+int bgl_pcg64_tables(const uint64_t* states, int64_t nb, uint64_t* tables, void* stream);
+/* 53-bit integers m of draws [first, first+n) of the stream of `table`
+ * (Generator.random() == m * 2^-53). Parity/diagnostics only. */
+int bgl_pcg64_draws(const uint64_t* table, int64_t first, int64_t n, uint64_t* out, void* stream);
+
+/* ---------------------------------------------------------------- sampler
+ * One hop of uniform without-replacement neighbour sampling, bit-exact with
+ * gnnio.sampler._sample_hop (sampler.py:65-94): parent q owns draws
+ * [draw_base[0] + sum_{q'<q} deg(q'), ... + deg(q)) of the batch stream and
+ * emits col[off_q + t] for the min(fanout, deg) smallest (draw, t), ascending,
+ * grouped by parent in parent order. Writes draw_base[1] = draw_base[0] +
+ * sum deg (the chain across hops, sampler.py:110-114) and *num_out_dev.
+ * fanout <= 4096 (any fanout when max degree <= 4096). */
+size_t bgl_sample_hop_workspace(int64_t max_parents);
+int bgl_sample_hop(const int64_t* indptr, const int32_t* indices,
+                   const int32_t* parents, const int64_t* num_parents_dev, int64_t max_parents,
+                   int32_t fanout, const uint64_t* table, int64_t* draw_base,
+                   int32_t* out_ids, int32_t* out_parent_idx, int64_t* num_out_dev,
+                   void* workspace, void* stream);
+
+/* Partition accounting of simulate_epoch (sampler.py:139-153).
+ * request_load[part_of[p]] += 1 for every parent; local_remote[0] += #parents
+ * with part_of[p] == origins[q]; local_remote[1] += the rest. origins NULL:
+ * only the load histogram (seed load, sampler.py:139). */
+int bgl_comm_account(const int32_t* parents, const int64_t* num_dev, int64_t max_n,
+                     const int32_t* origins, const int32_t* part_of, int32_t k,
+                     int64_t* load, int64_t* local_remote, void* stream);
+/* out[i] = src[idx[i]] for i < *num_dev (origin propagation, sampler.py:153). */
+int bgl_take_i32(const int32_t* src, const int32_t* idx, const int64_t* num_dev, int64_t max_n,
+                 int32_t* out, void* stream);
+
+/* ---------------------------------------------------------------- dedup / relabel
+ * Sorted distinct node set of a batch (np.unique, sampler.py:115,157) and the
+ * relabel map rank-in-sorted-set. Direct-address bitmap over the node-ID space
+ * (the paper's "contiguous 1D array as a hashmap") scanned with
+ * a decoupled look-back prefix: output is sorted without a sort.
+ * Keys come in up to 8 segments (seeds, hop 1, hop 2, ...): segment s is
+ * keys + seg_off[s] with *seg_cnt_dev[s] valid entries (max seg_max[s]).
+ * The workspace must be zeroed once (bgl_unique_workspace_init) and is left
+ * clean by bgl_unique_reset. */
+size_t bgl_unique_workspace(int64_t num_nodes);
+int bgl_unique_workspace_init(void* workspace, int64_t num_nodes, void* stream);
+int bgl_unique_sorted(const int32_t* keys, int32_t nseg, const int64_t* seg_off,
+                      const int64_t* seg_cnt_dev, const int64_t* seg_max,
+                      int64_t num_nodes, void* workspace,
+                      int32_t* uniq_out, int64_t* num_uniq_dev, void* stream);
+/* local[i] = rank of keys[i] in the sorted set (np.unique return_inverse);
+ * same segment layout for keys and local. Call before bgl_unique_reset. */
+int bgl_relabel(const int32_t* keys, int32_t nseg, const int64_t* seg_off,
+                const int64_t* seg_cnt_dev, const int64_t* seg_max,
+                int64_t num_nodes, const void* workspace, int32_t* local, void* stream);
+int bgl_unique_reset(void* workspace, int64_t num_nodes, const int32_t* uniq,
+                     const int64_t* num_uniq_dev, int64_t max_uniq, void* stream);
+
+/* ---------------------------------------------------------------- FIFO cache
+ * BGL's dynamic FIFO feature cache (gnnio.cachesim FifoLevel, cachesim.py:
+ * 267-293, engine cachesim.py:376-389, simulate cachesim.py:461-549).
+ * `num_shards` device rings of `shard_capacity` slots (node v lives on shard
+ * v % num_shards), one shared host ring of `host_capacity` slots, a direct-
+ * address index per level, and optionally `row_bytes` of feature storage per
+ * device slot. Batch protocol: lookup -> (gather) -> insert. */
+typedef struct bgl_cache* bgl_cache_t;
+int bgl_cache_create(int64_t num_nodes, int32_t num_shards, int64_t shard_capacity,
+                     int64_t host_capacity, int64_t row_bytes, bgl_cache_t* out);
+int bgl_cache_destroy(bgl_cache_t cache);
+/* Grow the node-ID space of the index (IDs >= old num_nodes become valid). */
+int bgl_cache_reserve_nodes(bgl_cache_t cache, int64_t num_nodes, void* stream);
+int bgl_cache_reset(bgl_cache_t cache, void* stream);
+/* Size the per-batch scratch for batches of up to max_batch distinct IDs
+ * (allocates; call outside CUDA-graph capture). */
+int bgl_cache_reserve_batch(bgl_cache_t cache, int64_t max_batch);
+/* Device pointers of the ring feature rows ([num_shards*shard_capacity][row_bytes]). */
+void* bgl_cache_rows(bgl_cache_t cache);
+/* Classify every query against the pre-batch state (cachesim.py:504-525):
+ * codes[i] in {0:D own, 1:P peer, 2:H host, 3:M miss} (may be NULL);
+ * src_row[i] = global ring row (shard*cap + slot) for D/P, -1 otherwise (may
+ * be NULL); counters[0..4] += queries, own, peer, host, miss.
+ * Then builds the ascending, duplicate-free insert lists from `sorted_ids`
+ * (= ids itself when the batch is already sorted and unique; else the sorted
+ * distinct set of ids, e.g. from bgl_unique_sorted). */
+int bgl_cache_lookup(bgl_cache_t cache, const int32_t* ids, const int64_t* n_dev, int64_t max_n,
+                     int32_t worker, const int32_t* sorted_ids, const int64_t* n_sorted_dev,
+                     int64_t max_sorted, uint8_t* codes, int64_t* src_row, int64_t* counters,
+                     void* stream);
+/* Insert-after-batch (cachesim.py:527-530): device-missed into their home
+ * ring, full misses into the host ring, ascending; counters[5..6] +=
+ * insertions, evictions. When batch_rows != NULL, row i of the batch output
+ * (aligned with sorted_ids) is copied into the slot its node lands in. */
+int bgl_cache_insert(bgl_cache_t cache, const int32_t* sorted_ids, int64_t max_sorted,
+                     const void* batch_rows, int64_t* counters, void* stream);
+/* Synchronous export of the ring contents (int64, -1 = empty) and tails, in
+ * the layout of FifoLevel.slots / .tail (cachesim.py:273-275). Any pointer may
+ * be NULL. dev_slots: [num_shards][shard_capacity]; dev_tails: [num_shards]. */
+int bgl_cache_export(bgl_cache_t cache, int64_t* dev_slots_host, int64_t* dev_tails_host,
+                     int64_t* host_slots_host, int64_t* host_tail_host);
+
+/* ---------------------------------------------------------------- feature gather
+ * Net-new (the reference only counts bytes, cachesim.py:447-458):
+ * out[i] = src_row[i] >= 0 ? ring_rows[src_row[i]] : table[ids[i]], 128-bit
+ * vectorised. `table` may be a device pointer (HBM-resident features) or the
+ * device alias of pinned host memory (zero-copy miss path). src_row NULL:
+ * plain gather out[i] = table[ids[i]]. row_bytes % 4 == 0. */
+int bgl_gather_rows(const int32_t* ids, const int64_t* src_row, const int64_t* n_dev, int64_t max_n,
+                    const void* ring_rows, const void* table, int64_t row_bytes, void* out,
+                    void* stream);
+/* Fill rows of the deterministic synthetic feature table (oracle/features_oracle.py). */
+int bgl_synthetic_features(int64_t first_node, int64_t num_nodes, int32_t dim, uint64_t seed,
+                           float* out, void* stream);
+
+/* ---------------------------------------------------------------- ordering
+ * Level-synchronous BFS of gnnio.ordering.generate_bfs_sequences
+ * (ordering.py:57-116) and the closed-form round-robin of form_batches over
+ * rotated sequences (ordering.py:119-151). The host keeps the numpy rng (one
+ * draw per restart, ordering.py:89-90) and reads two scalars per level.
+ * flags: uint8[n], bit0 = in shard, bit1 = emitted, bit2 = visited.
+ * best:  int64[n] scratch, INT64_MAX on entry and left so on exit. */
+size_t bgl_bfs_workspace(int64_t num_nodes);
+/* One level: frontier members in the shard and not yet emitted are appended
+ * to seq_out at *seq_len_dev in frontier order (*remaining_dev decremented);
+ * unless *remaining_dev reached 0, the next frontier = first occurrence of
+ * every unvisited neighbour in (frontier position, adjacency offset) order is
+ * written to next_front / *n_next_dev and marked visited. */
+int bgl_bfs_level(const int64_t* indptr, const int32_t* indices, int64_t num_nodes,
+                  uint8_t* flags, const int32_t* frontier, const int64_t* n_front_dev,
+                  int64_t max_front, int32_t* seq_out, int64_t* seq_len_dev,
+                  int32_t* next_front, int64_t* n_next_dev, int64_t max_next,
+                  int64_t* best, void* workspace, int64_t* remaining_dev, void* stream);
+/* Restart root: frontier_out[0] = the r-th shard member (shard ascending) not
+ * yet emitted, marked visited; *n_front_dev = 1 (ordering.py:89-92). */
+int bgl_select_pending(const int32_t* shard, int64_t len, const uint8_t* flags, int64_t r,
+                       int32_t* frontier_out, int64_t* n_front_dev, void* workspace,
+                       int64_t num_nodes, void* stream);
+/* out[pos(i, r)] = seq_i[(r + shift[i]) % L_i] with pos(i, r) = sum_j min(L_j, r)
+ * + #{j < i : L_j > r}: the round-robin of form_batches over np.roll(seq_i,
+ * -shift[i]). seq_off: device int64[S+1]; shift: device int64[S]. */
+int bgl_interleave(const int32_t* seq_concat, const int64_t* seq_off, const int64_t* shift,
+                   int32_t S, int64_t total, int32_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BGL_B200_H */

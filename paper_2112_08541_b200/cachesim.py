@@ -1,0 +1,342 @@
+"""Dynamic FIFO feature cache on the B200 (drop-in for gnnio.cachesim).
+
+Same public surface as the reference module (`gnnio/cachesim.py`):
+`POLICIES` (:208), `CacheConfig` (:211-225), `CacheEngineState` (:376-380),
+`cold_state` (:383-389), `warm_static` (:392-410), `CacheSimReport`
+(:413-458), `simulate` (:461-549), `amortized_update_ops` (:552-561),
+`compare_policies` (:564-595).
+
+The FIFO policy -- BGL's cache -- runs on the device (`bgl_cache_*`):
+per-batch classification against the pre-batch state, insert-after-batch in
+ascending ID order, sharded rings (node v on device v % d) plus the shared
+host ring. Results (outcome codes, counters, ring contents and tails) are
+bit-exact with the reference. The state lives in HBM and persists across
+`simulate` calls exactly like the reference's in-place-mutated state.
+
+LRU/LFU are not BGL's path (the paper rejects them) and
+static-degree is its comparison baseline (SURVEY.md §8f "next" #1): they are
+not implemented on the device and raise NotImplementedError -- there is no
+CPU fallback.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+
+POLICIES = ("static-degree", "fifo", "lru", "lfu")
+CODE_CHARS = "DPHM"
+
+
+@dataclass
+class CacheConfig:
+    device_capacity: int
+    host_capacity: int = 0
+    num_devices: int = 1
+    policy: str = "fifo"
+    feature_bytes_per_node: int = 512
+
+    def __post_init__(self):
+        if self.policy not in POLICIES:
+            raise ValueError(f"unknown policy {self.policy!r}; expected one of {POLICIES}")
+        if self.num_devices < 1:
+            raise ValueError("num_devices must be >= 1")
+        if self.device_capacity < 0 or self.host_capacity < 0:
+            raise ValueError("capacities must be >= 0")
+
+
+def _not_on_device(policy: str):
+    return NotImplementedError(
+        f"policy {policy!r} is not on the B200 path (only BGL's 'fifo' cache is; see SURVEY.md §2)")
+
+
+class FifoCacheDevice:
+    """Owner of one bgl_cache handle (rings, indices, tails, optional rows)."""
+
+    def __init__(self, cfg: CacheConfig, num_nodes: int, row_bytes: int = 0):
+        self.cfg = cfg
+        self.num_nodes = max(1, int(num_nodes))
+        self.row_bytes = int(row_bytes)
+        h = _lib.c_vp()
+        _lib.check(_lib.load().bgl_cache_create(self.num_nodes, cfg.num_devices, cfg.device_capacity,
+                                                cfg.host_capacity, self.row_bytes, _lib.ctypes.byref(h)))
+        self.handle = h.value
+        self.max_batch = 0
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            try:
+                _lib.load(require_cuda=False).bgl_cache_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+    def reserve(self, num_nodes: int, max_batch: int) -> None:
+        lib = _lib.load()
+        if num_nodes > self.num_nodes:
+            _lib.check(lib.bgl_cache_reserve_nodes(self.handle, int(num_nodes), _lib.stream_ptr()))
+            self.num_nodes = int(num_nodes)
+        if max_batch > self.max_batch:
+            _lib.check(lib.bgl_cache_reserve_batch(self.handle, int(max_batch)))
+            self.max_batch = int(max_batch)
+
+    def rows_ptr(self) -> int:
+        return _lib.load().bgl_cache_rows(self.handle) or 0
+
+    def export(self):
+        c = self.cfg
+        d, C, Ch = c.num_devices, c.device_capacity, c.host_capacity
+        dev_slots = np.full((d, C), -1, dtype=np.int64)
+        dev_tails = np.zeros(d, dtype=np.int64)
+        host_slots = np.full(Ch, -1, dtype=np.int64)
+        host_tail = np.zeros(1, dtype=np.int64)
+        _lib.check(_lib.load().bgl_cache_export(self.handle, dev_slots.ctypes.data, dev_tails.ctypes.data,
+                                                host_slots.ctypes.data, host_tail.ctypes.data))
+        return dev_slots, dev_tails, host_slots, int(host_tail[0])
+
+
+class FifoLevelView:
+    """Read-only view of one ring with the FifoLevel attributes the reference
+    exposes (`capacity`, `slots`, `tail`, `__contains__`, `__len__`,
+    cachesim.py:267-293). Reading synchronises with the device."""
+
+    def __init__(self, state: "CacheEngineState", level: int):
+        self._state = state
+        self._level = level
+
+    def _snap(self):
+        dev_slots, dev_tails, host_slots, host_tail = self._state.engine.export()
+        if self._level < 0:
+            return host_slots, host_tail
+        return dev_slots[self._level], int(dev_tails[self._level])
+
+    @property
+    def capacity(self) -> int:
+        c = self._state.cfg
+        return c.host_capacity if self._level < 0 else c.device_capacity
+
+    @property
+    def slots(self) -> np.ndarray:
+        return self._snap()[0]
+
+    @property
+    def tail(self) -> int:
+        return self._snap()[1]
+
+    @property
+    def residency(self) -> dict[int, int]:
+        s = self.slots
+        return {int(v): i for i, v in enumerate(s) if v >= 0}
+
+    def __contains__(self, node) -> bool:
+        return bool(np.any(self.slots == int(node)))
+
+    def __len__(self) -> int:
+        return int(np.count_nonzero(self.slots >= 0))
+
+
+@dataclass
+class CacheEngineState:
+    """Device-resident cache state (the reference's CacheEngineState,
+    cachesim.py:376-380); `devices[h]` / `host` are views of the rings."""
+
+    cfg: CacheConfig
+    engine: FifoCacheDevice
+    policy: str = "fifo"
+
+    @property
+    def devices(self) -> list[FifoLevelView]:
+        return [FifoLevelView(self, h) for h in range(self.cfg.num_devices)]
+
+    @property
+    def host(self) -> FifoLevelView:
+        return FifoLevelView(self, -1)
+
+
+def cold_state(cfg: CacheConfig, num_nodes: int = 1, row_bytes: int = 0) -> CacheEngineState:
+    """Empty caches (cachesim.py:383-389). The index grows on demand."""
+    if cfg.policy == "static-degree":
+        raise ValueError("static policy requires warm_static(g, cfg)")
+    if cfg.policy != "fifo":
+        raise _not_on_device(cfg.policy)
+    return CacheEngineState(cfg=cfg, engine=FifoCacheDevice(cfg, num_nodes, row_bytes), policy="fifo")
+
+
+def warm_static(g, cfg: CacheConfig):
+    if cfg.policy != "static-degree":
+        raise ValueError("warm_static requires policy='static-degree'")
+    raise _not_on_device(cfg.policy)
+
+
+@dataclass
+class CacheSimReport:
+    num_devices: int
+    feature_bytes_per_node: int
+    batch_queries: list[int] = field(default_factory=list)
+    batch_own_hits: list[int] = field(default_factory=list)
+    batch_peer_hits: list[int] = field(default_factory=list)
+    batch_host_hits: list[int] = field(default_factory=list)
+    batch_misses: list[int] = field(default_factory=list)
+    batch_insertions: list[int] = field(default_factory=list)
+    batch_evictions: list[int] = field(default_factory=list)
+    batch_metadata_updates: list[int] = field(default_factory=list)
+    outcomes: list[list[str]] | None = None
+
+    @property
+    def total_queries(self) -> int:
+        return sum(self.batch_queries)
+
+    @property
+    def device_hits(self) -> int:
+        return sum(self.batch_own_hits) + sum(self.batch_peer_hits)
+
+    @property
+    def host_hits(self) -> int:
+        return sum(self.batch_host_hits)
+
+    @property
+    def misses(self) -> int:
+        return sum(self.batch_misses)
+
+    @property
+    def hit_ratio(self) -> float:
+        total = self.total_queries
+        return (self.device_hits + self.host_hits) / total if total else 0.0
+
+    @property
+    def peer_bytes(self) -> int:
+        return sum(self.batch_peer_hits) * self.feature_bytes_per_node
+
+    @property
+    def host_to_device_bytes(self) -> int:
+        return sum(self.batch_host_hits) * self.feature_bytes_per_node
+
+    @property
+    def remote_fetch_bytes(self) -> int:
+        return sum(self.batch_misses) * self.feature_bytes_per_node
+
+    @classmethod
+    def from_counters(cls, cfg: CacheConfig, counters: np.ndarray, codes=None) -> "CacheSimReport":
+        c = np.asarray(counters, dtype=np.int64).reshape(-1, 8)
+        rep = cls(num_devices=cfg.num_devices, feature_bytes_per_node=cfg.feature_bytes_per_node,
+                  batch_queries=c[:, 0].tolist(), batch_own_hits=c[:, 1].tolist(),
+                  batch_peer_hits=c[:, 2].tolist(), batch_host_hits=c[:, 3].tolist(),
+                  batch_misses=c[:, 4].tolist(), batch_insertions=c[:, 5].tolist(),
+                  batch_evictions=c[:, 6].tolist(), batch_metadata_updates=c[:, 7].tolist())
+        if codes is not None:
+            lut = np.array(list(CODE_CHARS))
+            rep.outcomes = [lut[cd].tolist() for cd in codes]
+        return rep
+
+
+class _UniqueScratch:
+    """Bitmap workspace for building sorted distinct insert lists of
+    arbitrary (unsorted / duplicated) batches on the device."""
+
+    def __init__(self, num_nodes: int, max_batch: int):
+        lib = _lib.load()
+        self.n = num_nodes
+        self.ws = torch.empty(int(lib.bgl_unique_workspace(num_nodes)), dtype=torch.uint8, device="cuda")
+        _lib.call("bgl_unique_workspace_init", self.ws.data_ptr(), num_nodes, _lib.stream_ptr())
+        self.uniq = torch.empty(max(max_batch, 1), dtype=torch.int32, device="cuda")
+        self.count = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+
+def simulate(trace, cfg: CacheConfig, g=None, batch_devices=None, state: CacheEngineState | None = None,
+             record_outcomes: bool = False) -> CacheSimReport:
+    """Replay an access trace through the two-level multi-device cache
+    (cachesim.py:461-549)."""
+    if cfg.policy == "static-degree":
+        if state is None and g is None:
+            raise ValueError("static policy needs the graph for degree warmup")
+        if state is not None and state.policy != "static-degree":
+            raise ValueError("state/policy mismatch")
+        raise _not_on_device(cfg.policy)
+    if state is not None and state.policy != cfg.policy:
+        raise ValueError("state/policy mismatch")
+    if cfg.policy != "fifo":
+        raise _not_on_device(cfg.policy)
+
+    batches = [np.asarray(b, dtype=np.int64).ravel() for b in trace.batches]
+    nb = len(batches)
+    d = cfg.num_devices
+    sizes = np.array([b.size for b in batches], dtype=np.int64)
+    flat = np.concatenate(batches) if nb else np.empty(0, np.int64)
+    if flat.size and flat.min() < 0:
+        raise ValueError("node IDs must be >= 0")
+    num_nodes = int(flat.max()) + 1 if flat.size else 1
+    if state is None:
+        state = cold_state(cfg, num_nodes)
+    eng = state.engine
+    maxb = int(sizes.max()) if nb else 0
+    eng.reserve(num_nodes, maxb)
+    counters = torch.zeros((max(nb, 1), 8), dtype=torch.int64, device="cuda")
+    if nb == 0:
+        return CacheSimReport.from_counters(cfg, np.zeros((0, 8)))
+
+    lib = _lib.load()
+    st = _lib.stream_ptr()
+    ids = torch.from_numpy(flat.astype(np.int32)).cuda()
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    # device-side batch lengths (the ABI takes counts on the device)
+    lens = torch.from_numpy(sizes).cuda()
+    codes = torch.empty(max(flat.size, 1), dtype=torch.uint8, device="cuda") if record_outcomes else None
+    scratch = _UniqueScratch(eng.num_nodes, maxb)
+    seg_off = _lib.c_i64 * 1
+    c_off = seg_off(0)
+    for i in range(nb):
+        worker = int(batch_devices[i]) if batch_devices is not None else i % d
+        if not 0 <= worker < d:
+            raise ValueError("worker device out of range")
+        n = int(sizes[i])
+        bptr = ids.data_ptr() + 4 * int(offs[i])
+        nptr = lens.data_ptr() + 8 * i
+        cptr = counters.data_ptr() + 64 * i
+        # sorted distinct set of the batch = the insert order (cachesim.py:527-530)
+        _lib.check(lib.bgl_unique_sorted(bptr, 1, c_off, nptr, (_lib.c_i64 * 1)(n), eng.num_nodes,
+                                         scratch.ws.data_ptr(), scratch.uniq.data_ptr(),
+                                         scratch.count.data_ptr(), st))
+        _lib.check(lib.bgl_cache_lookup(eng.handle, bptr, nptr, n, worker, scratch.uniq.data_ptr(),
+                                        scratch.count.data_ptr(), n,
+                                        None if codes is None else codes.data_ptr() + int(offs[i]),
+                                        None, cptr, st))
+        _lib.check(lib.bgl_cache_insert(eng.handle, scratch.uniq.data_ptr(), n, None, cptr, st))
+        _lib.check(lib.bgl_unique_reset(scratch.ws.data_ptr(), eng.num_nodes, scratch.uniq.data_ptr(),
+                                        scratch.count.data_ptr(), n, st))
+    host_counters = counters[:nb].cpu().numpy()
+    host_codes = None
+    if record_outcomes:
+        cc = codes.cpu().numpy()
+        host_codes = [cc[offs[i]:offs[i + 1]] for i in range(nb)]
+    return CacheSimReport.from_counters(cfg, host_counters, host_codes)
+
+
+def amortized_update_ops(report: CacheSimReport) -> dict[str, float]:
+    """Per-batch mean operation counts (cachesim.py:552-561)."""
+    nb = max(1, len(report.batch_queries))
+    return {
+        "lookups_per_batch": report.total_queries / nb,
+        "insertions_per_batch": sum(report.batch_insertions) / nb,
+        "evictions_per_batch": sum(report.batch_evictions) / nb,
+        "metadata_updates_per_batch": sum(report.batch_metadata_updates) / nb,
+    }
+
+
+def compare_policies(g, trace, capacities, policies=("fifo",), num_devices: int = 1, host_capacity: int = 0,
+                     feature_bytes_per_node: int = 512) -> list[dict]:
+    """Hit-ratio table over a (policy x capacity) sweep (cachesim.py:564-595).
+    Only the FIFO cells run on the device; the default sweeps FIFO only."""
+    rows = []
+    for policy in policies:
+        for cap in capacities:
+            cfg = CacheConfig(device_capacity=cap, host_capacity=host_capacity, num_devices=num_devices,
+                              policy=policy, feature_bytes_per_node=feature_bytes_per_node)
+            rep = simulate(trace, cfg, g=g)
+            rows.append({"policy": policy, "capacity": cap, "hit_ratio": rep.hit_ratio,
+                         "device_hits": rep.device_hits, "host_hits": rep.host_hits, "misses": rep.misses})
+    return rows

@@ -1,0 +1,451 @@
+// K3/K4: BGL's dynamic FIFO feature cache, bit-exact with gnnio.cachesim's
+// FIFO policy (FifoLevel cachesim.py:267-293; simulate cachesim.py:461-549).
+//
+// State (all device-resident):
+//   rings   int32 [d][C]   node in each slot, -1 empty   (FifoLevel.slots)
+//   hring   int32 [Ch]     shared host level
+//   slot_of int32 [n]      slot of v in ring v % d, -1 absent (the paper's
+//                          "contiguous 1D array as a hashmap")
+//   hslot_of int32 [n]     slot in the host ring
+//   tails   int64 [d+1]    next insertion slot per level
+//   rows    [d*C][row_bytes] feature rows of the device rings
+//
+// One batch = lookup (classify every query against the pre-batch state)
+// -> the caller gathers rows -> insert. The insert is the exact batch-
+// parallel closed form of the sequential ring: with tail t
+// and ascending miss list m_0..m_{M-1}, m_j lands in slot (t+j) % C and only
+// j >= M-C survive; evictions = #occupied among the first min(M, C) slots +
+// max(0, M-C); tail <- (t+M) % C. It is computed slot-centrically (one warp
+// per touched slot), so no two writers ever race.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+struct bgl_cache {
+    int64_t n = 0;          // node-ID space of the index
+    int32_t d = 1;
+    int64_t C = 0, Ch = 0, rb = 0;
+    int32_t* slot_of = nullptr;
+    int32_t* hslot_of = nullptr;
+    int32_t* rings = nullptr;
+    int32_t* hring = nullptr;
+    int64_t* tails = nullptr;     // [d+1]
+    int64_t* mcount = nullptr;    // [d+1] misses per level in the current batch
+    unsigned char* rows = nullptr;
+    int32_t* lists = nullptr;     // [(d+1)][list_cap] positions into sorted_ids
+    int64_t list_cap = 0;
+    int64_t* tile_counts = nullptr;   // [max_tiles][d+1] (exclusive offsets after scan)
+    int64_t max_tiles = 0;
+};
+
+namespace bgl {
+
+constexpr int kCThreads = 256;
+constexpr int kCRounds = 4;
+constexpr int kCTile = kCThreads * kCRounds;
+constexpr int kMaxLevels = 65;   // d <= 64 plus the host level
+
+enum : uint8_t { kD = 0, kP = 1, kH = 2, kM = 3 };
+
+__global__ void lookup_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ n_dev, int32_t worker,
+                              int32_t d, int64_t C, const int32_t* __restrict__ slot_of,
+                              const int32_t* __restrict__ hslot_of, uint8_t* __restrict__ codes,
+                              int64_t* __restrict__ src_row, int64_t* __restrict__ counters) {
+    const int64_t n = *n_dev;
+    int64_t c[4] = {0, 0, 0, 0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = ids[i];
+        const int32_t h = v % d;
+        const int32_t s = slot_of[v];
+        uint8_t code;
+        int64_t src = -1;
+        if (s >= 0) {
+            code = (h == worker) ? kD : kP;
+            src = (int64_t)h * C + s;
+        } else if (hslot_of != nullptr && hslot_of[v] >= 0) {
+            code = kH;
+        } else {
+            code = kM;
+        }
+        c[code]++;
+        if (codes) codes[i] = code;
+        if (src_row) src_row[i] = src;
+    }
+    __shared__ int64_t s_c[4];
+    if (threadIdx.x < 4) s_c[threadIdx.x] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        int64_t w = warp_sum_i64(c[k]);
+        if (lane_id() == 0 && w) atomicAdd((unsigned long long*)&s_c[k], (unsigned long long)w);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        atomicAdd((unsigned long long*)&counters[0], (unsigned long long)(s_c[0] + s_c[1] + s_c[2] + s_c[3]));
+    }
+    if (threadIdx.x < 4 && s_c[threadIdx.x])
+        atomicAdd((unsigned long long*)&counters[1 + threadIdx.x], (unsigned long long)s_c[threadIdx.x]);
+}
+
+// level of a sorted id: shard (dev-missed) and whether it is a full miss
+__device__ __forceinline__ void classify(int32_t v, int32_t d, const int32_t* slot_of, const int32_t* hslot_of,
+                                         int* shard, bool* full) {
+    *shard = -1;
+    *full = false;
+    if (slot_of[v] < 0) {
+        *shard = v % d;
+        *full = (hslot_of == nullptr) || (hslot_of[v] < 0);
+    }
+}
+
+__global__ void __launch_bounds__(kCThreads)
+miss_count_kernel(const int32_t* __restrict__ sorted_ids, const int64_t* __restrict__ n_dev, int32_t d,
+                  const int32_t* __restrict__ slot_of, const int32_t* __restrict__ hslot_of,
+                  int64_t* __restrict__ tile_counts) {
+    __shared__ int64_t s_cnt[kMaxLevels];
+    const int64_t n = *n_dev;
+    const int64_t tile = blockIdx.x;
+    for (int y = threadIdx.x; y <= d; y += blockDim.x) s_cnt[y] = 0;
+    __syncthreads();
+    if (tile * kCTile < n) {
+        for (int r = 0; r < kCRounds; ++r) {
+            int64_t e = tile * kCTile + r * kCThreads + threadIdx.x;
+            if (e < n) {
+                int sh;
+                bool full;
+                classify(sorted_ids[e], d, slot_of, hslot_of, &sh, &full);
+                if (sh >= 0) atomicAdd((unsigned long long*)&s_cnt[sh], 1ull);
+                if (full) atomicAdd((unsigned long long*)&s_cnt[d], 1ull);
+            }
+        }
+    }
+    __syncthreads();
+    for (int y = threadIdx.x; y <= d; y += blockDim.x) tile_counts[tile * (d + 1) + y] = s_cnt[y];
+}
+
+// one block: exclusive scan of tile_counts per level, totals -> mcount
+__global__ void miss_scan_kernel(int64_t* __restrict__ tile_counts, int64_t ntiles, int32_t d,
+                                 int64_t* __restrict__ mcount) {
+    __shared__ int64_t s_red[kCThreads / 32 + 1];
+    for (int y = 0; y <= d; ++y) {
+        int64_t carry = 0;
+        for (int64_t b = 0; b < ntiles; b += blockDim.x) {
+            int64_t t = b + threadIdx.x;
+            int64_t v = t < ntiles ? tile_counts[t * (d + 1) + y] : 0;
+            int64_t tot;
+            int64_t ex = block_excl_scan(v, s_red, &tot);
+            if (t < ntiles) tile_counts[t * (d + 1) + y] = carry + ex;
+            carry += tot;
+        }
+        if (threadIdx.x == 0) mcount[y] = carry;
+    }
+}
+
+__global__ void __launch_bounds__(kCThreads)
+miss_scatter_kernel(const int32_t* __restrict__ sorted_ids, const int64_t* __restrict__ n_dev, int32_t d,
+                    const int32_t* __restrict__ slot_of, const int32_t* __restrict__ hslot_of,
+                    const int64_t* __restrict__ tile_off, int32_t* __restrict__ lists, int64_t list_cap) {
+    constexpr int NW = kCThreads / 32;
+    __shared__ int32_t s_w[NW][kMaxLevels];
+    __shared__ int64_t s_run[kMaxLevels];
+    const int64_t n = *n_dev;
+    const int64_t tile = blockIdx.x;
+    if (tile * kCTile >= n) return;
+    const int lane = lane_id(), wid = warp_id();
+    const unsigned lt = (1u << lane) - 1u;
+    for (int y = threadIdx.x; y <= d; y += blockDim.x) s_run[y] = tile_off[tile * (d + 1) + y];
+    __syncthreads();
+    for (int r = 0; r < kCRounds; ++r) {
+        int64_t e = tile * kCTile + r * kCThreads + threadIdx.x;
+        int sh = -1;
+        bool full = false;
+        if (e < n) classify(sorted_ids[e], d, slot_of, hslot_of, &sh, &full);
+        int my_rank_sh = 0, my_rank_h = 0;
+        for (int y = 0; y < d; ++y) {
+            unsigned m = __ballot_sync(0xffffffffu, sh == y);
+            if (sh == y) my_rank_sh = __popc(m & lt);
+            if (lane == 0) s_w[wid][y] = __popc(m);
+        }
+        {
+            unsigned m = __ballot_sync(0xffffffffu, full);
+            if (full) my_rank_h = __popc(m & lt);
+            if (lane == 0) s_w[wid][d] = __popc(m);
+        }
+        __syncthreads();
+        if (sh >= 0) {
+            int64_t pos = s_run[sh] + my_rank_sh;
+            for (int w = 0; w < wid; ++w) pos += s_w[w][sh];
+            lists[(int64_t)sh * list_cap + pos] = (int32_t)e;
+        }
+        if (full) {
+            int64_t pos = s_run[d] + my_rank_h;
+            for (int w = 0; w < wid; ++w) pos += s_w[w][d];
+            lists[(int64_t)d * list_cap + pos] = (int32_t)e;
+        }
+        __syncthreads();
+        for (int y = threadIdx.x; y <= d; y += blockDim.x) {
+            int64_t add = 0;
+            for (int w = 0; w < NW; ++w) add += s_w[w][y];
+            s_run[y] += add;
+        }
+        __syncthreads();
+    }
+}
+
+// warp per touched slot r of level y (= blockIdx.y; y == d is the host ring)
+__global__ void insert_kernel(const int32_t* __restrict__ sorted_ids, int32_t d, int64_t C, int64_t Ch,
+                              int32_t* __restrict__ rings, int32_t* __restrict__ hring, int32_t* __restrict__ slot_of,
+                              int32_t* __restrict__ hslot_of, const int64_t* __restrict__ tails,
+                              const int64_t* __restrict__ mcount, const int32_t* __restrict__ lists, int64_t list_cap,
+                              const unsigned char* __restrict__ batch_rows, unsigned char* __restrict__ rows,
+                              int64_t rb, int64_t* __restrict__ counters) {
+    const int y = blockIdx.y;
+    const bool host = (y == d);
+    const int64_t cap = host ? Ch : C;
+    if (cap == 0) return;
+    const int64_t M = mcount[y];
+    const int64_t lim = M < cap ? M : cap;
+    const int64_t t0 = tails[y];
+    int32_t* ring = host ? hring : rings + (int64_t)y * C;
+    int32_t* index = host ? hslot_of : slot_of;
+    const int32_t* list = lists + (int64_t)y * list_cap;
+    const int lane = lane_id();
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int64_t ev = 0;
+    for (int64_t r = gw; r < lim; r += nw) {
+        const int64_t slot = (t0 + r) % cap;
+        const int64_t j = r + cap * ((M - 1 - r) / cap);   // last miss landing in this slot
+        const int32_t pos = list[j];
+        const int32_t v = sorted_ids[pos];
+        if (lane == 0) {
+            const int32_t old = ring[slot];
+            if (old >= 0) {
+                index[old] = -1;
+                ++ev;
+            }
+            ring[slot] = v;
+            index[v] = (int32_t)slot;
+        }
+        if (!host && batch_rows != nullptr) {
+            const unsigned char* src = batch_rows + (int64_t)pos * rb;
+            unsigned char* dst = rows + ((int64_t)y * C + slot) * rb;
+            if ((rb & 15) == 0) {
+                for (int64_t b = (int64_t)lane * 16; b < rb; b += 32 * 16)
+                    *reinterpret_cast<uint4*>(dst + b) = __ldg(reinterpret_cast<const uint4*>(src + b));
+            } else {
+                for (int64_t b = (int64_t)lane * 4; b < rb; b += 32 * 4)
+                    *reinterpret_cast<uint32_t*>(dst + b) = __ldg(reinterpret_cast<const uint32_t*>(src + b));
+            }
+        }
+    }
+    if (lane == 0 && ev) atomicAdd((unsigned long long*)&counters[6], (unsigned long long)ev);
+}
+
+__global__ void insert_finalize_kernel(int32_t d, int64_t C, int64_t Ch, int64_t* __restrict__ tails,
+                                       const int64_t* __restrict__ mcount, int64_t* __restrict__ counters) {
+    if (threadIdx.x != 0) return;
+    int64_t ins = 0, ev = 0;
+    for (int y = 0; y <= d; ++y) {
+        const int64_t cap = (y == d) ? Ch : C;
+        if (cap == 0) continue;
+        const int64_t M = mcount[y];
+        tails[y] = (tails[y] + M) % cap;
+        ins += M;
+        ev += M > cap ? M - cap : 0;
+    }
+    counters[5] += ins;
+    counters[6] += ev;
+}
+
+}  // namespace bgl
+
+using namespace bgl;
+
+namespace {
+
+int alloc_fill(void** p, size_t bytes, int byte, const char* what) {
+    if (bytes == 0) {
+        *p = nullptr;
+        return BGL_OK;
+    }
+    BGL_TRY(cuda_status(cudaMalloc(p, bytes), what));
+    return cuda_status(cudaMemset(*p, byte, bytes), what);
+}
+
+void free_cache(bgl_cache* c) {
+    cudaFree(c->slot_of);
+    cudaFree(c->hslot_of);
+    cudaFree(c->rings);
+    cudaFree(c->hring);
+    cudaFree(c->tails);
+    cudaFree(c->mcount);
+    cudaFree(c->rows);
+    cudaFree(c->lists);
+    cudaFree(c->tile_counts);
+}
+
+}  // namespace
+
+extern "C" {
+
+int bgl_cache_create(int64_t num_nodes, int32_t num_shards, int64_t shard_capacity, int64_t host_capacity,
+                     int64_t row_bytes, bgl_cache_t* out) {
+    BGL_CHECK_ARG(out, "bgl_cache_create: null out");
+    BGL_CHECK_ARG(num_shards >= 1 && num_shards <= kMaxLevels - 1, "num_devices must be in [1, 64]");
+    BGL_CHECK_ARG(shard_capacity >= 0 && host_capacity >= 0, "capacities must be >= 0");
+    BGL_CHECK_ARG(shard_capacity < (1ll << 31) && host_capacity < (1ll << 31), "capacity must be < 2^31");
+    BGL_CHECK_ARG(num_nodes >= 1 && num_nodes < (1ll << 31), "num_nodes must be in [1, 2^31)");
+    BGL_CHECK_ARG(row_bytes >= 0 && row_bytes % 4 == 0, "row_bytes must be a multiple of 4");
+    bgl_cache* c = new bgl_cache();
+    c->n = num_nodes;
+    c->d = num_shards;
+    c->C = shard_capacity;
+    c->Ch = host_capacity;
+    c->rb = row_bytes;
+    int st = BGL_OK;
+    do {
+        if ((st = alloc_fill((void**)&c->slot_of, num_nodes * 4, 0xFF, "cache index")) != BGL_OK) break;
+        if (host_capacity > 0 &&
+            (st = alloc_fill((void**)&c->hslot_of, num_nodes * 4, 0xFF, "cache host index")) != BGL_OK) break;
+        if ((st = alloc_fill((void**)&c->rings, (size_t)num_shards * shard_capacity * 4, 0xFF, "cache rings")) != BGL_OK) break;
+        if ((st = alloc_fill((void**)&c->hring, (size_t)host_capacity * 4, 0xFF, "cache host ring")) != BGL_OK) break;
+        if ((st = alloc_fill((void**)&c->tails, (size_t)(num_shards + 1) * 8, 0, "cache tails")) != BGL_OK) break;
+        if ((st = alloc_fill((void**)&c->mcount, (size_t)(num_shards + 1) * 8, 0, "cache mcount")) != BGL_OK) break;
+        if (row_bytes > 0 &&
+            (st = alloc_fill((void**)&c->rows, (size_t)num_shards * shard_capacity * row_bytes, 0, "cache rows")) != BGL_OK)
+            break;
+    } while (0);
+    if (st != BGL_OK) {
+        free_cache(c);
+        delete c;
+        return st;
+    }
+    *out = c;
+    return BGL_OK;
+}
+
+int bgl_cache_destroy(bgl_cache_t c) {
+    if (!c) return BGL_OK;
+    free_cache(c);
+    delete c;
+    return BGL_OK;
+}
+
+void* bgl_cache_rows(bgl_cache_t c) { return c ? c->rows : nullptr; }
+
+int bgl_cache_reserve_nodes(bgl_cache_t c, int64_t num_nodes, void* stream) {
+    BGL_CHECK_ARG(c, "null cache");
+    BGL_CHECK_ARG(num_nodes < (1ll << 31), "num_nodes must be < 2^31");
+    if (num_nodes <= c->n) return BGL_OK;
+    cudaStream_t st = as_stream(stream);
+    BGL_TRY(cuda_status(cudaStreamSynchronize(st), "reserve sync"));
+    int32_t* arrs[2] = {c->slot_of, c->hslot_of};
+    for (int a = 0; a < 2; ++a) {
+        if (!arrs[a]) continue;
+        int32_t* nw = nullptr;
+        BGL_TRY(alloc_fill((void**)&nw, num_nodes * 4, 0xFF, "cache index grow"));
+        BGL_TRY(cuda_status(cudaMemcpy(nw, arrs[a], c->n * 4, cudaMemcpyDeviceToDevice), "cache index copy"));
+        cudaFree(arrs[a]);
+        arrs[a] = nw;
+    }
+    c->slot_of = arrs[0];
+    c->hslot_of = arrs[1];
+    c->n = num_nodes;
+    return BGL_OK;
+}
+
+int bgl_cache_reserve_batch(bgl_cache_t c, int64_t max_batch) {
+    BGL_CHECK_ARG(c, "null cache");
+    if (max_batch <= c->list_cap) return BGL_OK;
+    BGL_TRY(cuda_status(cudaDeviceSynchronize(), "reserve batch sync"));
+    cudaFree(c->lists);
+    cudaFree(c->tile_counts);
+    c->lists = nullptr;
+    c->tile_counts = nullptr;
+    int64_t cap = std::max<int64_t>(max_batch, 1024);
+    c->max_tiles = ceil_div(cap, kCTile);
+    BGL_TRY(cuda_status(cudaMalloc((void**)&c->lists, (size_t)(c->d + 1) * cap * 4), "cache lists"));
+    BGL_TRY(cuda_status(cudaMalloc((void**)&c->tile_counts, (size_t)(c->d + 1) * c->max_tiles * 8), "cache tiles"));
+    c->list_cap = cap;
+    return BGL_OK;
+}
+
+int bgl_cache_reset(bgl_cache_t c, void* stream) {
+    BGL_CHECK_ARG(c, "null cache");
+    cudaStream_t st = as_stream(stream);
+    BGL_TRY(cuda_status(cudaMemsetAsync(c->slot_of, 0xFF, c->n * 4, st), "reset"));
+    if (c->hslot_of) BGL_TRY(cuda_status(cudaMemsetAsync(c->hslot_of, 0xFF, c->n * 4, st), "reset"));
+    if (c->rings) BGL_TRY(cuda_status(cudaMemsetAsync(c->rings, 0xFF, (size_t)c->d * c->C * 4, st), "reset"));
+    if (c->hring) BGL_TRY(cuda_status(cudaMemsetAsync(c->hring, 0xFF, (size_t)c->Ch * 4, st), "reset"));
+    return cuda_status(cudaMemsetAsync(c->tails, 0, (size_t)(c->d + 1) * 8, st), "reset");
+}
+
+int bgl_cache_lookup(bgl_cache_t c, const int32_t* ids, const int64_t* n_dev, int64_t max_n, int32_t worker,
+                     const int32_t* sorted_ids, const int64_t* n_sorted_dev, int64_t max_sorted, uint8_t* codes,
+                     int64_t* src_row, int64_t* counters, void* stream) {
+    BGL_CHECK_ARG(c && ids && n_dev && sorted_ids && n_sorted_dev && counters, "bgl_cache_lookup: null pointer");
+    BGL_CHECK_ARG(worker >= 0 && worker < c->d, "worker device out of range");
+    BGL_CHECK_ARG(max_sorted <= c->list_cap, "batch larger than reserved (call bgl_cache_reserve_batch)");
+    cudaStream_t st = as_stream(stream);
+    if (max_n > 0) {
+        lookup_kernel<<<grid_for(max_n, 256), 256, 0, st>>>(ids, n_dev, worker, c->d, c->C, c->slot_of, c->hslot_of,
+                                                            codes, src_row, counters);
+        BGL_TRY(launch_status("lookup_kernel"));
+    }
+    const int64_t ntiles = std::max<int64_t>(1, ceil_div(max_sorted, kCTile));
+    miss_count_kernel<<<(unsigned)ntiles, kCThreads, 0, st>>>(sorted_ids, n_sorted_dev, c->d, c->slot_of,
+                                                              c->hslot_of, c->tile_counts);
+    BGL_TRY(launch_status("miss_count_kernel"));
+    miss_scan_kernel<<<1, kCThreads, 0, st>>>(c->tile_counts, ntiles, c->d, c->mcount);
+    BGL_TRY(launch_status("miss_scan_kernel"));
+    miss_scatter_kernel<<<(unsigned)ntiles, kCThreads, 0, st>>>(sorted_ids, n_sorted_dev, c->d, c->slot_of,
+                                                                c->hslot_of, c->tile_counts, c->lists, c->list_cap);
+    return launch_status("miss_scatter_kernel");
+}
+
+int bgl_cache_insert(bgl_cache_t c, const int32_t* sorted_ids, int64_t max_sorted, const void* batch_rows,
+                     int64_t* counters, void* stream) {
+    BGL_CHECK_ARG(c && sorted_ids && counters, "bgl_cache_insert: null pointer");
+    BGL_CHECK_ARG(batch_rows == nullptr || c->rb > 0, "cache was created without feature rows");
+    cudaStream_t st = as_stream(stream);
+    const int64_t cap = std::max(c->C, c->Ch);
+    const int64_t work = std::min<int64_t>(max_sorted, cap);
+    if (work > 0) {
+        const int threads = 256;
+        unsigned gx = grid_for(work * 32, threads, 8);
+        dim3 grid(gx, c->d + 1);
+        insert_kernel<<<grid, threads, 0, st>>>(sorted_ids, c->d, c->C, c->Ch, c->rings, c->hring, c->slot_of,
+                                                c->hslot_of, c->tails, c->mcount, c->lists, c->list_cap,
+                                                (const unsigned char*)batch_rows, c->rows, c->rb, counters);
+        BGL_TRY(launch_status("insert_kernel"));
+    }
+    insert_finalize_kernel<<<1, 32, 0, st>>>(c->d, c->C, c->Ch, c->tails, c->mcount, counters);
+    return launch_status("insert_finalize_kernel");
+}
+
+int bgl_cache_export(bgl_cache_t c, int64_t* dev_slots_host, int64_t* dev_tails_host, int64_t* host_slots_host,
+                     int64_t* host_tail_host) {
+    BGL_CHECK_ARG(c, "null cache");
+    BGL_TRY(cuda_status(cudaDeviceSynchronize(), "export sync"));
+    std::vector<int32_t> tmp;
+    if (dev_slots_host && c->C > 0) {
+        tmp.resize((size_t)c->d * c->C);
+        BGL_TRY(cuda_status(cudaMemcpy(tmp.data(), c->rings, tmp.size() * 4, cudaMemcpyDeviceToHost), "export"));
+        for (size_t i = 0; i < tmp.size(); ++i) dev_slots_host[i] = tmp[i];
+    }
+    std::vector<int64_t> tails(c->d + 1);
+    BGL_TRY(cuda_status(cudaMemcpy(tails.data(), c->tails, tails.size() * 8, cudaMemcpyDeviceToHost), "export"));
+    if (dev_tails_host)
+        for (int i = 0; i < c->d; ++i) dev_tails_host[i] = tails[i];
+    if (host_tail_host) *host_tail_host = tails[c->d];
+    if (host_slots_host && c->Ch > 0) {
+        tmp.resize((size_t)c->Ch);
+        BGL_TRY(cuda_status(cudaMemcpy(tmp.data(), c->hring, tmp.size() * 4, cudaMemcpyDeviceToHost), "export"));
+        for (size_t i = 0; i < tmp.size(); ++i) host_slots_host[i] = tmp[i];
+    }
+    return BGL_OK;
+}
+
+}  // extern "C"

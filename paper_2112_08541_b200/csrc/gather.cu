@@ -1,0 +1,143 @@
+// K5/K6: feature-row gather for a mini-batch (net-new: the reference only
+// counts bytes, cachesim.py:447-458; contract rows[i] = F[batch[i]]).
+//
+// out[i] = src_row[i] >= 0 ? ring_rows[src_row[i]]   (cache hit, HBM)
+//                          : table[ids[i]]            (miss: zero-copy read of
+//                                                      pinned host memory over
+//                                                      the host link, or HBM)
+// 16-byte vector moves, every thread keeps kUnroll independent loads in
+// flight (the host link needs ~bandwidth x latency bytes outstanding), rows
+// flattened into a chunk index space so a 400-byte row (25 chunks) does not
+// strand lanes.
+#include "common.cuh"
+
+namespace bgl {
+
+constexpr int kGThreads = 256;
+constexpr int kUnroll = 4;
+
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ void st_na_v4(void* p, const uint4& v) {
+    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+
+__device__ __forceinline__ const unsigned char* row_src(int64_t row, const int32_t* ids, const int64_t* src_row,
+                                                        const unsigned char* ring, const unsigned char* table,
+                                                        int64_t rb) {
+    int64_t s = src_row ? __ldg(src_row + row) : -1;
+    return s >= 0 ? ring + s * rb : table + (int64_t)__ldg(ids + row) * rb;
+}
+
+__global__ void __launch_bounds__(kGThreads)
+gather_v4_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ src_row,
+                 const int64_t* __restrict__ n_dev, const unsigned char* __restrict__ ring,
+                 const unsigned char* __restrict__ table, int64_t rb, unsigned char* __restrict__ out) {
+    const int64_t n = *n_dev;
+    const int64_t cpr = rb >> 4;
+    const int64_t total = n * cpr;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t c0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c0 < total; c0 += stride * kUnroll) {
+        uint4 v[kUnroll];
+        int64_t dst[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            int64_t c = c0 + u * stride;
+            dst[u] = -1;
+            if (c < total) {
+                int64_t row = c / cpr;
+                int64_t part = c - row * cpr;
+                v[u] = ld_nc_v4(row_src(row, ids, src_row, ring, table, rb) + part * 16);
+                dst[u] = row * rb + part * 16;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+            if (dst[u] >= 0) st_na_v4(out + dst[u], v[u]);
+    }
+}
+
+__global__ void __launch_bounds__(kGThreads)
+gather_v1_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ src_row,
+                 const int64_t* __restrict__ n_dev, const unsigned char* __restrict__ ring,
+                 const unsigned char* __restrict__ table, int64_t rb, unsigned char* __restrict__ out) {
+    const int64_t n = *n_dev;
+    const int64_t cpr = rb >> 2;
+    const int64_t total = n * cpr;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < total; c += (int64_t)gridDim.x * blockDim.x) {
+        int64_t row = c / cpr;
+        int64_t part = c - row * cpr;
+        const unsigned char* s = row_src(row, ids, src_row, ring, table, rb) + part * 4;
+        *reinterpret_cast<uint32_t*>(out + row * rb + part * 4) = *reinterpret_cast<const uint32_t*>(s);
+    }
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+}
+
+__global__ void synth_kernel(int64_t first, int64_t nrows, int32_t dim, uint64_t seed, float* __restrict__ out) {
+    const int64_t total = nrows * dim;
+    const uint64_t salt = seed * 0xD1B54A32D192ED03ull;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = i / dim;
+        int64_t j = i - r * dim;
+        uint64_t key = ((uint64_t)(first + r) << 20) | (uint64_t)j;
+        uint64_t z = splitmix64(key + salt);
+        out[i] = (float)((double)((z >> 40) & 0xFFFFFFull) * (1.0 / 16777216.0) - 0.5);
+    }
+}
+
+}  // namespace bgl
+
+using namespace bgl;
+
+extern "C" {
+
+int bgl_gather_rows(const int32_t* ids, const int64_t* src_row, const int64_t* n_dev, int64_t max_n,
+                    const void* ring_rows, const void* table, int64_t row_bytes, void* out, void* stream) {
+    BGL_CHECK_ARG(row_bytes > 0 && row_bytes % 4 == 0, "row_bytes must be a positive multiple of 4");
+    BGL_CHECK_ARG(ids && n_dev && table && out, "bgl_gather_rows: null pointer");
+    BGL_CHECK_ARG(src_row == nullptr || ring_rows != nullptr, "bgl_gather_rows: src_row without ring rows");
+    if (max_n <= 0) return BGL_OK;
+    cudaStream_t st = as_stream(stream);
+    const bool v4 = (row_bytes % 16 == 0) && ((uintptr_t)table % 16 == 0) && ((uintptr_t)out % 16 == 0) &&
+                    (ring_rows == nullptr || (uintptr_t)ring_rows % 16 == 0);
+    if (v4) {
+        int64_t chunks = max_n * (row_bytes / 16);
+        unsigned grid = grid_for(ceil_div(chunks, kUnroll), kGThreads, 8);
+        gather_v4_kernel<<<grid, kGThreads, 0, st>>>(ids, src_row, n_dev, (const unsigned char*)ring_rows,
+                                                     (const unsigned char*)table, row_bytes, (unsigned char*)out);
+        return launch_status("gather_v4_kernel");
+    }
+    int64_t chunks = max_n * (row_bytes / 4);
+    gather_v1_kernel<<<grid_for(chunks, kGThreads, 8), kGThreads, 0, st>>>(
+        ids, src_row, n_dev, (const unsigned char*)ring_rows, (const unsigned char*)table, row_bytes,
+        (unsigned char*)out);
+    return launch_status("gather_v1_kernel");
+}
+
+int bgl_synthetic_features(int64_t first_node, int64_t num_nodes, int32_t dim, uint64_t seed, float* out,
+                           void* stream) {
+    BGL_CHECK_ARG(dim >= 1 && dim < (1 << 20), "dim must be in [1, 2^20)");
+    BGL_CHECK_ARG(first_node >= 0 && num_nodes >= 0, "negative range");
+    if (num_nodes == 0) return BGL_OK;
+    synth_kernel<<<grid_for(num_nodes * dim, 256, 16), 256, 0, as_stream(stream)>>>(first_node, num_nodes, dim, seed,
+                                                                                    out);
+    return launch_status("synth_kernel");
+}
+
+}  // extern "C"

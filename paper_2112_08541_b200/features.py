@@ -1,0 +1,115 @@
+"""Feature retrieval through BGL's dynamic FIFO cache (net-new API).
+
+The reference never materialises features (`gnnio/graph.py:3-6`); it counts
+the bytes a batch would move (`cachesim.py:447-458`). This module adds the
+retrieval the paper describes without changing
+`simulate`'s signature: `FeatureCacheEngine.state` is a `CacheEngineState`,
+so `cachesim.simulate(trace, cfg, state=engine.state)` drives the same
+device state, and `retrieve` returns the rows `F[batch]` byte-exactly:
+
+    lookup (pre-batch state) -> gather hits from the HBM ring slots and misses
+    from the feature store (pinned host memory read zero-copy over the host
+    link, or HBM) -> insert-after-batch, copying each surviving miss's row
+    into the slot it lands in.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .cachesim import CacheConfig, CacheEngineState, CacheSimReport, FifoCacheDevice
+
+
+def synthetic_features(num_nodes: int, dim: int, seed: int = 0, pinned: bool = True,
+                       device_resident: bool = False, chunk_rows: int = 1 << 20) -> torch.Tensor:
+    """Deterministic float32 table F[v, j] = hash(v, j, seed) (restated in
+    oracle/features_oracle.py), generated on the GPU chunk by chunk and
+    stored in pinned host memory (or kept in HBM)."""
+    if device_resident:
+        out = torch.empty((num_nodes, dim), dtype=torch.float32, device="cuda")
+        _lib.call("bgl_synthetic_features", 0, num_nodes, dim, seed, out.data_ptr(), _lib.stream_ptr())
+        return out
+    out = torch.empty((num_nodes, dim), dtype=torch.float32, pin_memory=pinned)
+    buf = torch.empty((min(chunk_rows, num_nodes), dim), dtype=torch.float32, device="cuda")
+    for lo in range(0, num_nodes, chunk_rows):
+        hi = min(num_nodes, lo + chunk_rows)
+        _lib.call("bgl_synthetic_features", lo, hi - lo, dim, seed, buf.data_ptr(), _lib.stream_ptr())
+        out[lo:hi].copy_(buf[: hi - lo], non_blocking=False)
+    return out
+
+
+def table_pointer(features: torch.Tensor) -> int:
+    """Device-usable pointer of the feature store (HBM or pinned host)."""
+    if features.is_cuda:
+        return features.data_ptr()
+    if not features.is_pinned():
+        raise ValueError("host feature store must be pinned (zero-copy miss path)")
+    return _lib.host_device_pointer(features)
+
+
+class FeatureCacheEngine:
+    """Per-batch retrieval through the sharded FIFO cache on one device.
+
+    With `cfg.num_devices = d > 1` the d shards are simulated on this GPU
+    (worker of batch i = i % d, as the reference's routing); the multi-GPU
+    engine places shard h on GPU h (see pipeline.py).
+    """
+
+    def __init__(self, cfg: CacheConfig, features: torch.Tensor, max_batch: int):
+        if cfg.policy != "fifo":
+            raise NotImplementedError("only BGL's FIFO cache runs on the device")
+        if features.dim() != 2 or not features.is_contiguous():
+            raise ValueError("features must be a contiguous [num_nodes, dim] tensor")
+        self.cfg = cfg
+        self.features = features
+        self.num_nodes, self.dim = features.shape
+        self.row_bytes = self.dim * features.element_size()
+        self.table = table_pointer(features)
+        self.dev = FifoCacheDevice(cfg, self.num_nodes, self.row_bytes)
+        self.dev.reserve(self.num_nodes, max_batch)
+        self.state = CacheEngineState(cfg=cfg, engine=self.dev, policy="fifo")
+        self.max_batch = int(max_batch)
+        self.codes = torch.empty(max(max_batch, 1), dtype=torch.uint8, device="cuda")
+        self.src_row = torch.empty(max(max_batch, 1), dtype=torch.int64, device="cuda")
+        self.n_dev = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self.out = torch.empty((max(max_batch, 1), self.dim), dtype=features.dtype, device="cuda")
+        self.counters = torch.zeros(8, dtype=torch.int64, device="cuda")
+
+    def retrieve_device(self, ids: torch.Tensor, n_dev: torch.Tensor, max_n: int, worker: int,
+                        counters: torch.Tensor | None = None, stream=None, out: torch.Tensor | None = None):
+        """Fully device-resident step: ids = sorted distinct int32 node IDs
+        (e.g. BatchSampler.uniq) with the live count in n_dev. Rows land in
+        `out` (default self.out) in batch order; codes in self.codes."""
+        lib = _lib.load()
+        st = _lib.stream_ptr(stream)
+        cnt = (self.counters if counters is None else counters).data_ptr()
+        out = self.out if out is None else out
+        h = self.dev.handle
+        _lib.check(lib.bgl_cache_lookup(h, ids.data_ptr(), n_dev.data_ptr(), max_n, worker, ids.data_ptr(),
+                                        n_dev.data_ptr(), max_n, self.codes.data_ptr(), self.src_row.data_ptr(),
+                                        cnt, st))
+        _lib.check(lib.bgl_gather_rows(ids.data_ptr(), self.src_row.data_ptr(), n_dev.data_ptr(), max_n,
+                                       self.dev.rows_ptr() or None, self.table, self.row_bytes, out.data_ptr(), st))
+        _lib.check(lib.bgl_cache_insert(h, ids.data_ptr(), max_n, out.data_ptr(), cnt, st))
+        return out
+
+    def retrieve(self, batch_ids, batch_index: int):
+        """rows = F[batch_ids] for one sorted distinct batch; returns
+        (rows [U, dim] on the device, outcome codes uint8 [U])."""
+        ids = torch.as_tensor(np.asarray(batch_ids, dtype=np.int64) if not isinstance(batch_ids, torch.Tensor)
+                              else batch_ids).to(device="cuda", dtype=torch.int32)
+        n = int(ids.numel())
+        if n > self.max_batch:
+            raise ValueError("batch larger than the engine was sized for")
+        if n > 1 and not bool((ids[1:] > ids[:-1]).all()):
+            raise ValueError("retrieve expects a sorted, duplicate-free batch (an AccessTrace batch)")
+        self.n_dev.fill_(n)
+        worker = batch_index % self.cfg.num_devices
+        self.retrieve_device(ids, self.n_dev, n, worker)
+        return self.out[:n], self.codes[:n]
+
+    def report(self, nbatches: int = 1) -> CacheSimReport:
+        """Cumulative counters as a one-row report."""
+        return CacheSimReport.from_counters(self.cfg, self.counters.cpu().numpy())

@@ -1,0 +1,133 @@
+"""GPU parity: FIFO cache engine and feature gather vs the reference's golden
+vectors and the CPU oracle (bit-exact)."""
+
+import numpy as np
+import pytest
+import torch
+
+from packing import get
+
+from oracle import cache_oracle as co
+from oracle import features_oracle as fo
+
+pytestmark = pytest.mark.gpu
+
+
+def _cases(npz):
+    specs = npz["specs"]
+    batches = get(npz, "batches")
+    codes = get(npz, "codes")
+    dsl = get(npz, "dev_slots")
+    dtl = get(npz, "dev_tails")
+    hsl = get(npz, "host_slots")
+    htl = get(npz, "host_tails")
+    cnt = npz["counters"]
+    b0 = 0
+    for ci, (d, cap, hcap, nb, use_bd, kind) in enumerate(specs):
+        bd = npz[f"bd_{ci}"].tolist() if use_bd else None
+        sl = slice(b0, b0 + nb)
+        yield ci, int(d), int(cap), int(hcap), bd, batches[sl], codes[sl], cnt[sl], dsl[sl], dtl[sl], hsl[sl], htl[ci]
+        b0 += nb
+
+
+def test_fifo_whole_trace_matches_reference(golden):
+    from paper_2112_08541_b200 import cachesim as cs
+    from paper_2112_08541_b200.sampler import AccessTrace
+    npz = golden("cache")
+    for ci, d, cap, hcap, bd, batches, codes, cnt, dsl, dtl, hsl, htl in _cases(npz):
+        cfg = cs.CacheConfig(device_capacity=cap, host_capacity=hcap, num_devices=d, feature_bytes_per_node=400)
+        rep = cs.simulate(AccessTrace(batches=batches), cfg, batch_devices=bd, record_outcomes=True)
+        assert np.array_equal(np.array([rep.batch_queries, rep.batch_own_hits, rep.batch_peer_hits,
+                                        rep.batch_host_hits, rep.batch_misses, rep.batch_insertions,
+                                        rep.batch_evictions, rep.batch_metadata_updates]).T, cnt), ci
+        assert rep.outcomes == [["DPHM"[c] for c in cd] for cd in codes], ci
+
+
+def test_fifo_eviction_order_every_batch(golden):
+    """Ring contents + tail of every level after every batch (state= path)."""
+    from paper_2112_08541_b200 import cachesim as cs
+    from paper_2112_08541_b200.sampler import AccessTrace
+    npz = golden("cache")
+    for ci, d, cap, hcap, bd, batches, codes, cnt, dsl, dtl, hsl, htl in _cases(npz):
+        if ci % 3:
+            continue
+        cfg = cs.CacheConfig(device_capacity=cap, host_capacity=hcap, num_devices=d)
+        state = cs.cold_state(cfg)
+        for i, b in enumerate(batches):
+            cs.simulate(AccessTrace(batches=[b]), cfg, batch_devices=[bd[i] if bd else i % d], state=state)
+            ds, dt, hs, ht = state.engine.export()
+            assert np.array_equal(ds.ravel(), dsl[i]), (ci, i)
+            assert dt.tolist() == dtl[i].tolist()
+            assert np.array_equal(hs, hsl[i])
+            assert ht == htl[i]
+        assert len(state.devices[0]) <= cap
+
+
+def test_fifo_real_trace(golden):
+    from paper_2112_08541_b200 import cachesim as cs
+    from paper_2112_08541_b200.sampler import AccessTrace
+    npz = golden("cache")
+    trace = AccessTrace(batches=get(npz, "real_trace"))
+    for j, d in enumerate((1, 2, 4, 8)):
+        rep = cs.simulate(trace, cs.CacheConfig(device_capacity=500 // d, host_capacity=250, num_devices=d))
+        got = np.array([rep.batch_queries, rep.batch_own_hits, rep.batch_peer_hits, rep.batch_host_hits,
+                        rep.batch_misses, rep.batch_insertions, rep.batch_evictions])
+        assert np.array_equal(got, npz["real_counters"][j])
+
+
+def test_reference_hand_cases():
+    from paper_2112_08541_b200 import cachesim as cs
+    from paper_2112_08541_b200.sampler import AccessTrace
+
+    def tr(*b):
+        return AccessTrace(batches=[np.array(x, dtype=np.int64) for x in b])
+
+    rep = cs.simulate(tr([0, 1], [2], [0]), cs.CacheConfig(device_capacity=2))
+    assert rep.batch_misses == [2, 1, 1] and rep.hit_ratio == 0.0
+    rep = cs.simulate(tr([3], [3]), cs.CacheConfig(device_capacity=4, num_devices=2), batch_devices=[0, 0],
+                      record_outcomes=True)
+    assert rep.outcomes == [["M"], ["P"]]
+    rep = cs.simulate(tr([0, 1], [0, 1], [0, 1]), cs.CacheConfig(device_capacity=1, host_capacity=8),
+                      record_outcomes=True)
+    assert rep.outcomes[0] == ["M", "M"] and rep.misses == 2
+    rep = cs.simulate(tr([0, 1], [2, 0]), cs.CacheConfig(device_capacity=0))
+    assert rep.hit_ratio == 0.0 and rep.misses == 4
+    with pytest.raises(ValueError, match="mismatch"):
+        st = cs.cold_state(cs.CacheConfig(device_capacity=2))
+        st.policy = "lru"
+        cs.simulate(tr([0]), cs.CacheConfig(device_capacity=2), state=st)
+    with pytest.raises(NotImplementedError):
+        cs.simulate(tr([0]), cs.CacheConfig(device_capacity=2, policy="lru"))
+
+
+@pytest.mark.parametrize("where", ["host", "hbm"])
+@pytest.mark.parametrize("d", [1, 4])
+def test_feature_retrieval_bit_exact(where, d):
+    from paper_2112_08541_b200 import cachesim as cs
+    from paper_2112_08541_b200.features import FeatureCacheEngine, synthetic_features
+    n, dim = 20000, 100
+    feats = synthetic_features(n, dim, seed=9, device_resident=(where == "hbm"))
+    ref_table = fo.synthetic_features(np.arange(n), dim, seed=9)
+    assert np.array_equal(feats.cpu().numpy(), ref_table)
+    rng = np.random.default_rng(3)
+    batches = [np.unique(rng.integers(0, 3000 + 1000 * i, size=2500)) for i in range(12)]
+    cfg = cs.CacheConfig(device_capacity=1500 // d, host_capacity=0, num_devices=d, feature_bytes_per_node=400)
+    eng = FeatureCacheEngine(cfg, feats, max_batch=max(len(b) for b in batches))
+    oracle = co.FifoEngine(cfg.device_capacity, 0, d)
+    for i, b in enumerate(batches):
+        rows, codes = eng.retrieve(b, i)
+        assert np.array_equal(rows.cpu().numpy(), ref_table[b]), i
+        _, ocodes = oracle.run([b], [i % d])
+        assert np.array_equal(codes.cpu().numpy(), ocodes[0]), i
+    # the ring rows hold exactly the features of the resident nodes
+    from paper_2112_08541_b200 import _lib
+    ds, _, _, _ = eng.dev.export()
+    flat = ds.ravel()
+    slots = np.flatnonzero(flat >= 0)
+    src = torch.from_numpy(slots.astype(np.int64)).cuda()
+    ids = torch.from_numpy(flat[slots].astype(np.int32)).cuda()
+    nd = torch.tensor([len(slots)], dtype=torch.int64, device="cuda")
+    out = torch.empty((len(slots), dim), dtype=torch.float32, device="cuda")
+    _lib.call("bgl_gather_rows", ids.data_ptr(), src.data_ptr(), nd.data_ptr(), len(slots), eng.dev.rows_ptr(),
+              eng.table, dim * 4, out.data_ptr(), _lib.stream_ptr())
+    assert np.array_equal(out.cpu().numpy(), ref_table[flat[slots]])
