@@ -1,0 +1,419 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native BGL per-mini-batch preprocessing path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl bgl|reference]
+                    [--config c2|c1] [--features host|hbm]
+
+One step = one mini-batch: 3-hop sampling (PCG64 replay) + dedup + FIFO
+cache lookup + feature gather (hits from HBM ring slots, misses zero-copy
+from pinned host memory) + insert-after-batch, on the ogbn-products-shaped
+synthetic graph (BASELINE.json configs[1]). Prints ONE JSON line (rank 0).
+
+`--impl reference` times the reference algorithm on the host CPU (the numpy
+oracle port of gnnio's sampler / FIFO cache + a numpy gather), with all host
+cores used for the sampler (batches are independent).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c2": dict(workload="ogbn-products-shaped synthetic power-law graph (2.4M nodes, ~62M undirected edges), "
+                        "100-d fp32 features in pinned host memory, GraphSAGE fanout [15,10,5], batch 1024, "
+                        "FIFO cache 10% of nodes in HBM, proximity (BFS, S=4) ordering",
+               n=2_400_000, avg_degree=51, dim=100, labels=47, train=0.08, fanouts=(15, 10, 5), b=1024,
+               cache_frac=0.10, S=4),
+    "c1": dict(workload="synthetic power-law graph 100K nodes / 1M edges, 128-d fp32 features in pinned host "
+                        "memory, fanout [10,5], batch 1024, FIFO cache 10% of nodes, BFS ordering",
+               n=100_000, avg_degree=20, dim=128, labels=64, train=0.10, fanouts=(10, 5), b=1024,
+               cache_frac=0.10, S=4),
+}
+METRIC = "mini-batches/sec (sample+cache+gather)"
+UNIT = "mini-batches/s"
+GRAPH_SEED, RUN_SEED = 1, 1
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+            time.sleep(0.2)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                p = [x.strip() for x in line.split(",")]
+                if len(p) >= 7 and p[0].isdigit():
+                    rows.append(p)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [int(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[3 + k].lower() == "active"})
+        busy = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": int(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- inputs
+
+def build_inputs(cfg, features_where: str):
+    import torch
+    from paper_2112_08541_b200.features import synthetic_features
+    from paper_2112_08541_b200.graph import generate_power_law_device
+    from paper_2112_08541_b200.ordering import proximity_schedule_device
+    t0 = time.time()
+    dg = generate_power_law_device(cfg["n"], cfg["avg_degree"], seed=GRAPH_SEED, train_fraction=cfg["train"],
+                                   num_labels=cfg["labels"])
+    torch.cuda.synchronize()
+    t1 = time.time()
+    feats = synthetic_features(cfg["n"], cfg["dim"], seed=GRAPH_SEED, device_resident=(features_where == "hbm"))
+    torch.cuda.synchronize()
+    t2 = time.time()
+    order, _ = proximity_schedule_device(dg, cfg["S"], cfg["b"], seed=RUN_SEED)
+    torch.cuda.synchronize()
+    t3 = time.time()
+    return dg, feats, order, {"graph_gen_s": round(t1 - t0, 3), "features_gen_s": round(t2 - t1, 3),
+                              "ordering_epoch_s": round(t3 - t2, 3)}
+
+
+def host_link_peak_gbs():
+    import torch
+    nbytes = 256 << 20
+    src = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    dst = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    for _ in range(2):
+        dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    best = 0.0
+    for _ in range(5):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        dst.copy_(src, non_blocking=True)
+        e.record()
+        e.synchronize()
+        best = max(best, nbytes / (s.elapsed_time(e) * 1e-3) / 1e9)
+    return best
+
+
+# ----------------------------------------------------------------------------- CPU reference
+
+_REF = {}
+
+
+def _ref_sample(i):
+    from oracle import sampler_oracle as so
+    r = _REF
+    _, _, distinct, _ = so.sample_batch(r["off"], r["col"], r["batches"][i], r["fanouts"], RUN_SEED, i)
+    return distinct
+
+
+def cpu_reference(hg, batches, cfg, feats_host, idx, cores):
+    """Reference algorithm on the host: sampler (per batch, `cores` processes),
+    FIFO cache (sequential state machine, 1 core), numpy gather."""
+    import multiprocessing as mp
+    from oracle import cache_oracle as co
+    _REF.update(off=hg.row_offsets, col=hg.col_indices, batches=batches, fanouts=cfg["fanouts"])
+    fifo = co.FifoEngine(int(cfg["cache_frac"] * cfg["n"]), 0, 1)
+    t0 = time.time()
+    if cores > 1:
+        with mp.get_context("fork").Pool(cores) as pool:
+            traces = pool.map(_ref_sample, idx, chunksize=1)
+    else:
+        traces = [_ref_sample(i) for i in idx]
+    t1 = time.time()
+    fb = 0
+    for tr in traces:
+        fifo.run([tr], [0])
+        rows = feats_host[tr]
+        fb += rows.nbytes
+    t2 = time.time()
+    return {"batches": len(idx), "seconds": t2 - t0, "sample_s": t1 - t0, "cache_gather_s": t2 - t1,
+            "feature_bytes": fb}
+
+
+# ----------------------------------------------------------------------------- arms
+
+def run_bgl(args, cfg):
+    import torch
+    import torch.distributed as dist
+    from paper_2112_08541_b200.cachesim import CacheConfig
+    from paper_2112_08541_b200.pipeline import MiniBatchPipeline
+
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dg, feats, order, setup = build_inputs(cfg, args.features)
+    b = cfg["b"]
+    cap = int(cfg["cache_frac"] * cfg["n"]) // world
+    rb = cfg["dim"] * 4
+    nb_total = (order.numel() + b - 1) // b
+    if world > 1:
+        # replicas: rank r runs the batches i = r (mod world) with its own shard
+        # of the cache capacity
+        mine = torch.arange(rank, nb_total, world, device="cuda")
+        idx = (mine.unsqueeze(1) * b + torch.arange(b, device="cuda").unsqueeze(0)).flatten()
+        idx = idx[idx < order.numel()]
+        order = order[idx]
+    pipe = MiniBatchPipeline(dg, cfg["fanouts"], b, order, RUN_SEED,
+                             CacheConfig(device_capacity=cap, feature_bytes_per_node=rb), feats)
+    pipe.step_eager()                       # warm the kernels before capture
+    torch.cuda.synchronize()
+    pipe.reset_cache()
+    pipe.capture()
+    peak_host = host_link_peak_gbs()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+
+    for _ in range(args.warmup):
+        pipe.step()
+    torch.cuda.synchronize()
+    c0 = pipe.counters.clone()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for k in range(args.steps):
+            flush.zero_()                  # L2 flush between timed steps (outside the events)
+            ev[k][0].record()
+            pipe.step()
+            ev[k][1].record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in ev]
+    total_ms = sum(step_ms)
+    c1 = pipe.counters.clone()
+    d = (c1 - c0).cpu().tolist()
+    queries, hits = d[0], d[1] + d[2] + d[3]
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        q = torch.tensor([queries, hits], dtype=torch.int64, device="cuda")
+        dist.all_reduce(q)
+        queries, hits = q.tolist()
+
+    # stage breakdown + gather roofline (eager steps with events, after the timed region)
+    R = 10
+    st_times = {k: [] for k in ("sample", "dedup", "lookup", "gather", "insert")}
+    g_bytes_host, g_ms, g_rows = [], [], []
+    for _ in range(R):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+        cb = pipe.counters.clone()
+        flush.zero_()
+        pipe.step_eager(events=evs)
+        torch.cuda.synchronize()
+        ca = (pipe.counters - cb).cpu().tolist()
+        t = [evs[i].elapsed_time(evs[i + 1]) for i in range(5)]
+        for k, v in zip(st_times, t):
+            st_times[k].append(v)
+        misses = ca[3] + ca[4]                 # H + M rows come from the feature store
+        g_bytes_host.append(misses * rb)
+        g_rows.append(ca[0])
+        g_ms.append(t[3])
+    gather_ms = statistics.mean(g_ms)
+    host_bytes = statistics.mean(g_bytes_host)
+    rows_mean = statistics.mean(g_rows)
+    if args.features == "host":
+        achieved = host_bytes / (gather_ms * 1e-3) / 1e9
+        roof = {"bound": "host_link", "achieved": round(achieved, 2), "peak": round(peak_host, 2), "unit": "GB/s",
+                "frac": round(achieved / peak_host, 3),
+                "traffic": None, "kernel": "gather_v4_kernel",
+                "algorithmic_bytes_per_launch": int(host_bytes),
+                "peak_source": "pinned host->device cudaMemcpy measured in this run (not in MEASURED_PEAKS.json)"}
+    else:
+        hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+        alg = 2 * rows_mean * rb
+        achieved = alg / (gather_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 3), "traffic": None, "kernel": "gather_v4_kernel",
+                "algorithmic_bytes_per_launch": int(alg)}
+    prof = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{args.features}.json")
+    if os.path.exists(prof):
+        roof["traffic"] = json.load(open(prof)).get("gather_dram_bytes_per_launch")
+
+    # e2e through the public API with host buffers
+    from paper_2112_08541_b200 import _lib
+    order_host = order.cpu().numpy().astype(np.int32)
+    nbl = pipe.num_batches
+    seeds_pinned = torch.from_numpy(order_host).pin_memory()
+    out_ids = torch.empty(pipe.sampler.max_uniq, dtype=torch.int32).pin_memory()
+    out_cnt = torch.empty(8, dtype=torch.int64).pin_memory()
+    s = pipe.sampler
+    e2e_ms, h2d, d2h = [], 0, 0
+    for k in range(max(3, min(args.steps, 50))):
+        i = (args.warmup + args.steps + R + k) % nbl
+        lo, hi = i * b, min((i + 1) * b, order_host.size)
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        s.nodes[: hi - lo].copy_(seeds_pinned[lo:hi], non_blocking=True)
+        s.counts[0].fill_(hi - lo)
+        s.run(pipe.tables[i])
+        pipe.engine.retrieve_device(s.uniq, s.num_uniq, s.max_uniq, 0, counters=pipe.counters)
+        u = int(s.num_uniq.item())
+        out_ids[:u].copy_(s.uniq[:u], non_blocking=True)
+        out_cnt.copy_(pipe.counters, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+        h2d += (hi - lo) * 4
+        d2h += u * 4 + 64
+    n_e2e = len(e2e_ms)
+
+    value = world * args.steps / (total_ms * 1e-3)
+    ms_per_step = total_ms / args.steps
+    feat_gbs = queries * rb / (total_ms * 1e-3) / 1e9
+    out = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32 ids / u53 PCG64 keys / fp32 rows moved",
+        "data": "synthetic (GPU power-law generator, seed 1; hashed fp32 features)",
+        "config": {"workload": cfg["workload"], "num_nodes": cfg["n"], "csr_entries": dg.num_edges,
+                   "max_degree": dg.max_degree, "feature_dim": cfg["dim"], "fanouts": list(cfg["fanouts"]),
+                   "batch": b, "cache_rows_per_gpu": cap, "features": args.features,
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "flushed between timed steps (256 MB write, outside the events)",
+                   "batches_per_epoch": nb_total},
+        "feature_gbs": round(feat_gbs, 2), "hit_pct": round(100.0 * hits / max(queries, 1), 2),
+        "rows_per_batch": round(queries / max(args.steps, 1) / 1, 1),
+        "stages_ms": {k: round(statistics.mean(v), 4) for k, v in st_times.items()},
+        "roofline": roof,
+        "e2e": {"value": round(n_e2e / (sum(e2e_ms) * 1e-3) * world, 2), "unit": UNIT,
+                "h2d_bytes_per_step": int(h2d / n_e2e), "d2h_bytes_per_step": int(d2h / n_e2e),
+                "api": "BatchSampler.run + FeatureCacheEngine.retrieve_device, seeds H2D from pinned host, "
+                       "distinct IDs + counters D2H"},
+        "gpu_launches": pipe.kernels_per_step * args.steps,
+        "clocks": clk.summary(),
+        "setup": setup,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import ordering_oracle  # noqa: F401  (the oracle is the checker/baseline only)
+        hg = dg.to_host()
+        batches = [order_host[i * b:(i + 1) * b].astype(np.int64) for i in range(nb_total)]
+        fh = feats.cpu().numpy() if feats.is_cuda else feats.numpy()
+        nsample = 2 if args.config == "c2" else 8
+        r = cpu_reference(hg, batches, cfg, fh, list(range(nsample)), cores=1)
+        out["cpu_baseline"] = {"value": round(r["batches"] / r["seconds"], 4), "unit": UNIT, "cores": 1,
+                               "kind": "port",
+                               "sample": f"{nsample} batches of this schedule: oracle sample_batch (numpy lexsort, "
+                                         f"sampler.py:65-116) {r['sample_s']:.1f}s + FIFO simulate + numpy F[ids] "
+                                         f"{r['cache_gather_s']:.2f}s, 1 core"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args, cfg):
+    rank, local_rank, world = dist_env()
+    if rank != 0:
+        return
+    import torch
+    torch.cuda.set_device(local_rank)
+    from oracle import ordering_oracle as oo
+    from paper_2112_08541_b200.graph import generate_power_law_device
+    # identical inputs: the same generated graph, copied to the host
+    dg = generate_power_law_device(cfg["n"], cfg["avg_degree"], seed=GRAPH_SEED, train_fraction=cfg["train"],
+                                   num_labels=cfg["labels"])
+    hg = dg.to_host()
+    del dg
+    torch.cuda.empty_cache()
+    from oracle import features_oracle as fo
+    feats = fo.synthetic_features(np.arange(cfg["n"]), cfg["dim"], seed=GRAPH_SEED)
+    t0 = time.time()
+    batches = oo.proximity_schedule(hg.row_offsets, hg.col_indices, hg.train_mask, cfg["S"], cfg["b"], RUN_SEED)
+    order_s = time.time() - t0
+    cores = os.cpu_count() or 1
+    nb = len(batches)
+    wi = [i % nb for i in range(args.warmup)]
+    ti = [(args.warmup + i) % nb for i in range(args.steps)]
+    cpu_reference(hg, batches, cfg, feats, wi, cores)
+    r = cpu_reference(hg, batches, cfg, feats, ti, cores)
+    value = r["batches"] / r["seconds"]
+    out = {
+        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * r["seconds"] / r["batches"], 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64 ids / fp64 priorities / fp32 rows moved",
+        "data": "synthetic (same generated graph + hashed features, on the host)", "impl": "reference",
+        "config": {"workload": cfg["workload"], "num_nodes": cfg["n"], "csr_entries": int(hg.num_edges),
+                   "fanouts": list(cfg["fanouts"]), "batch": cfg["b"]},
+        "feature_gbs": round(r["feature_bytes"] / r["seconds"] / 1e9, 3),
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{r['batches']} batches: numpy oracle of gnnio sample_batch on {cores} "
+                                   f"processes ({r['sample_s']:.1f}s) + sequential FIFO simulate + numpy gather "
+                                   f"({r['cache_gather_s']:.1f}s); proximity schedule {order_s:.1f}s untimed"},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["bgl", "reference"], default="bgl")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--features", choices=["host", "hbm"], default="host")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_bgl(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

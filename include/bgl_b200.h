@@ -194,6 +194,17 @@ int bgl_select_pending(const int32_t* shard, int64_t len, const uint8_t* flags, 
 int bgl_interleave(const int32_t* seq_concat, const int64_t* seq_off, const int64_t* shift,
                    int32_t S, int64_t total, int32_t* out, void* stream);
 
+/* ---------------------------------------------------------------- pipeline staging
+ * Step staging for the CUDA-graph-captured pipeline (no reference
+ * counterpart: the reference loops batches in Python, sampler.py:136).
+ * i = *batch_counter % num_batches; seeds_out = order[i*b, min((i+1)*b,
+ * total)), *seed_count_out = its length, table_out = tables[i] (65x4),
+ * *batch_index_out = i (may be NULL); then *batch_counter += 1. */
+int bgl_stage_batch(const int32_t* order, int64_t total, int64_t batch_size, int64_t num_batches,
+                    const uint64_t* tables, int64_t* batch_counter, int32_t* seeds_out,
+                    int64_t* seed_count_out, uint64_t* table_out, int64_t* batch_index_out,
+                    void* stream);
+
 #ifdef __cplusplus
 }
 #endif

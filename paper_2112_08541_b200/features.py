@@ -78,7 +78,8 @@ class FeatureCacheEngine:
         self.counters = torch.zeros(8, dtype=torch.int64, device="cuda")
 
     def retrieve_device(self, ids: torch.Tensor, n_dev: torch.Tensor, max_n: int, worker: int,
-                        counters: torch.Tensor | None = None, stream=None, out: torch.Tensor | None = None):
+                        counters: torch.Tensor | None = None, stream=None, out: torch.Tensor | None = None,
+                        events=None):
         """Fully device-resident step: ids = sorted distinct int32 node IDs
         (e.g. BatchSampler.uniq) with the live count in n_dev. Rows land in
         `out` (default self.out) in batch order; codes in self.codes."""
@@ -90,9 +91,15 @@ class FeatureCacheEngine:
         _lib.check(lib.bgl_cache_lookup(h, ids.data_ptr(), n_dev.data_ptr(), max_n, worker, ids.data_ptr(),
                                         n_dev.data_ptr(), max_n, self.codes.data_ptr(), self.src_row.data_ptr(),
                                         cnt, st))
+        if events is not None:
+            events[0].record()
         _lib.check(lib.bgl_gather_rows(ids.data_ptr(), self.src_row.data_ptr(), n_dev.data_ptr(), max_n,
                                        self.dev.rows_ptr() or None, self.table, self.row_bytes, out.data_ptr(), st))
+        if events is not None:
+            events[1].record()
         _lib.check(lib.bgl_cache_insert(h, ids.data_ptr(), max_n, out.data_ptr(), cnt, st))
+        if events is not None and len(events) > 2:
+            events[2].record()
         return out
 
     def retrieve(self, batch_ids, batch_index: int):
