@@ -68,13 +68,16 @@ int bgl_pcg64_draws(const uint64_t* table, int64_t first, int64_t n, uint64_t* o
  * emits col[off_q + t] for the min(fanout, deg) smallest (draw, t), ascending,
  * grouped by parent in parent order. Writes draw_base[1] = draw_base[0] +
  * sum deg (the chain across hops, sampler.py:110-114) and *num_out_dev.
- * fanout <= 4096 (any fanout when max degree <= 4096). */
+ * fanout <= 4096 (clamp it to the graph's max degree: k = min(fanout, deg)).
+ * mark_bitmap (may be NULL): the dedup workspace of bgl_unique_sorted; every
+ * output is also marked there (fused K2 mark), so the later
+ * bgl_unique_sorted call only needs the seed segment. */
 size_t bgl_sample_hop_workspace(int64_t max_parents);
 int bgl_sample_hop(const int64_t* indptr, const int32_t* indices,
                    const int32_t* parents, const int64_t* num_parents_dev, int64_t max_parents,
                    int32_t fanout, const uint64_t* table, int64_t* draw_base,
                    int32_t* out_ids, int32_t* out_parent_idx, int64_t* num_out_dev,
-                   void* workspace, void* stream);
+                   void* workspace, void* mark_bitmap, void* stream);
 
 /* Partition accounting of simulate_epoch (sampler.py:139-153).
  * request_load[part_of[p]] += 1 for every parent; local_remote[0] += #parents

@@ -29,7 +29,8 @@ PROTOTYPES = {
     "bgl_pcg64_tables": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp]),
     "bgl_pcg64_draws": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp]),
     "bgl_sample_hop_workspace": (c_sz, [c_i64]),
-    "bgl_sample_hop": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "bgl_sample_hop": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                       c_vp]),
     "bgl_comm_account": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),
     "bgl_take_i32": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "bgl_unique_workspace": (c_sz, [c_i64]),

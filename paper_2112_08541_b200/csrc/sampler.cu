@@ -6,21 +6,27 @@
 // of the batch stream and emits col[off_q + t] for the k = min(fanout, deg)
 // smallest (u, t) pairs in ascending order (np.lexsort is stable, so equal
 // draws keep adjacency order). u = m * 2^-53 with m the 53-bit integer, so
-// comparing (m, t) integer pairs is exact and needs no fp64.
+// comparing (m, t) integer pairs is exact and needs no fp64; for deg <= 2048
+// the pair packs into one 64-bit key (m << 11 | t).
 //
 // Kernels per hop:
 //   hop_scan     decoupled look-back prefix of deg (draw offsets) and k
-//                (output offsets) over the parents; writes the chained draw
-//                base of the next hop and the output count.
-//   sample_warp  k <= 32: one warp walks a contiguous run of parents; lanes
-//                hold PCG64 states for 32 consecutive draws and keep a running
-//                top-32 of (m, t) keys as a bitonic-sorted warp register
-//                list; the state is handed from one parent to the next with a
-//                lane rotation (no per-parent jump-ahead).
-//   sample_block k > 32 (fanout > 32): one CTA per parent, chunked bitonic
-//                sort in shared memory (KCAP <= 4096).
+//                (output offsets); writes the chained draw base of the next
+//                hop and the output count, and lists the "heavy" parents
+//                (deg > 2048 or k > 32) for the block kernel.
+//   sample_warp  light parents: one warp walks a contiguous run of parents;
+//                lanes hold PCG64 states for 32 consecutive draws and keep a
+//                running top-k as a warp-distributed sorted list. A chunk of
+//                32 draws is merged by bitonic sort+merge when many lanes beat
+//                the current k-th key, else by per-candidate insertion. The
+//                stream is handed from one parent to the next with a lane
+//                rotation (no per-parent jump-ahead).
+//   sample_heavy one CTA per heavy parent: k <= 32 -> 8 warps each keep a
+//                top-k over a strided share of the chunks, merged in smem;
+//                k > 32 -> chunked bitonic sort in smem (KCAP <= 4096).
 // Only the k selected neighbours are read from col: the draws need deg, not
 // the neighbour IDs, so col traffic is k * 4 B per parent, not deg * 4 B.
+// Optionally every output is also marked in the dedup bitmap (fused K2 mark).
 #include "common.cuh"
 #include "pcg64.cuh"
 #include "scan.cuh"
@@ -30,10 +36,13 @@ namespace bgl {
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
+constexpr int64_t kNarrowMaxDeg = 2048;   // t fits 11 bits next to the 53-bit draw
 
 struct HopWorkspace {
     int64_t* deg_prefix;   // [max_parents]
     int64_t* k_prefix;     // [max_parents]
+    int32_t* heavy;        // [max_parents] heavy parent positions (unordered)
+    int64_t* heavy_count;  // [1]
     void* scan;            // scan state for 2 values
     int64_t max_tiles;
 };
@@ -48,16 +57,26 @@ static HopWorkspace carve_hop_ws(void* ws, int64_t max_parents) {
     p += align256(m * 8);
     w.k_prefix = reinterpret_cast<int64_t*>(p);
     p += align256(m * 8);
+    w.heavy = reinterpret_cast<int32_t*>(p);
+    p += align256(m * 4);
     w.max_tiles = ceil_div(m, kScanTile);
     w.scan = p;
+    p += align256(scan_state_bytes(2, w.max_tiles));
+    w.heavy_count = reinterpret_cast<int64_t*>(p);   // zeroed with the scan state (contiguous)
     return w;
+}
+
+__device__ __forceinline__ void mark_bit(uint32_t* bitmap, int32_t v) {
+    uint32_t bit = 1u << (v & 31);
+    uint32_t* w = bitmap + (v >> 5);
+    if (!(ld_volatile(w) & bit)) atomicOr(w, bit);
 }
 
 __global__ void __launch_bounds__(kScanThreads)
 hop_scan_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ parents,
                 const int64_t* __restrict__ num_parents_dev, int32_t fanout, ScanState ss,
-                int64_t* __restrict__ deg_prefix, int64_t* __restrict__ k_prefix,
-                int64_t* __restrict__ draw_base, int64_t* __restrict__ num_out) {
+                int64_t* __restrict__ deg_prefix, int64_t* __restrict__ k_prefix, int32_t* __restrict__ heavy,
+                int64_t* __restrict__ heavy_count, int64_t* __restrict__ draw_base, int64_t* __restrict__ num_out) {
     __shared__ int64_t s_deg[kScanTile];
     __shared__ int32_t s_k[kScanTile];
     __shared__ int64_t s_red[kScanThreads / 32 + 1];
@@ -76,8 +95,17 @@ hop_scan_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
             int64_t p = parents[q];
             d = indptr[p + 1] - indptr[p];
         }
+        const int32_t k = (int32_t)(d < fanout ? d : fanout);
         s_deg[i] = d;
-        s_k[i] = (int32_t)(d < fanout ? d : fanout);
+        s_k[i] = k;
+        const bool hv = k > 32 || d > kNarrowMaxDeg;
+        const unsigned m = __ballot_sync(0xffffffffu, hv);
+        if (m) {
+            int64_t slot = 0;
+            if (lane_id() == 0) slot = (int64_t)atomicAdd((unsigned long long*)heavy_count, (unsigned long long)__popc(m));
+            slot = __shfl_sync(0xffffffffu, slot, 0);
+            if (hv) heavy[slot + __popc(m & ((1u << lane_id()) - 1u))] = (int32_t)q;
+        }
     }
     __syncthreads();
     int64_t my_d = 0, my_k = 0;
@@ -97,7 +125,6 @@ hop_scan_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
     __syncthreads();
     lookback<2>(ss, tile, s_agg, s_pre);
     const int64_t pd = s_pre[0], pk = s_pre[1];
-    // write blocked results back to smem, then coalesced stores
     int64_t rd = ex_d, rk = ex_k;
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
@@ -122,40 +149,47 @@ hop_scan_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ 
     }
 }
 
-// ---------------------------------------------------------------- warp top-k
-struct Key {
+// ---------------------------------------------------------------- key types
+// Narrow: 64-bit (m << 11 | t), deg <= 2048. Wide: (m, t) pair.
+struct WideKey {
     uint64_t m;
     uint32_t t;
 };
 
-__device__ __forceinline__ bool key_lt(const Key& a, const Key& b) {
+__device__ __forceinline__ bool key_lt(uint64_t a, uint64_t b) { return a < b; }
+__device__ __forceinline__ bool key_lt(const WideKey& a, const WideKey& b) {
     return a.m < b.m || (a.m == b.m && a.t < b.t);
 }
-
-__device__ __forceinline__ Key shfl_key(const Key& k, int src) {
-    Key r;
-    r.m = __shfl_sync(0xffffffffu, k.m, src);
-    r.t = __shfl_sync(0xffffffffu, k.t, src);
-    return r;
+__device__ __forceinline__ uint64_t shfl(uint64_t k, int src) { return __shfl_sync(0xffffffffu, k, src); }
+__device__ __forceinline__ WideKey shfl(const WideKey& k, int src) {
+    return WideKey{__shfl_sync(0xffffffffu, k.m, src), __shfl_sync(0xffffffffu, k.t, src)};
 }
-
-__device__ __forceinline__ Key shfl_xor_key(const Key& k, int mask) {
-    Key r;
-    r.m = __shfl_xor_sync(0xffffffffu, k.m, mask);
-    r.t = __shfl_xor_sync(0xffffffffu, k.t, mask);
-    return r;
+__device__ __forceinline__ uint64_t shfl_xor(uint64_t k, int m) { return __shfl_xor_sync(0xffffffffu, k, m); }
+__device__ __forceinline__ WideKey shfl_xor(const WideKey& k, int m) {
+    return WideKey{__shfl_xor_sync(0xffffffffu, k.m, m), __shfl_xor_sync(0xffffffffu, k.t, m)};
 }
+__device__ __forceinline__ uint64_t shfl_up(uint64_t k, int d) { return __shfl_up_sync(0xffffffffu, k, d); }
+__device__ __forceinline__ WideKey shfl_up(const WideKey& k, int d) {
+    return WideKey{__shfl_up_sync(0xffffffffu, k.m, d), __shfl_up_sync(0xffffffffu, k.t, d)};
+}
+template <typename K> __device__ __forceinline__ K key_inf();
+template <> __device__ __forceinline__ uint64_t key_inf<uint64_t>() { return ~0ull; }
+template <> __device__ __forceinline__ WideKey key_inf<WideKey>() { return WideKey{~0ull, ~0u}; }
+__device__ __forceinline__ uint64_t make_key(uint64_t m, uint32_t t, uint64_t*) { return (m << 11) | t; }
+__device__ __forceinline__ WideKey make_key(uint64_t m, uint32_t t, WideKey*) { return WideKey{m, t}; }
+__device__ __forceinline__ uint32_t key_t(uint64_t k) { return (uint32_t)(k & 2047u); }
+__device__ __forceinline__ uint32_t key_t(const WideKey& k) { return k.t; }
 
-// compare-exchange with the partner lane^j; lower lane keeps the min when asc.
-__device__ __forceinline__ Key cmpx(const Key& x, int j, bool asc) {
-    Key o = shfl_xor_key(x, j);
+// compare-exchange with lane^j; the lower lane keeps the min when asc
+template <typename K>
+__device__ __forceinline__ K cmpx(const K& x, int j, bool asc) {
+    K o = shfl_xor(x, j);
     bool lower = (lane_id() & j) == 0;
-    bool take_min = (lower == asc);
-    bool o_lt = key_lt(o, x);
-    return (take_min == o_lt) ? o : x;
+    return ((lower == asc) == key_lt(o, x)) ? o : x;
 }
 
-__device__ __forceinline__ Key warp_bitonic_sort(Key x) {
+template <typename K>
+__device__ __forceinline__ K warp_bitonic_sort(K x) {
     const int lane = lane_id();
 #pragma unroll
     for (int k = 2; k <= 32; k <<= 1) {
@@ -165,10 +199,45 @@ __device__ __forceinline__ Key warp_bitonic_sort(Key x) {
     return x;
 }
 
-__device__ __forceinline__ Key warp_bitonic_merge(Key x) {
+template <typename K>
+__device__ __forceinline__ K warp_bitonic_merge(K x) {
 #pragma unroll
     for (int j = 16; j > 0; j >>= 1) x = cmpx(x, j, true);
     return x;
+}
+
+// best: ascending warp list; merge a sorted candidate list (32 smallest kept)
+template <typename K>
+__device__ __forceinline__ K merge_sorted(const K& best, const K& sorted_cand) {
+    K rev = shfl(sorted_cand, 31 - lane_id());
+    K x = key_lt(rev, best) ? rev : best;
+    return warp_bitonic_merge(x);
+}
+
+constexpr int kInsertMax = 6;   // <= this many passing lanes: insert one by one
+
+// Fold one chunk of candidates (one per lane, INF when invalid) into `best`.
+template <typename K>
+__device__ __forceinline__ void fold_chunk(K& best, K& kth, K cand, int k) {
+    const bool pass = key_lt(cand, kth);
+    unsigned mask = __ballot_sync(0xffffffffu, pass);
+    if (!mask) return;
+    if (__popc(mask) > kInsertMax) {
+        if (!pass) cand = key_inf<K>();
+        best = merge_sorted(best, warp_bitonic_sort(cand));
+    } else {
+        const int lane = lane_id();
+        while (mask) {
+            const int src = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const K c = shfl(cand, src);
+            const int pos = __popc(__ballot_sync(0xffffffffu, key_lt(best, c)));
+            const K up = shfl_up(best, 1);
+            if (lane == pos) best = c;
+            else if (lane > pos) best = up;
+        }
+    }
+    kth = shfl(best, k - 1);
 }
 
 constexpr int kWarpsPerBlock = 8;
@@ -179,7 +248,7 @@ sample_warp_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
                    int32_t fanout, const uint64_t* __restrict__ table,
                    const int64_t* __restrict__ draw_base, const int64_t* __restrict__ deg_prefix,
                    const int64_t* __restrict__ k_prefix, int32_t* __restrict__ out_ids,
-                   int32_t* __restrict__ out_pidx, int32_t run) {
+                   int32_t* __restrict__ out_pidx, uint32_t* __restrict__ bitmap, int32_t run) {
     const int64_t n = *num_parents_dev;
     const int lane = lane_id();
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -187,19 +256,21 @@ sample_warp_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
     const PcgTable T{table};
     const U128 A32 = T.A(5), C32 = T.C(5);
     const int64_t D0 = draw_base[0];
-    const Key INF{~0ull, ~0u};
+    const uint64_t INF = ~0ull;
 
     for (int64_t q0 = warp * run; q0 < n; q0 += nwarps * run) {
         const int64_t q1 = min(q0 + run, n);
         bool have = false;
         U128 s{0, 0};
+        int32_t p_next = parents[q0];
         for (int64_t q = q0; q < q1; ++q) {
-            const int32_t p = parents[q];
+            const int32_t p = p_next;
+            if (q + 1 < q1) p_next = parents[q + 1];
             const int64_t off = indptr[p];
             const int64_t deg = indptr[p + 1] - off;
             if (deg == 0) continue;                  // consumes no draws (sampler.py:77-79)
             const int k = (int)(deg < fanout ? deg : fanout);
-            if (k > 32) {                            // sample_block_kernel's parent
+            if (k > 32 || deg > kNarrowMaxDeg) {     // sample_heavy_kernel's parent
                 have = false;
                 continue;
             }
@@ -207,29 +278,17 @@ sample_warp_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
                 s = T.at((uint64_t)(D0 + deg_prefix[q] + lane + 1));
                 have = true;
             }
-            Key best = INF;
-            Key kth = INF;   // current k-th smallest (threshold)
+            uint64_t best = INF, kth = INF;
             const int64_t nc = (deg + 31) >> 5;
             for (int64_t c = 0; c < nc; ++c) {
                 if (c > 0) s = affine(A32, C32, s);
                 const int64_t t = (c << 5) + lane;
-                Key cand = INF;
-                if (t < deg) {
-                    cand.m = draw_of_state(s);
-                    cand.t = (uint32_t)t;
-                }
-                const bool better = key_lt(cand, kth);
-                if (!__any_sync(0xffffffffu, better)) continue;
-                if (!better) cand = INF;
-                cand = warp_bitonic_sort(cand);
-                Key rev = shfl_key(cand, 31 - lane);
-                if (key_lt(rev, best)) best = rev;
-                best = warp_bitonic_merge(best);
-                kth = shfl_key(best, k - 1);
+                const uint64_t cand = t < deg ? make_key(draw_of_state(s), (uint32_t)t, (uint64_t*)nullptr) : INF;
+                fold_chunk(best, kth, cand, k);
             }
-            // hand the stream to the next parent: it starts at draw deg (relative)
+            // hand the stream to the next parent: it starts at relative draw deg
             {
-                const int64_t x = deg + lane;           // wanted relative draw
+                const int64_t x = deg + lane;
                 const int src = (int)(x & 31);
                 U128 r;
                 r.hi = __shfl_sync(0xffffffffu, s.hi, src);
@@ -239,15 +298,18 @@ sample_warp_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
             }
             if (lane < k) {
                 const int64_t o = k_prefix[q] + lane;
-                out_ids[o] = indices[off + best.t];
+                const int32_t v = indices[off + key_t(best)];
+                out_ids[o] = v;
                 out_pidx[o] = (int32_t)q;
+                if (bitmap) mark_bit(bitmap, v);
             }
         }
     }
 }
 
-// ---------------------------------------------------------------- block top-k
-constexpr int kBlockThreads = 256;
+// ---------------------------------------------------------------- heavy parents
+constexpr int kHeavyThreads = 256;
+constexpr int kHeavyWarps = kHeavyThreads / 32;
 
 __device__ __forceinline__ void smem_bitonic_sort(uint64_t* m, uint32_t* t, int n) {
     for (int k = 2; k <= n; k <<= 1) {
@@ -270,51 +332,81 @@ __device__ __forceinline__ void smem_bitonic_sort(uint64_t* m, uint32_t* t, int 
     }
 }
 
-__global__ void __launch_bounds__(kBlockThreads)
-sample_block_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                    const int32_t* __restrict__ parents, const int64_t* __restrict__ num_parents_dev,
-                    int32_t fanout, int kcap, const uint64_t* __restrict__ table,
-                    const int64_t* __restrict__ draw_base, const int64_t* __restrict__ deg_prefix,
-                    const int64_t* __restrict__ k_prefix, int32_t* __restrict__ out_ids,
-                    int32_t* __restrict__ out_pidx) {
+__global__ void __launch_bounds__(kHeavyThreads)
+sample_heavy_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                    const int32_t* __restrict__ parents, const int32_t* __restrict__ heavy,
+                    const int64_t* __restrict__ heavy_count, int32_t fanout, int kcap,
+                    const uint64_t* __restrict__ table, const int64_t* __restrict__ draw_base,
+                    const int64_t* __restrict__ deg_prefix, const int64_t* __restrict__ k_prefix,
+                    int32_t* __restrict__ out_ids, int32_t* __restrict__ out_pidx, uint32_t* __restrict__ bitmap) {
     extern __shared__ __align__(16) unsigned char smem[];
-    uint64_t* m = reinterpret_cast<uint64_t*>(smem);
-    uint32_t* tt = reinterpret_cast<uint32_t*>(smem + sizeof(uint64_t) * 2 * kcap);
-    const int64_t n = *num_parents_dev;
+    uint64_t* sm = reinterpret_cast<uint64_t*>(smem);
+    uint32_t* st = reinterpret_cast<uint32_t*>(smem + sizeof(uint64_t) * 2 * kcap);
+    const int64_t nh = *heavy_count;
     const PcgTable T{table};
-    const U128 A256 = T.A(8), C256 = T.C(8);
     const int64_t D0 = draw_base[0];
-    for (int64_t q = blockIdx.x; q < n; q += gridDim.x) {
+    const int lane = lane_id(), wid = warp_id();
+    for (int64_t h = blockIdx.x; h < nh; h += gridDim.x) {
+        const int64_t q = heavy[h];
         const int32_t p = parents[q];
         const int64_t off = indptr[p];
         const int64_t deg = indptr[p + 1] - off;
-        const int64_t k = deg < fanout ? deg : fanout;
-        if (k <= 32) continue;
-        for (int i = threadIdx.x; i < kcap; i += blockDim.x) {
-            m[i] = ~0ull;
-            tt[i] = ~0u;
-        }
+        const int k = (int)(deg < fanout ? deg : fanout);
         const int64_t dq = D0 + deg_prefix[q];
-        for (int64_t base = 0; base < deg; base += kcap) {
-            U128 s = T.at((uint64_t)(dq + base + threadIdx.x + 1));
-            for (int i = threadIdx.x; i < kcap; i += blockDim.x) {
-                if (i != (int)threadIdx.x) s = affine(A256, C256, s);
-                int64_t t = base + i;
-                if (t < deg) {
-                    m[kcap + i] = draw_of_state(s);
-                    tt[kcap + i] = (uint32_t)t;
-                } else {
-                    m[kcap + i] = ~0ull;
-                    tt[kcap + i] = ~0u;
+        const int64_t o = k_prefix[q];
+        if (k <= 32) {
+            // warp w folds chunks w, w+8, ... into its own top-k
+            const U128 A256 = T.A(8), C256 = T.C(8);
+            WideKey best = key_inf<WideKey>(), kth = best;
+            const int64_t nc = (deg + 31) >> 5;
+            U128 s{0, 0};
+            for (int64_t c = wid; c < nc; c += kHeavyWarps) {
+                s = (c == wid) ? T.at((uint64_t)(dq + (c << 5) + lane + 1)) : affine(A256, C256, s);
+                const int64_t t = (c << 5) + lane;
+                WideKey cand = key_inf<WideKey>();
+                if (t < deg) cand = WideKey{draw_of_state(s), (uint32_t)t};
+                fold_chunk(best, kth, cand, k);
+            }
+            uint32_t* st2 = reinterpret_cast<uint32_t*>(smem + sizeof(uint64_t) * kHeavyThreads);
+            sm[wid * 32 + lane] = best.m;
+            st2[wid * 32 + lane] = best.t;
+            __syncthreads();
+            if (wid == 0) {
+                WideKey acc{sm[lane], st2[lane]};
+                for (int w = 1; w < kHeavyWarps; ++w)
+                    acc = merge_sorted(acc, WideKey{sm[w * 32 + lane], st2[w * 32 + lane]});
+                if (lane < k) {
+                    const int32_t v = indices[off + acc.t];
+                    out_ids[o + lane] = v;
+                    out_pidx[o + lane] = (int32_t)q;
+                    if (bitmap) mark_bit(bitmap, v);
                 }
             }
             __syncthreads();
-            smem_bitonic_sort(m, tt, 2 * kcap);
+            continue;
         }
-        const int64_t o = k_prefix[q];
+        // k > 32: chunked bitonic sort of (current top-kcap | next kcap draws)
+        const U128 Ab = T.A(8), Cb = T.C(8);   // blockDim == 256 == 2^8
+        for (int i = threadIdx.x; i < kcap; i += blockDim.x) {
+            sm[i] = ~0ull;
+            st[i] = ~0u;
+        }
+        for (int64_t base = 0; base < deg; base += kcap) {
+            U128 s = T.at((uint64_t)(dq + base + threadIdx.x + 1));
+            for (int i = threadIdx.x; i < kcap; i += blockDim.x) {
+                if (i != (int)threadIdx.x) s = affine(Ab, Cb, s);
+                int64_t t = base + i;
+                sm[kcap + i] = t < deg ? draw_of_state(s) : ~0ull;
+                st[kcap + i] = t < deg ? (uint32_t)t : ~0u;
+            }
+            __syncthreads();
+            smem_bitonic_sort(sm, st, 2 * kcap);
+        }
         for (int i = threadIdx.x; i < k; i += blockDim.x) {
-            out_ids[o + i] = indices[off + tt[i]];
+            const int32_t v = indices[off + st[i]];
+            out_ids[o + i] = v;
             out_pidx[o + i] = (int32_t)q;
+            if (bitmap) mark_bit(bitmap, v);
         }
         __syncthreads();
     }
@@ -328,23 +420,29 @@ extern "C" {
 
 size_t bgl_sample_hop_workspace(int64_t max_parents) {
     int64_t m = max_parents > 0 ? max_parents : 1;
-    return align256(m * 8) * 2 + scan_state_bytes(2, ceil_div(m, kScanTile)) + 256;
+    return align256(m * 8) * 2 + align256(m * 4) + align256(scan_state_bytes(2, ceil_div(m, kScanTile))) + 256;
 }
 
 int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t* parents,
                    const int64_t* num_parents_dev, int64_t max_parents, int32_t fanout,
                    const uint64_t* table, int64_t* draw_base, int32_t* out_ids,
-                   int32_t* out_parent_idx, int64_t* num_out_dev, void* workspace, void* stream) {
+                   int32_t* out_parent_idx, int64_t* num_out_dev, void* workspace, void* mark_bitmap,
+                   void* stream) {
     BGL_CHECK_ARG(fanout >= 1, "fanouts must be positive");
+    BGL_CHECK_ARG(fanout <= 4096, "fanout > 4096 unsupported (clamp it to the graph's max degree)");
     BGL_CHECK_ARG(max_parents >= 0, "bgl_sample_hop: max_parents < 0");
     BGL_CHECK_ARG(indptr && table && draw_base && num_parents_dev && num_out_dev && workspace,
                   "bgl_sample_hop: null pointer");
     cudaStream_t st = as_stream(stream);
     HopWorkspace w = carve_hop_ws(workspace, max_parents);
-    BGL_TRY(reset_scan_state(w.scan, 2, w.max_tiles, st));
+    // scan state + heavy counter are contiguous: one memset
+    BGL_TRY(cuda_status(cudaMemsetAsync(w.scan, 0, align256(scan_state_bytes(2, w.max_tiles)) + 8, st),
+                        "hop workspace reset"));
     ScanState ss = make_scan_state(w.scan, 2, w.max_tiles);
+    uint32_t* bm = reinterpret_cast<uint32_t*>(mark_bitmap);
     hop_scan_kernel<<<(unsigned)w.max_tiles, kScanThreads, 0, st>>>(
-        indptr, parents, num_parents_dev, fanout, ss, w.deg_prefix, w.k_prefix, draw_base, num_out_dev);
+        indptr, parents, num_parents_dev, fanout, ss, w.deg_prefix, w.k_prefix, w.heavy, w.heavy_count,
+        draw_base, num_out_dev);
     BGL_TRY(launch_status("hop_scan_kernel"));
     if (max_parents == 0) return BGL_OK;
     // contiguous runs of parents per warp; ~4 runs per resident warp
@@ -356,22 +454,22 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     unsigned blocks = (unsigned)ceil_div(warps, kWarpsPerBlock);
     sample_warp_kernel<<<blocks, kWarpsPerBlock * 32, 0, st>>>(
         indptr, indices, parents, num_parents_dev, fanout, table, draw_base, w.deg_prefix, w.k_prefix,
-        out_ids, out_parent_idx, (int32_t)run);
+        out_ids, out_parent_idx, bm, (int32_t)run);
     BGL_TRY(launch_status("sample_warp_kernel"));
+    int kcap = 32;
     if (fanout > 32) {
-        int kcap = 64;
-        while (kcap < fanout && kcap < 4096) kcap <<= 1;
-        size_t smem = (size_t)2 * kcap * (sizeof(uint64_t) + sizeof(uint32_t));
-        if (smem > 48 * 1024)
-            BGL_TRY(cuda_status(cudaFuncSetAttribute(sample_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                     (int)smem), "cudaFuncSetAttribute(sample_block)"));
-        unsigned grid = grid_for(max_parents, 1, 16);
-        sample_block_kernel<<<grid, kBlockThreads, smem, st>>>(
-            indptr, indices, parents, num_parents_dev, fanout, kcap, table, draw_base, w.deg_prefix,
-            w.k_prefix, out_ids, out_parent_idx);
-        BGL_TRY(launch_status("sample_block_kernel"));
+        kcap = 64;
+        while (kcap < fanout) kcap <<= 1;
     }
-    return BGL_OK;
+    size_t smem = (size_t)2 * kcap * (sizeof(uint64_t) + sizeof(uint32_t));
+    if (smem < (size_t)kHeavyWarps * 32 * 12) smem = (size_t)kHeavyWarps * 32 * 12;
+    if (smem > 48 * 1024)
+        BGL_TRY(cuda_status(cudaFuncSetAttribute(sample_heavy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem), "cudaFuncSetAttribute(sample_heavy)"));
+    sample_heavy_kernel<<<(unsigned)kNumSMs * 4, kHeavyThreads, smem, st>>>(
+        indptr, indices, parents, w.heavy, w.heavy_count, fanout, kcap, table, draw_base, w.deg_prefix,
+        w.k_prefix, out_ids, out_parent_idx, bm);
+    return launch_status("sample_heavy_kernel");
 }
 
 }  // extern "C"

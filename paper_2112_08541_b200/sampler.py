@@ -167,11 +167,12 @@ class BatchSampler:
                 self.dg.indptr.data_ptr(), self.dg.indices.data_ptr(),
                 base + self._seg_bytes[h], cnt + 8 * h, self.caps[h], self.eff[h], tptr, db + 8 * h,
                 base + self._seg_bytes[h + 1], self.pidx[h].data_ptr(), cnt + 8 * (h + 1),
-                self.hop_ws.data_ptr(), st))
+                self.hop_ws.data_ptr(), self.uws.data_ptr(), st))
             if hooks is not None:
                 hooks(h)
+        # hop outputs were marked by the sampler kernels; mark the seeds and emit
         _lib.check(lib.bgl_unique_sorted(
-            base, self.H + 1, self._c_seg_off, cnt, self._c_seg_max, self.dg.num_nodes,
+            base, 1, self._c_seg_off, cnt, self._c_seg_max, self.dg.num_nodes,
             self.uws.data_ptr(), self.uniq.data_ptr(), self.num_uniq.data_ptr(), st))
         if self.local is not None:
             _lib.check(lib.bgl_relabel(base, self.H + 1, self._c_seg_off, cnt, self._c_seg_max,
