@@ -203,12 +203,15 @@ def run_bgl(args, cfg):
     pipe = MiniBatchPipeline(dg, cfg["fanouts"], b, order, RUN_SEED,
                              CacheConfig(device_capacity=cap, feature_bytes_per_node=rb), feats)
     pipe.step_eager()                       # warm the kernels before capture
+    pipe.step_eager()
     torch.cuda.synchronize()
-    pipe.reset_cache()
     pipe.capture()
+    pipe.capture(fed=True)
+    pipe.reset()
     peak_host = host_link_peak_gbs()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
 
+    pipe.prime()
     for _ in range(args.warmup):
         pipe.step()
     torch.cuda.synchronize()
@@ -221,7 +224,7 @@ def run_bgl(args, cfg):
         for k in range(args.steps):
             flush.zero_()                  # L2 flush between timed steps (outside the events)
             ev[k][0].record()
-            pipe.step()
+            pipe.step()                    # graph: cache+gather of batch k || sampling of batch k+1
             ev[k][1].record()
         torch.cuda.synchronize()
     if world > 1:
@@ -239,7 +242,7 @@ def run_bgl(args, cfg):
         dist.all_reduce(q)
         queries, hits = q.tolist()
 
-    # stage breakdown + gather roofline (eager steps with events, after the timed region)
+    # stage breakdown + gather roofline (serialised steps with events, after the timed region)
     R = 10
     st_times = {k: [] for k in ("sample", "dedup", "lookup", "gather", "insert")}
     g_bytes_host, g_ms, g_rows = [], [], []
@@ -247,7 +250,7 @@ def run_bgl(args, cfg):
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
         cb = pipe.counters.clone()
         flush.zero_()
-        pipe.step_eager(events=evs)
+        pipe.step_serial(evs)
         torch.cuda.synchronize()
         ca = (pipe.counters - cb).cpu().tolist()
         t = [evs[i].elapsed_time(evs[i + 1]) for i in range(5)]
@@ -279,33 +282,40 @@ def run_bgl(args, cfg):
     if os.path.exists(prof):
         roof["traffic"] = json.load(open(prof)).get("gather_dram_bytes_per_launch")
 
-    # e2e through the public API with host buffers
-    from paper_2112_08541_b200 import _lib
+    # e2e through the public API with host buffers: every step copies the next
+    # batch's seeds from pinned host memory and reads this batch's distinct IDs
+    # (the AccessTrace row) and the cache counters back to pinned host memory.
     order_host = order.cpu().numpy().astype(np.int32)
     nbl = pipe.num_batches
     seeds_pinned = torch.from_numpy(order_host).pin_memory()
-    out_ids = torch.empty(pipe.sampler.max_uniq, dtype=torch.int32).pin_memory()
+    out_ids = torch.empty(pipe.max_uniq, dtype=torch.int32).pin_memory()
     out_cnt = torch.empty(8, dtype=torch.int64).pin_memory()
-    s = pipe.sampler
+
+    def feed(i):
+        lo, hi = (i % nbl) * b, min((i % nbl + 1) * b, order_host.size)
+        pipe.fed_seeds[: hi - lo].copy_(seeds_pinned[lo:hi], non_blocking=True)
+        pipe.fed_count.fill_(hi - lo)
+        return (hi - lo) * 4
+
+    pipe.reset()
+    feed(0)
+    pipe.prime(fed=True)
+    torch.cuda.synchronize()
     e2e_ms, h2d, d2h = [], 0, 0
-    for k in range(max(3, min(args.steps, 50))):
-        i = (args.warmup + args.steps + R + k) % nbl
-        lo, hi = i * b, min((i + 1) * b, order_host.size)
+    for k in range(max(3, min(args.steps, 100))):
         flush.zero_()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        s.nodes[: hi - lo].copy_(seeds_pinned[lo:hi], non_blocking=True)
-        s.counts[0].fill_(hi - lo)
-        s.run(pipe.tables[i])
-        pipe.engine.retrieve_device(s.uniq, s.num_uniq, s.max_uniq, 0, counters=pipe.counters)
+        h2d += feed(k + 1)
+        pipe.step(fed=True)
+        s = pipe.samplers[pipe.last_slot()]
         u = int(s.num_uniq.item())
         out_ids[:u].copy_(s.uniq[:u], non_blocking=True)
         out_cnt.copy_(pipe.counters, non_blocking=True)
         e1.record()
         e1.synchronize()
         e2e_ms.append(e0.elapsed_time(e1))
-        h2d += (hi - lo) * 4
         d2h += u * 4 + 64
     n_e2e = len(e2e_ms)
 

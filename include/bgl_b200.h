@@ -202,11 +202,13 @@ int bgl_interleave(const int32_t* seq_concat, const int64_t* seq_off, const int6
  * counterpart: the reference loops batches in Python, sampler.py:136).
  * i = *batch_counter % num_batches; seeds_out = order[i*b, min((i+1)*b,
  * total)), *seed_count_out = its length, table_out = tables[i] (65x4),
- * *batch_index_out = i (may be NULL); then *batch_counter += 1. */
+ * *batch_index_out = i (may be NULL); then *batch_counter += 1.
+ * fed_count_dev != NULL (host-fed mode): `order` holds only this batch's
+ * seeds (copied from the host), *fed_count_dev of them. */
 int bgl_stage_batch(const int32_t* order, int64_t total, int64_t batch_size, int64_t num_batches,
                     const uint64_t* tables, int64_t* batch_counter, int32_t* seeds_out,
                     int64_t* seed_count_out, uint64_t* table_out, int64_t* batch_index_out,
-                    void* stream);
+                    const int64_t* fed_count_dev, void* stream);
 
 #ifdef __cplusplus
 }

@@ -1,24 +1,29 @@
 """The fused per-mini-batch preprocessing pipeline on one B200.
 
-One step = one mini-batch of BGL's data path:
+One mini-batch of BGL's data path:
     stage seeds  (device-resident proximity schedule, bgl_stage_batch)
-    sample       H hops, PCG64 replay                 (bgl_sample_hop x H)
-    dedup        sorted distinct set                   (bgl_unique_sorted)
-    lookup       FIFO cache, pre-batch state           (bgl_cache_lookup)
+    sample       H hops, PCG64 replay, fused dedup mark (bgl_sample_hop x H)
+    dedup        sorted distinct set                    (bgl_unique_sorted)
+    lookup       FIFO cache, pre-batch state            (bgl_cache_lookup)
     gather       hits from HBM ring slots, misses zero-copy from pinned host
                  (bgl_gather_rows)
     insert       insert-after-batch + row copy into the ring (bgl_cache_insert)
 
-Everything is device-resident (counts, batch index, PCG64 tables), so the
-whole step is captured once in a CUDA graph and replayed per batch; the
-outputs of batch i (distinct IDs, feature rows, outcome codes, counters) are
-exactly the reference's `simulate_epoch` trace / `simulate` report rows and
+Software pipelining (the paper's overlap of sampling with feature retrieval,
+PAPER.md:536-576): sampling is cache-independent (its rng is keyed by the
+batch index, sampler.py:138), so step k runs cache+gather of batch k on one
+stream while batch k+1 is sampled on another, with double-buffered sampler
+and row buffers. The cache state machine still sees batches strictly in
+order. Every step is captured once per buffer parity in a CUDA graph and
+replayed; counts, batch index and PCG64 tables stay on the device.
+
+Outputs of batch i (distinct IDs, rows, outcome codes, counters) equal the
+reference's `simulate_epoch` trace / `simulate` report rows and
 `F[trace.batches[i]]`.
 """
 
 from __future__ import annotations
 
-import numpy as np
 import torch
 
 from . import _lib
@@ -38,68 +43,124 @@ class MiniBatchPipeline:
         self.order = order.to(device="cuda", dtype=torch.int32).contiguous()
         total = int(self.order.numel())
         self.num_batches = int(num_batches or (total + self.b - 1) // self.b)
-        self.sampler = BatchSampler(dg, fanouts, self.b)
-        self.engine = FeatureCacheEngine(cache_cfg, features, max_batch=self.sampler.max_uniq)
+        self.samplers = [BatchSampler(dg, fanouts, self.b) for _ in range(2)]
+        self.max_uniq = self.samplers[0].max_uniq
+        self.engine = FeatureCacheEngine(cache_cfg, features, max_batch=self.max_uniq)
+        self.outs = [self.engine.out, torch.empty_like(self.engine.out)]
         self.tables = pcg_tables(pcg_states(seed, range(self.num_batches)))
-        self.table_stage = torch.empty((65, 4), dtype=torch.int64, device="cuda")
+        self.table_stage = [torch.empty((65, 4), dtype=torch.int64, device="cuda") for _ in range(2)]
         self.batch_counter = torch.zeros(1, dtype=torch.int64, device="cuda")
-        self.batch_index = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self.batch_index = torch.zeros(2, dtype=torch.int64, device="cuda")
         self.counters = torch.zeros(8, dtype=torch.int64, device="cuda")
-        self.graph: torch.cuda.CUDAGraph | None = None
-        self.kernels_per_step = self._count_kernels()
+        self.fed_seeds = torch.empty(self.b, dtype=torch.int32, device="cuda")
+        self.fed_count = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self.s_stream = torch.cuda.Stream()
+        self.c_stream = torch.cuda.Stream()
+        self.graphs: dict = {}
+        self.k = 0              # batches that went through the cache
+        self.primed = False     # batch k already sampled into samplers[k % 2]
+        s = self.samplers[0]
+        hops = 3 * s.H                                  # scan + warp + heavy per hop
+        self.kernels_per_step = 1 + hops + 3 + 4 + 1 + 2   # stage, hops, dedup(mark, emit, reset), lookup, gather, insert
 
-    def _count_kernels(self) -> int:
-        hops = sum(3 if f > 32 else 2 for f in self.sampler.eff)   # scan + warp (+ block)
-        return 1 + hops + 3 + 4 + 1 + 2                              # stage, hops, dedup, lookup, gather, insert
-
-    # -- one step, eager -------------------------------------------------------
-    def step_eager(self, stream=None, events=None) -> None:
-        """events (optional, eager only): 6 CUDA events recorded after staging,
-        sampling, dedup, lookup, gather and insert -> per-stage times."""
-        s = self.sampler
-        _lib.call("bgl_stage_batch", self.order.data_ptr(), self.order.numel(), self.b, self.num_batches,
+    # -- building blocks ------------------------------------------------------------
+    def _sample(self, slot: int, stream=None, fed: bool = False, hooks=None) -> None:
+        s = self.samplers[slot]
+        order = self.fed_seeds if fed else self.order
+        _lib.call("bgl_stage_batch", order.data_ptr(), self.order.numel(), self.b, self.num_batches,
                   self.tables.data_ptr(), self.batch_counter.data_ptr(), s.nodes.data_ptr(), s.counts.data_ptr(),
-                  self.table_stage.data_ptr(), self.batch_index.data_ptr(), _lib.stream_ptr(stream))
-        if events is None:
-            s.run(self.table_stage, stream=stream)
-            self.engine.retrieve_device(s.uniq, s.num_uniq, s.max_uniq, 0, counters=self.counters, stream=stream)
-            return
-        events[0].record()
-        s.run(self.table_stage, stream=stream, hooks=lambda h: events[1].record() if h == s.H - 1 else None)
-        events[2].record()
-        self.engine.retrieve_device(s.uniq, s.num_uniq, s.max_uniq, 0, counters=self.counters, stream=stream,
-                                    events=events[3:6])
+                  self.table_stage[slot].data_ptr(), self.batch_index.data_ptr() + 8 * slot,
+                  self.fed_count.data_ptr() if fed else None, _lib.stream_ptr(stream))
+        s.run(self.table_stage[slot], stream=stream, hooks=hooks)
 
-    # -- CUDA graph ------------------------------------------------------------
-    def capture(self) -> None:
-        """Capture one step; replays advance the device batch counter."""
-        saved = self.batch_counter.clone()
+    def _cache(self, slot: int, stream=None, events=None) -> None:
+        s = self.samplers[slot]
+        self.engine.retrieve_device(s.uniq, s.num_uniq, s.max_uniq, 0, counters=self.counters, stream=stream,
+                                    out=self.outs[slot], events=events)
+
+    def prime(self, fed: bool = False) -> None:
+        """Sample the first batch (pipeline prologue, untimed)."""
+        if not self.primed:
+            self._sample(self.k % 2, fed=fed)
+            self.primed = True
+
+    # -- one overlapped step: cache(k) || sample(k+1) ------------------------------
+    def _overlapped(self, parity: int, fed: bool, stream=None) -> None:
+        cur = torch.cuda.current_stream() if stream is None else stream
+        self.s_stream.wait_stream(cur)
+        self.c_stream.wait_stream(cur)
+        with torch.cuda.stream(self.s_stream):
+            self._sample(1 - parity, stream=self.s_stream, fed=fed)
+        with torch.cuda.stream(self.c_stream):
+            self._cache(parity, stream=self.c_stream)
+        cur.wait_stream(self.s_stream)
+        cur.wait_stream(self.c_stream)
+
+    def step_eager(self, fed: bool = False) -> None:
+        self.prime(fed)
+        self._overlapped(self.k % 2, fed)
+        self.k += 1
+
+    def step_serial(self, events) -> None:
+        """Same work, serialised on the current stream with 6 events recorded
+        around sample(k+1), dedup, lookup, gather and insert of batch k
+        (stage breakdown; not used for the headline number)."""
+        self.prime()
+        parity = self.k % 2
+        s = self.samplers[1 - parity]
+        events[0].record()
+        self._sample(1 - parity, hooks=lambda h: events[1].record() if h == s.H - 1 else None)
+        events[2].record()
+        self._cache(parity, events=events[3:6])
+        self.k += 1
+
+    def capture(self, fed: bool = False) -> None:
+        """Capture the overlapped step for both buffer parities."""
+        self.prime(fed)
         torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        side = torch.cuda.Stream()
-        side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side):
-            with torch.cuda.graph(g, stream=side):
-                self.step_eager(stream=side)
-        torch.cuda.current_stream().wait_stream(side)
+        saved = self.batch_counter.clone()
+        for parity in (0, 1):
+            g = torch.cuda.CUDAGraph()
+            cs = torch.cuda.Stream()
+            cs.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cs):
+                with torch.cuda.graph(g, stream=cs):
+                    self._overlapped(parity, fed, stream=cs)
+            torch.cuda.current_stream().wait_stream(cs)
+            self.graphs[(parity, fed)] = g
         torch.cuda.synchronize()
         self.batch_counter.copy_(saved)        # capture does not execute; keep the counter exact
-        self.graph = g
 
-    def step(self) -> None:
-        if self.graph is None:
-            self.step_eager()
-        else:
-            self.graph.replay()
+    def step(self, fed: bool = False) -> None:
+        g = self.graphs.get((self.k % 2, fed))
+        if g is None:
+            self.step_eager(fed)
+            return
+        self.prime(fed)
+        g.replay()
+        self.k += 1
 
-    # -- views -----------------------------------------------------------------
-    def rows(self) -> torch.Tensor:
-        return self.engine.out[: int(self.sampler.num_uniq.item())]
+    # -- views of the last batch through the cache -----------------------------
+    def last_slot(self) -> int:
+        return (self.k - 1) % 2
 
     def distinct(self) -> torch.Tensor:
-        return self.sampler.distinct()
+        return self.samplers[self.last_slot()].distinct()
 
-    def reset_cache(self) -> None:
+    def rows(self) -> torch.Tensor:
+        n = int(self.samplers[self.last_slot()].num_uniq.item())
+        return self.outs[self.last_slot()][:n]
+
+    def codes(self) -> torch.Tensor:
+        n = int(self.samplers[self.last_slot()].num_uniq.item())
+        return self.engine.codes[:n]
+
+    def reset(self) -> None:
+        """Cold cache, batch 0 next (graphs stay valid)."""
+        torch.cuda.synchronize()
         _lib.call("bgl_cache_reset", self.engine.dev.handle, _lib.stream_ptr())
         self.counters.zero_()
         self.batch_counter.zero_()
+        self.k = 0
+        self.primed = False
+        torch.cuda.synchronize()

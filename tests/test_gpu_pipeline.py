@@ -45,7 +45,28 @@ def test_pipeline_matches_oracle(use_graph):
         rows = pipe.rows().cpu().numpy()
         assert np.array_equal(rows, fo.synthetic_features(distinct, dim, seed=2)), i
         c, codes = fifo.run([distinct], [0])
-        assert np.array_equal(pipe.engine.codes[: len(distinct)].cpu().numpy(), codes[0])
+        assert np.array_equal(pipe.codes().cpu().numpy(), codes[0])
         now = pipe.counters.cpu().numpy()
         assert np.array_equal(now[:7] - prev[:7], c[0]), i
         prev = now
+    # reset -> the same epoch again from a cold cache, host-fed seeds
+    if use_graph:
+        pipe.capture(fed=True)
+    pipe.reset()
+    fifo = co.FifoEngine(cap, 0, 1)
+
+    def feed(i):
+        sb = torch.from_numpy(ref_batches[i].astype(np.int32))
+        pipe.fed_seeds[: len(sb)].copy_(sb)
+        pipe.fed_count.fill_(len(sb))
+
+    feed(0)
+    pipe.prime(fed=True)
+    for i in range(4):
+        feed(i + 1)
+        pipe.step(fed=True)
+        torch.cuda.synchronize()
+        _, _, distinct, _ = so.sample_batch(hg.row_offsets, hg.col_indices, ref_batches[i], fan, seed, i)
+        assert np.array_equal(pipe.distinct().cpu().numpy(), distinct), i
+        _, codes = fifo.run([distinct], [0])
+        assert np.array_equal(pipe.codes().cpu().numpy(), codes[0])
