@@ -71,13 +71,15 @@ int bgl_pcg64_draws(const uint64_t* table, int64_t first, int64_t n, uint64_t* o
  * fanout <= 4096 (clamp it to the graph's max degree: k = min(fanout, deg)).
  * mark_bitmap (may be NULL): the dedup workspace of bgl_unique_sorted; every
  * output is also marked there (fused K2 mark), so the later
- * bgl_unique_sorted call only needs the seed segment. */
+ * bgl_unique_sorted call only needs the seed segment. max_ctas > 0 caps the
+ * CTAs of the sampling kernels (grid-stride loops cover the rest), leaving
+ * SMs to a concurrently running gather; 0 = fill the GPU. */
 size_t bgl_sample_hop_workspace(int64_t max_parents);
 int bgl_sample_hop(const int64_t* indptr, const int32_t* indices,
                    const int32_t* parents, const int64_t* num_parents_dev, int64_t max_parents,
                    int32_t fanout, const uint64_t* table, int64_t* draw_base,
                    int32_t* out_ids, int32_t* out_parent_idx, int64_t* num_out_dev,
-                   void* workspace, void* mark_bitmap, void* stream);
+                   void* workspace, void* mark_bitmap, int32_t max_ctas, void* stream);
 
 /* Partition accounting of simulate_epoch (sampler.py:139-153).
  * request_load[part_of[p]] += 1 for every parent; local_remote[0] += #parents
@@ -160,10 +162,14 @@ int bgl_cache_export(bgl_cache_t cache, int64_t* dev_slots_host, int64_t* dev_ta
  * out[i] = src_row[i] >= 0 ? ring_rows[src_row[i]] : table[ids[i]], 128-bit
  * vectorised. `table` may be a device pointer (HBM-resident features) or the
  * device alias of pinned host memory (zero-copy miss path). src_row NULL:
- * plain gather out[i] = table[ids[i]]. row_bytes % 4 == 0. */
+ * plain gather out[i] = table[ids[i]]. row_bytes % 4 == 0. mode: 0 = every row,
+ * 1 = only hits (src_row >= 0), 2 = only misses (src_row < 0). ctas > 0:
+ * launch exactly ctas CTAs of two warps (the host-link miss path needs only
+ * ~150 warps in flight, the rest of the GPU stays free for the sampler);
+ * 0 = fill the GPU (HBM rows). */
 int bgl_gather_rows(const int32_t* ids, const int64_t* src_row, const int64_t* n_dev, int64_t max_n,
                     const void* ring_rows, const void* table, int64_t row_bytes, void* out,
-                    void* stream);
+                    int32_t mode, int32_t ctas, void* stream);
 /* Fill rows of the deterministic synthetic feature table (oracle/features_oracle.py). */
 int bgl_synthetic_features(int64_t first_node, int64_t num_nodes, int32_t dim, uint64_t seed,
                            float* out, void* stream);

@@ -30,7 +30,7 @@ PROTOTYPES = {
     "bgl_pcg64_draws": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp]),
     "bgl_sample_hop_workspace": (c_sz, [c_i64]),
     "bgl_sample_hop": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
-                                       c_vp]),
+                                       c_i32, c_vp]),
     "bgl_comm_account": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),
     "bgl_take_i32": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "bgl_unique_workspace": (c_sz, [c_i64]),
@@ -47,7 +47,7 @@ PROTOTYPES = {
     "bgl_cache_lookup": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "bgl_cache_insert": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "bgl_cache_export": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
-    "bgl_gather_rows": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "bgl_gather_rows": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_i32, c_i32, c_vp]),
     "bgl_synthetic_features": (ctypes.c_int, [c_i64, c_i64, c_i32, c_u64, c_vp, c_vp]),
     "bgl_bfs_workspace": (c_sz, [c_i64]),
     "bgl_bfs_level": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64,

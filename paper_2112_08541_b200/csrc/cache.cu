@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "scan.cuh"
 
 struct bgl_cache {
     int64_t n = 0;          // node-ID space of the index
@@ -190,6 +191,96 @@ miss_scatter_kernel(const int32_t* __restrict__ sorted_ids, const int64_t* __res
             s_run[y] += add;
         }
         __syncthreads();
+    }
+}
+
+// Single-pass lookup + insert-list compaction for one device shard (d == 1)
+// and an already sorted, distinct batch: classify, count and write the two
+// ascending lists (device-missed, full-missed) with a decoupled look-back.
+__global__ void __launch_bounds__(kCThreads)
+lookup_fused_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ n_dev, int32_t worker, int64_t C,
+                    const int32_t* __restrict__ slot_of, const int32_t* __restrict__ hslot_of,
+                    uint8_t* __restrict__ codes, int64_t* __restrict__ src_row, int64_t* __restrict__ counters,
+                    ScanState ss, int32_t* __restrict__ lists, int64_t list_cap, int64_t* __restrict__ mcount) {
+    constexpr int NW = kCThreads / 32;
+    __shared__ int32_t s_w[2][kCRounds][NW];
+    __shared__ int64_t s_c[4];
+    __shared__ int64_t s_agg[2], s_pre[2], s_slot;
+    const int64_t n = *n_dev;
+    const int64_t ntiles = n > 0 ? ceil_div(n, kCTile) : 1;
+    const int64_t tile = claim_tile(ss, &s_slot);
+    if (tile >= ntiles) return;
+    const int lane = lane_id(), wid = warp_id();
+    const unsigned lt = (1u << lane) - 1u;
+    if (threadIdx.x < 4) s_c[threadIdx.x] = 0;
+    unsigned bm_d[kCRounds], bm_f[kCRounds];
+    int64_t c[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int r = 0; r < kCRounds; ++r) {
+        const int64_t e = tile * kCTile + r * kCThreads + threadIdx.x;
+        bool dm = false, fm = false;
+        if (e < n) {
+            const int32_t v = ids[e];
+            const int32_t s = slot_of[v];
+            uint8_t code;
+            int64_t src = -1;
+            if (s >= 0) {
+                code = (worker == 0) ? kD : kP;
+                src = s;
+            } else {
+                dm = true;
+                fm = hslot_of == nullptr || hslot_of[v] < 0;
+                code = fm ? kM : kH;
+            }
+            c[code]++;
+            if (codes) codes[e] = code;
+            if (src_row) src_row[e] = src;
+        }
+        bm_d[r] = __ballot_sync(0xffffffffu, dm);
+        bm_f[r] = __ballot_sync(0xffffffffu, fm);
+        if (lane == 0) {
+            s_w[0][r][wid] = __popc(bm_d[r]);
+            s_w[1][r][wid] = __popc(bm_f[r]);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        int64_t w = warp_sum_i64(c[k]);
+        if (lane == 0 && w) atomicAdd((unsigned long long*)&s_c[k], (unsigned long long)w);
+    }
+    if (threadIdx.x < 2) {
+        int64_t t = 0;
+        for (int r = 0; r < kCRounds; ++r)
+            for (int w = 0; w < NW; ++w) t += s_w[threadIdx.x][r][w];
+        s_agg[threadIdx.x] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        atomicAdd((unsigned long long*)&counters[0], (unsigned long long)(s_c[0] + s_c[1] + s_c[2] + s_c[3]));
+        for (int k = 0; k < 4; ++k)
+            if (s_c[k]) atomicAdd((unsigned long long*)&counters[1 + k], (unsigned long long)s_c[k]);
+    }
+    lookback<2>(ss, tile, s_agg, s_pre);
+    int64_t run_d = s_pre[0], run_f = s_pre[1];
+#pragma unroll
+    for (int r = 0; r < kCRounds; ++r) {
+        const int64_t e = tile * kCTile + r * kCThreads + threadIdx.x;
+        int64_t pd = run_d + __popc(bm_d[r] & lt), pf = run_f + __popc(bm_f[r] & lt);
+        for (int w = 0; w < wid; ++w) {
+            pd += s_w[0][r][w];
+            pf += s_w[1][r][w];
+        }
+        if ((bm_d[r] >> lane) & 1u) lists[pd] = (int32_t)e;
+        if ((bm_f[r] >> lane) & 1u) lists[list_cap + pf] = (int32_t)e;
+        for (int w = 0; w < NW; ++w) {
+            run_d += s_w[0][r][w];
+            run_f += s_w[1][r][w];
+        }
+    }
+    if (tile == ntiles - 1 && threadIdx.x == 0) {
+        mcount[0] = s_pre[0] + s_agg[0];
+        mcount[1] = s_pre[1] + s_agg[1];
     }
 }
 
@@ -367,7 +458,9 @@ int bgl_cache_reserve_batch(bgl_cache_t c, int64_t max_batch) {
     int64_t cap = std::max<int64_t>(max_batch, 1024);
     c->max_tiles = ceil_div(cap, kCTile);
     BGL_TRY(cuda_status(cudaMalloc((void**)&c->lists, (size_t)(c->d + 1) * cap * 4), "cache lists"));
-    BGL_TRY(cuda_status(cudaMalloc((void**)&c->tile_counts, (size_t)(c->d + 1) * c->max_tiles * 8), "cache tiles"));
+    // tile counts of the generic path; doubles as the look-back state of the fused one
+    BGL_TRY(cuda_status(cudaMalloc((void**)&c->tile_counts, (size_t)(c->d + 1) * c->max_tiles * 8 + 256),
+                        "cache tiles"));
     c->list_cap = cap;
     return BGL_OK;
 }
@@ -389,6 +482,14 @@ int bgl_cache_lookup(bgl_cache_t c, const int32_t* ids, const int64_t* n_dev, in
     BGL_CHECK_ARG(worker >= 0 && worker < c->d, "worker device out of range");
     BGL_CHECK_ARG(max_sorted <= c->list_cap, "batch larger than reserved (call bgl_cache_reserve_batch)");
     cudaStream_t st = as_stream(stream);
+    if (c->d == 1 && ids == sorted_ids && n_dev == n_sorted_dev) {
+        const int64_t ntiles = std::max<int64_t>(1, ceil_div(max_sorted, kCTile));
+        BGL_TRY(reset_scan_state(c->tile_counts, 2, ntiles, st));
+        lookup_fused_kernel<<<(unsigned)ntiles, kCThreads, 0, st>>>(
+            ids, n_dev, worker, c->C, c->slot_of, c->hslot_of, codes, src_row, counters,
+            make_scan_state(c->tile_counts, 2, ntiles), c->lists, c->list_cap, c->mcount);
+        return launch_status("lookup_fused_kernel");
+    }
     if (max_n > 0) {
         lookup_kernel<<<grid_for(max_n, 256), 256, 0, st>>>(ids, n_dev, worker, c->d, c->C, c->slot_of, c->hslot_of,
                                                             codes, src_row, counters);

@@ -427,7 +427,7 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
                    const int64_t* num_parents_dev, int64_t max_parents, int32_t fanout,
                    const uint64_t* table, int64_t* draw_base, int32_t* out_ids,
                    int32_t* out_parent_idx, int64_t* num_out_dev, void* workspace, void* mark_bitmap,
-                   void* stream) {
+                   int32_t max_ctas, void* stream) {
     BGL_CHECK_ARG(fanout >= 1, "fanouts must be positive");
     BGL_CHECK_ARG(fanout <= 4096, "fanout > 4096 unsupported (clamp it to the graph's max degree)");
     BGL_CHECK_ARG(max_parents >= 0, "bgl_sample_hop: max_parents < 0");
@@ -452,6 +452,7 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     if (run > 64) run = 64;
     int64_t warps = ceil_div(max_parents, run);
     unsigned blocks = (unsigned)ceil_div(warps, kWarpsPerBlock);
+    if (max_ctas > 0 && blocks > (unsigned)max_ctas) blocks = (unsigned)max_ctas;   // grid-stride covers the rest
     sample_warp_kernel<<<blocks, kWarpsPerBlock * 32, 0, st>>>(
         indptr, indices, parents, num_parents_dev, fanout, table, draw_base, w.deg_prefix, w.k_prefix,
         out_ids, out_parent_idx, bm, (int32_t)run);
@@ -466,7 +467,9 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     if (smem > 48 * 1024)
         BGL_TRY(cuda_status(cudaFuncSetAttribute(sample_heavy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem), "cudaFuncSetAttribute(sample_heavy)"));
-    sample_heavy_kernel<<<(unsigned)kNumSMs * 4, kHeavyThreads, smem, st>>>(
+    unsigned hblocks = (unsigned)kNumSMs * 4;
+    if (max_ctas > 0 && hblocks > (unsigned)max_ctas) hblocks = (unsigned)max_ctas;
+    sample_heavy_kernel<<<hblocks, kHeavyThreads, smem, st>>>(
         indptr, indices, parents, w.heavy, w.heavy_count, fanout, kcap, table, draw_base, w.deg_prefix,
         w.k_prefix, out_ids, out_parent_idx, bm);
     return launch_status("sample_heavy_kernel");

@@ -76,6 +76,10 @@ class FeatureCacheEngine:
         self.n_dev = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.out = torch.empty((max(max_batch, 1), self.dim), dtype=features.dtype, device="cuda")
         self.counters = torch.zeros(8, dtype=torch.int64, device="cuda")
+        # host-link miss gather: 74 CTAs x 8 warps saturate the link while
+        # leaving half the SMs' load/store pipes to the overlapped sampler
+        # (tools/gather_bench.cu, tools/overlap_probe*.py)
+        self.miss_ctas = 74
 
     def retrieve_device(self, ids: torch.Tensor, n_dev: torch.Tensor, max_n: int, worker: int,
                         counters: torch.Tensor | None = None, stream=None, out: torch.Tensor | None = None,
@@ -93,8 +97,17 @@ class FeatureCacheEngine:
                                         cnt, st))
         if events is not None:
             events[0].record()
-        _lib.check(lib.bgl_gather_rows(ids.data_ptr(), self.src_row.data_ptr(), n_dev.data_ptr(), max_n,
-                                       self.dev.rows_ptr() or None, self.table, self.row_bytes, out.data_ptr(), st))
+        ring = self.dev.rows_ptr() or None
+        if self.features.is_cuda:
+            _lib.check(lib.bgl_gather_rows(ids.data_ptr(), self.src_row.data_ptr(), n_dev.data_ptr(), max_n, ring,
+                                           self.table, self.row_bytes, out.data_ptr(), 0, 0, st))
+        else:
+            # hits from HBM with the whole GPU, then misses over the host link
+            # with ~150 warps (keeps the SMs free for the overlapped sampler)
+            _lib.check(lib.bgl_gather_rows(ids.data_ptr(), self.src_row.data_ptr(), n_dev.data_ptr(), max_n, ring,
+                                           self.table, self.row_bytes, out.data_ptr(), 1, 0, st))
+            _lib.check(lib.bgl_gather_rows(ids.data_ptr(), self.src_row.data_ptr(), n_dev.data_ptr(), max_n, ring,
+                                           self.table, self.row_bytes, out.data_ptr(), 2, self.miss_ctas, st))
         if events is not None:
             events[1].record()
         _lib.check(lib.bgl_cache_insert(h, ids.data_ptr(), max_n, out.data_ptr(), cnt, st))

@@ -35,7 +35,8 @@ from .sampler import BatchSampler, pcg_states, pcg_tables
 
 class MiniBatchPipeline:
     def __init__(self, dg: DeviceGraph, fanouts, batch_size: int, order: torch.Tensor, seed: int,
-                 cache_cfg: CacheConfig, features: torch.Tensor, num_batches: int | None = None):
+                 cache_cfg: CacheConfig, features: torch.Tensor, num_batches: int | None = None,
+                 sampler_ctas: int | None = None):
         if cache_cfg.num_devices != 1:
             raise ValueError("single-GPU pipeline: one cache shard (num_devices=1)")
         self.dg = dg
@@ -43,7 +44,9 @@ class MiniBatchPipeline:
         self.order = order.to(device="cuda", dtype=torch.int32).contiguous()
         total = int(self.order.numel())
         self.num_batches = int(num_batches or (total + self.b - 1) // self.b)
-        self.samplers = [BatchSampler(dg, fanouts, self.b) for _ in range(2)]
+        if sampler_ctas is None:
+            sampler_ctas = 0          # the miss gather takes only 2 warps per SM
+        self.samplers = [BatchSampler(dg, fanouts, self.b, max_ctas=sampler_ctas) for _ in range(2)]
         self.max_uniq = self.samplers[0].max_uniq
         self.engine = FeatureCacheEngine(cache_cfg, features, max_batch=self.max_uniq)
         self.outs = [self.engine.out, torch.empty_like(self.engine.out)]
@@ -54,14 +57,18 @@ class MiniBatchPipeline:
         self.counters = torch.zeros(8, dtype=torch.int64, device="cuda")
         self.fed_seeds = torch.empty(self.b, dtype=torch.int32, device="cuda")
         self.fed_count = torch.zeros(1, dtype=torch.int64, device="cuda")
-        self.s_stream = torch.cuda.Stream()
-        self.c_stream = torch.cuda.Stream()
+        # the cache/gather chain is the critical path (host link): its blocks are
+        # dispatched ahead of the sampler's when both are pending
+        self.s_stream = torch.cuda.Stream(priority=0)
+        self.c_stream = torch.cuda.Stream(priority=-5)
         self.graphs: dict = {}
         self.k = 0              # batches that went through the cache
         self.primed = False     # batch k already sampled into samplers[k % 2]
         s = self.samplers[0]
         hops = 3 * s.H                                  # scan + warp + heavy per hop
-        self.kernels_per_step = 1 + hops + 3 + 4 + 1 + 2   # stage, hops, dedup(mark, emit, reset), lookup, gather, insert
+        gathers = 1 if features.is_cuda else 2
+        # stage, hops, dedup (mark seeds, emit, reset), lookup (fused), gather(s), insert + finalize
+        self.kernels_per_step = 1 + hops + 3 + 1 + gathers + 2
 
     # -- building blocks ------------------------------------------------------------
     def _sample(self, slot: int, stream=None, fed: bool = False, hooks=None) -> None:

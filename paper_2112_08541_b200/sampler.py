@@ -103,8 +103,9 @@ class BatchSampler:
     `counts[h]` (device int64) holds the live length of segment h.
     """
 
-    def __init__(self, g, fanouts, max_batch: int, relabel: bool = False):
+    def __init__(self, g, fanouts, max_batch: int, relabel: bool = False, max_ctas: int = 0):
         self.dg: DeviceGraph = device_graph(g)
+        self.max_ctas = int(max_ctas)   # cap on sampler CTAs (0 = whole GPU)
         self.fanouts = tuple(int(f) for f in fanouts)
         self.H = len(self.fanouts)
         if self.H > 7:
@@ -167,7 +168,7 @@ class BatchSampler:
                 self.dg.indptr.data_ptr(), self.dg.indices.data_ptr(),
                 base + self._seg_bytes[h], cnt + 8 * h, self.caps[h], self.eff[h], tptr, db + 8 * h,
                 base + self._seg_bytes[h + 1], self.pidx[h].data_ptr(), cnt + 8 * (h + 1),
-                self.hop_ws.data_ptr(), self.uws.data_ptr(), st))
+                self.hop_ws.data_ptr(), self.uws.data_ptr(), self.max_ctas, st))
             if hooks is not None:
                 hooks(h)
         # hop outputs were marked by the sampler kernels; mark the seeds and emit

@@ -42,7 +42,7 @@ def test_library_exports_every_declared_symbol():
 def test_library_error_path_without_gpu():
     lib = _lib.load(require_cuda=False)
     # argument validation runs before any CUDA call
-    assert lib.bgl_gather_rows(None, None, None, 0, None, None, 3, None, None) == _lib.BGL_EINVAL
+    assert lib.bgl_gather_rows(None, None, None, 0, None, None, 3, None, 0, 0, None) == _lib.BGL_EINVAL
     assert b"row_bytes" in lib.bgl_last_error()
     with pytest.raises(ValueError):
         _lib.check(_lib.BGL_EINVAL)

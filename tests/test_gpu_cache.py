@@ -129,5 +129,5 @@ def test_feature_retrieval_bit_exact(where, d):
     nd = torch.tensor([len(slots)], dtype=torch.int64, device="cuda")
     out = torch.empty((len(slots), dim), dtype=torch.float32, device="cuda")
     _lib.call("bgl_gather_rows", ids.data_ptr(), src.data_ptr(), nd.data_ptr(), len(slots), eng.dev.rows_ptr(),
-              eng.table, dim * 4, out.data_ptr(), _lib.stream_ptr())
+              eng.table, dim * 4, out.data_ptr(), 0, 0, _lib.stream_ptr())
     assert np.array_equal(out.cpu().numpy(), ref_table[flat[slots]])
