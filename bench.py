@@ -193,13 +193,6 @@ def run_bgl(args, cfg):
     cap = int(cfg["cache_frac"] * cfg["n"]) // world
     rb = cfg["dim"] * 4
     nb_total = (order.numel() + b - 1) // b
-    if world > 1:
-        # replicas: rank r runs the batches i = r (mod world) with its own shard
-        # of the cache capacity
-        mine = torch.arange(rank, nb_total, world, device="cuda")
-        idx = (mine.unsqueeze(1) * b + torch.arange(b, device="cuda").unsqueeze(0)).flatten()
-        idx = idx[idx < order.numel()]
-        order = order[idx]
     pipe = MiniBatchPipeline(dg, cfg["fanouts"], b, order, RUN_SEED,
                              CacheConfig(device_capacity=cap, feature_bytes_per_node=rb), feats)
     pipe.step_eager()                       # warm the kernels before capture
@@ -280,7 +273,15 @@ def run_bgl(args, cfg):
                 "algorithmic_bytes_per_launch": int(alg)}
     prof = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{args.features}.json")
     if os.path.exists(prof):
-        roof["traffic"] = json.load(open(prof)).get("gather_dram_bytes_per_launch")
+        tr = json.load(open(prof))
+        if args.features == "host":
+            # bytes that crossed the host link per miss-gather launch (ncu pcie__read_bytes)
+            roof["traffic"] = tr["miss_gather"]["pcie_read_bytes_per_launch"]
+            roof["traffic_kind"] = "pcie_read_bytes (ncu, one launch)"
+        else:
+            roof["traffic"] = tr.get("hit_gather", {}).get("dram_bytes_per_launch")
+            roof["traffic_kind"] = "dram__bytes_read+write (ncu, one launch)"
+        roof["traffic_source"] = tr.get("source")
 
     # e2e through the public API with host buffers: every step copies the next
     # batch's seeds from pinned host memory and reads this batch's distinct IDs
@@ -363,6 +364,109 @@ def run_bgl(args, cfg):
         dist.destroy_process_group()
 
 
+def run_sharded(args, cfg):
+    """N GPUs, one process each: node-ID-sharded FIFO cache (home = v % N,
+    cachesim.py:505-506), rank w samples batches i = j*N + w, IDs and rows
+    exchanged with NCCL all-to-all (paper_2112_08541_b200/distributed.py).
+    One step = one round = N mini-batches (one per GPU)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2112_08541_b200.distributed import GpuShardEngine, GpuShardOps, ShardedFeatureCache
+    from paper_2112_08541_b200.sampler import BatchSampler, pcg_states, pcg_tables
+
+    if "RANK" not in os.environ:            # single process without torchrun (--sharded at N=1)
+        os.environ.update(RANK="0", LOCAL_RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
+                          MASTER_PORT=os.environ.get("MASTER_PORT", "29531"))
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dg, feats, order, setup = build_inputs(cfg, args.features)
+    b, rb, dim = cfg["b"], cfg["dim"] * 4, cfg["dim"]
+    cap = int(cfg["cache_frac"] * cfg["n"]) // world
+    nb_total = (order.numel() + b - 1) // b
+    sampler = BatchSampler(dg, cfg["fanouts"], b)
+    engine = GpuShardEngine(rank, world, cap, feats, sampler.max_uniq)
+    ops = GpuShardOps(world, sampler.max_uniq, rb)
+    sc = ShardedFeatureCache(rank, world, engine, ops, dim)
+    tables = pcg_tables(pcg_states(RUN_SEED, range(nb_total)))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    order_host = order.cpu().numpy().astype(np.int32)
+    seeds_pinned = torch.from_numpy(order_host).pin_memory()
+    out_ids = torch.empty(sampler.max_uniq, dtype=torch.int32).pin_memory()
+
+    def one_round(j, host_fed=False):
+        i = (j * world + rank) % nb_total
+        lo, hi = i * b, min((i + 1) * b, order.numel())
+        src = seeds_pinned[lo:hi] if host_fed else order[lo:hi]
+        sampler.load_seeds(src)
+        sampler.run(tables[i])
+        u = int(sampler.num_uniq.item())
+        rows, codes = sc.step(sampler.uniq[:u])
+        if host_fed:
+            out_ids[:u].copy_(sampler.uniq[:u], non_blocking=True)
+        return u
+
+    for j in range(args.warmup):
+        one_round(j)
+    torch.cuda.synchronize()
+    c0 = engine.counters.clone()
+    dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record()
+            one_round(args.warmup + k)
+            ev[k][1].record()
+        torch.cuda.synchronize()
+    dist.barrier()
+    total_ms = sum(s.elapsed_time(e) for s, e in ev)
+    d = engine.counters - c0
+    dist.all_reduce(d)
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    q, own, peer, hst = (int(x) for x in d[:4].tolist())
+    # e2e: seeds H2D from pinned host, distinct IDs D2H, every round
+    e2e_ms, h2d, d2h = [], 0, 0
+    for k in range(max(3, min(args.steps, 50))):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        u = one_round(args.warmup + args.steps + k, host_fed=True)
+        e1.record()
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+        h2d += b * 4
+        d2h += u * 4
+    t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    n_e2e = len(e2e_ms)
+    out = {
+        "metric": METRIC, "value": round(world * args.steps / (total_ms * 1e-3), 2), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32 ids / u53 PCG64 keys / fp32 rows moved",
+        "data": "synthetic (GPU power-law generator, seed 1; hashed fp32 features)",
+        "config": {"workload": cfg["workload"], "num_nodes": cfg["n"], "csr_entries": dg.num_edges,
+                   "feature_dim": cfg["dim"], "fanouts": list(cfg["fanouts"]), "batch": b,
+                   "cache_rows_per_gpu": cap, "features": args.features,
+                   "parallelism": f"dp{world} + node-ID-sharded FIFO cache (home = v % {world}), NCCL all-to-all",
+                   "l2": "flushed between timed steps (256 MB write, outside the events)",
+                   "step": f"one round = {world} mini-batches (one per GPU)"},
+        "feature_gbs": round(q * rb / (total_ms * 1e-3) / 1e9, 2),
+        "hit_pct": round(100.0 * (own + peer + hst) / max(q, 1), 2),
+        "peer_hit_pct": round(100.0 * peer / max(q, 1), 2),
+        "e2e": {"value": round(world * n_e2e / (float(t.item()) * 1e-3), 2), "unit": UNIT,
+                "h2d_bytes_per_step": int(h2d / n_e2e), "d2h_bytes_per_step": int(d2h / n_e2e)},
+        "gpu_launches": (3 * len(cfg["fanouts"]) + 4 + 3 + 5 * world) * args.steps,
+        "clocks": clk.summary(), "setup": setup,
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    dist.destroy_process_group()
+
+
 def run_reference(args, cfg):
     rank, local_rank, world = dist_env()
     if rank != 0:
@@ -415,12 +519,15 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--features", choices=["host", "hbm"], default="host")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="use the multi-GPU sharded engine even at N=1")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif dist_env()[2] > 1 or args.sharded:
+        run_sharded(args, cfg)
     else:
         run_bgl(args, cfg)
 

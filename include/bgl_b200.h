@@ -132,6 +132,11 @@ int bgl_cache_reset(bgl_cache_t cache, void* stream);
 /* Size the per-batch scratch for batches of up to max_batch distinct IDs
  * (allocates; call outside CUDA-graph capture). */
 int bgl_cache_reserve_batch(bgl_cache_t cache, int64_t max_batch);
+/* Multi-GPU: this single-shard handle is shard `shard_index` of
+ * `num_global_shards` (node v lives on GPU v % num_global_shards,
+ * cachesim.py:505-506); lookups code a hit D when worker == shard_index,
+ * else P. Single-process handles keep the default (0 of num_shards). */
+int bgl_cache_set_shard(bgl_cache_t cache, int32_t shard_index, int32_t num_global_shards);
 /* Device pointers of the ring feature rows ([num_shards*shard_capacity][row_bytes]). */
 void* bgl_cache_rows(bgl_cache_t cache);
 /* Classify every query against the pre-batch state (cachesim.py:504-525):
@@ -202,6 +207,19 @@ int bgl_select_pending(const int32_t* shard, int64_t len, const uint8_t* flags, 
  * -shift[i]). seq_off: device int64[S+1]; shift: device int64[S]. */
 int bgl_interleave(const int32_t* seq_concat, const int64_t* seq_off, const int64_t* shift,
                    int32_t S, int64_t total, int32_t* out, void* stream);
+
+/* ---------------------------------------------------------------- multi-GPU exchange
+ * Node-ID sharding of the cache across GPUs (home of v = v % H,
+ * cachesim.py:505-506). Stable split of a sorted batch into H ascending
+ * buckets (out_ids, home-major), out_pos[i] = position of out_ids[i] in the
+ * batch, counts_dev[h] = bucket sizes. Then the homes' rows come back and
+ * bgl_scatter_rows puts row i at out[pos[i]]. */
+size_t bgl_partition_workspace(int64_t max_n, int32_t num_homes);
+int bgl_partition_by_home(const int32_t* ids, const int64_t* n_dev, int64_t max_n, int32_t num_homes,
+                          int32_t* out_ids, int32_t* out_pos, int64_t* counts_dev, void* workspace,
+                          void* stream);
+int bgl_scatter_rows(const int32_t* pos, const int64_t* n_dev, int64_t max_n, const void* rows,
+                     int64_t row_bytes, void* out, void* stream);
 
 /* ---------------------------------------------------------------- pipeline staging
  * Step staging for the CUDA-graph-captured pipeline (no reference

@@ -44,6 +44,7 @@ PROTOTYPES = {
     "bgl_cache_reset": (ctypes.c_int, [c_vp, c_vp]),
     "bgl_cache_reserve_batch": (ctypes.c_int, [c_vp, c_i64]),
     "bgl_cache_rows": (c_vp, [c_vp]),
+    "bgl_cache_set_shard": (ctypes.c_int, [c_vp, c_i32, c_i32]),
     "bgl_cache_lookup": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "bgl_cache_insert": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "bgl_cache_export": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
@@ -54,7 +55,10 @@ PROTOTYPES = {
                                      c_vp, c_vp, c_vp, c_vp]),
     "bgl_select_pending": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "bgl_interleave": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp]),
-    "bgl_stage_batch": (ctypes.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "bgl_partition_workspace": (c_sz, [c_i64, c_i32]),
+    "bgl_partition_by_home": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "bgl_scatter_rows": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp]),
+    "bgl_stage_batch":(ctypes.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
 }
 
 _lib = None

@@ -38,6 +38,8 @@ struct bgl_cache {
     int64_t list_cap = 0;
     int64_t* tile_counts = nullptr;   // [max_tiles][d+1] (exclusive offsets after scan)
     int64_t max_tiles = 0;
+    int32_t shard_index = 0;     // global shard of this handle (multi-GPU: rank)
+    int32_t global_shards = 0;   // 0 = d (single process)
 };
 
 namespace bgl {
@@ -50,7 +52,7 @@ constexpr int kMaxLevels = 65;   // d <= 64 plus the host level
 enum : uint8_t { kD = 0, kP = 1, kH = 2, kM = 3 };
 
 __global__ void lookup_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ n_dev, int32_t worker,
-                              int32_t d, int64_t C, const int32_t* __restrict__ slot_of,
+                              int32_t shard, int32_t d, int64_t C, const int32_t* __restrict__ slot_of,
                               const int32_t* __restrict__ hslot_of, uint8_t* __restrict__ codes,
                               int64_t* __restrict__ src_row, int64_t* __restrict__ counters) {
     const int64_t n = *n_dev;
@@ -62,7 +64,7 @@ __global__ void lookup_kernel(const int32_t* __restrict__ ids, const int64_t* __
         uint8_t code;
         int64_t src = -1;
         if (s >= 0) {
-            code = (h == worker) ? kD : kP;
+            code = (h + shard == worker) ? kD : kP;
             src = (int64_t)h * C + s;
         } else if (hslot_of != nullptr && hslot_of[v] >= 0) {
             code = kH;
@@ -198,7 +200,8 @@ miss_scatter_kernel(const int32_t* __restrict__ sorted_ids, const int64_t* __res
 // and an already sorted, distinct batch: classify, count and write the two
 // ascending lists (device-missed, full-missed) with a decoupled look-back.
 __global__ void __launch_bounds__(kCThreads)
-lookup_fused_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ n_dev, int32_t worker, int64_t C,
+lookup_fused_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ n_dev, int32_t worker, int32_t shard,
+                    int64_t C,
                     const int32_t* __restrict__ slot_of, const int32_t* __restrict__ hslot_of,
                     uint8_t* __restrict__ codes, int64_t* __restrict__ src_row, int64_t* __restrict__ counters,
                     ScanState ss, int32_t* __restrict__ lists, int64_t list_cap, int64_t* __restrict__ mcount) {
@@ -225,7 +228,7 @@ lookup_fused_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__
             uint8_t code;
             int64_t src = -1;
             if (s >= 0) {
-                code = (worker == 0) ? kD : kP;
+                code = (worker == shard) ? kD : kP;
                 src = s;
             } else {
                 dm = true;
@@ -479,19 +482,20 @@ int bgl_cache_lookup(bgl_cache_t c, const int32_t* ids, const int64_t* n_dev, in
                      const int32_t* sorted_ids, const int64_t* n_sorted_dev, int64_t max_sorted, uint8_t* codes,
                      int64_t* src_row, int64_t* counters, void* stream) {
     BGL_CHECK_ARG(c && ids && n_dev && sorted_ids && n_sorted_dev && counters, "bgl_cache_lookup: null pointer");
-    BGL_CHECK_ARG(worker >= 0 && worker < c->d, "worker device out of range");
+    const int32_t nglobal = c->global_shards > 0 ? c->global_shards : c->d;
+    BGL_CHECK_ARG(worker >= 0 && worker < nglobal, "worker device out of range");
     BGL_CHECK_ARG(max_sorted <= c->list_cap, "batch larger than reserved (call bgl_cache_reserve_batch)");
     cudaStream_t st = as_stream(stream);
     if (c->d == 1 && ids == sorted_ids && n_dev == n_sorted_dev) {
         const int64_t ntiles = std::max<int64_t>(1, ceil_div(max_sorted, kCTile));
         BGL_TRY(reset_scan_state(c->tile_counts, 2, ntiles, st));
         lookup_fused_kernel<<<(unsigned)ntiles, kCThreads, 0, st>>>(
-            ids, n_dev, worker, c->C, c->slot_of, c->hslot_of, codes, src_row, counters,
+            ids, n_dev, worker, c->shard_index, c->C, c->slot_of, c->hslot_of, codes, src_row, counters,
             make_scan_state(c->tile_counts, 2, ntiles), c->lists, c->list_cap, c->mcount);
         return launch_status("lookup_fused_kernel");
     }
     if (max_n > 0) {
-        lookup_kernel<<<grid_for(max_n, 256), 256, 0, st>>>(ids, n_dev, worker, c->d, c->C, c->slot_of, c->hslot_of,
+        lookup_kernel<<<grid_for(max_n, 256), 256, 0, st>>>(ids, n_dev, worker, c->shard_index, c->d, c->C, c->slot_of, c->hslot_of,
                                                             codes, src_row, counters);
         BGL_TRY(launch_status("lookup_kernel"));
     }
@@ -550,3 +554,13 @@ int bgl_cache_export(bgl_cache_t c, int64_t* dev_slots_host, int64_t* dev_tails_
 }
 
 }  // extern "C"
+
+extern "C" int bgl_cache_set_shard(bgl_cache_t c, int32_t shard_index, int32_t num_global_shards) {
+    BGL_CHECK_ARG(c, "null cache");
+    BGL_CHECK_ARG(num_global_shards >= 1 && shard_index >= 0 && shard_index < num_global_shards,
+                  "shard index out of range");
+    BGL_CHECK_ARG(c->d == 1 || num_global_shards == c->d, "a multi-shard handle is its own global sharding");
+    c->shard_index = shard_index;
+    c->global_shards = num_global_shards;
+    return BGL_OK;
+}

@@ -1,0 +1,151 @@
+// Multi-GPU exchange helpers for the node-ID-sharded cache (home of node v is
+// GPU v % H, gnnio/cachesim.py:505-506):
+//   partition  stable split of a sorted batch by home -> H ascending buckets
+//              (the insert order each home needs, cachesim.py:527-528) and the
+//              position of every bucketed ID in the batch;
+//   scatter    rows returned by the homes back into batch order.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace bgl {
+
+constexpr int kXThreads = 256;
+constexpr int kXRounds = 4;
+constexpr int kXTile = kXThreads * kXRounds;
+constexpr int kXMaxHomes = 64;
+
+__global__ void __launch_bounds__(kXThreads)
+home_count_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ n_dev, int32_t H,
+                  int64_t* __restrict__ tile_counts) {
+    __shared__ int32_t s_cnt[kXMaxHomes];
+    const int64_t n = *n_dev;
+    for (int h = threadIdx.x; h < H; h += blockDim.x) s_cnt[h] = 0;
+    __syncthreads();
+    for (int r = 0; r < kXRounds; ++r) {
+        const int64_t e = blockIdx.x * (int64_t)kXTile + r * kXThreads + threadIdx.x;
+        const int h = e < n ? ids[e] % H : -1;
+        for (int y = 0; y < H; ++y) {
+            const unsigned m = __ballot_sync(0xffffffffu, h == y);
+            if (lane_id() == 0 && m) atomicAdd(&s_cnt[y], __popc(m));
+        }
+    }
+    __syncthreads();
+    for (int h = threadIdx.x; h < H; h += blockDim.x) tile_counts[blockIdx.x * (int64_t)H + h] = s_cnt[h];
+}
+
+// one block: per-home exclusive offsets over (home, tile) in home-major order
+__global__ void home_scan_kernel(int64_t* __restrict__ tile_counts, int64_t ntiles, int32_t H,
+                                 int64_t* __restrict__ counts_out) {
+    __shared__ int64_t s_red[kXThreads / 32 + 1];
+    int64_t carry = 0;
+    for (int h = 0; h < H; ++h) {
+        int64_t home_total = 0;
+        for (int64_t b = 0; b < ntiles; b += blockDim.x) {
+            const int64_t t = b + threadIdx.x;
+            const int64_t v = t < ntiles ? tile_counts[t * H + h] : 0;
+            int64_t tot;
+            const int64_t ex = block_excl_scan(v, s_red, &tot);
+            if (t < ntiles) tile_counts[t * H + h] = carry + home_total + ex;
+            home_total += tot;
+        }
+        if (threadIdx.x == 0) counts_out[h] = home_total;
+        carry += home_total;
+    }
+}
+
+__global__ void __launch_bounds__(kXThreads)
+home_scatter_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ n_dev, int32_t H,
+                    const int64_t* __restrict__ tile_off, int32_t* __restrict__ out_ids,
+                    int32_t* __restrict__ out_pos) {
+    constexpr int NW = kXThreads / 32;
+    __shared__ int32_t s_w[NW][kXMaxHomes];
+    __shared__ int64_t s_run[kXMaxHomes];
+    const int64_t n = *n_dev;
+    const int lane = lane_id(), wid = warp_id();
+    const unsigned lt = (1u << lane) - 1u;
+    for (int h = threadIdx.x; h < H; h += blockDim.x) s_run[h] = tile_off[blockIdx.x * (int64_t)H + h];
+    __syncthreads();
+    for (int r = 0; r < kXRounds; ++r) {
+        const int64_t e = blockIdx.x * (int64_t)kXTile + r * kXThreads + threadIdx.x;
+        const int32_t v = e < n ? ids[e] : 0;
+        const int h = e < n ? v % H : -1;
+        int rank = 0;
+        for (int y = 0; y < H; ++y) {
+            const unsigned m = __ballot_sync(0xffffffffu, h == y);
+            if (h == y) rank = __popc(m & lt);
+            if (lane == 0) s_w[wid][y] = __popc(m);
+        }
+        __syncthreads();
+        if (h >= 0) {
+            int64_t p = s_run[h] + rank;
+            for (int w = 0; w < wid; ++w) p += s_w[w][h];
+            out_ids[p] = v;
+            out_pos[p] = (int32_t)e;
+        }
+        __syncthreads();
+        for (int y = threadIdx.x; y < H; y += blockDim.x) {
+            int64_t add = 0;
+            for (int w = 0; w < NW; ++w) add += s_w[w][y];
+            s_run[y] += add;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void scatter_rows_kernel(const int32_t* __restrict__ pos, const int64_t* __restrict__ n_dev,
+                                    const unsigned char* __restrict__ rows, int64_t rb,
+                                    unsigned char* __restrict__ out) {
+    const int64_t n = *n_dev;
+    const int lane = lane_id();
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = w; i < n; i += nw) {
+        const unsigned char* s = rows + i * rb;
+        unsigned char* d = out + (int64_t)pos[i] * rb;
+        if ((rb & 15) == 0) {
+            for (int64_t b = (int64_t)lane * 16; b < rb; b += 32 * 16)
+                *reinterpret_cast<uint4*>(d + b) = *reinterpret_cast<const uint4*>(s + b);
+        } else {
+            for (int64_t b = (int64_t)lane * 4; b < rb; b += 32 * 4)
+                *reinterpret_cast<uint32_t*>(d + b) = *reinterpret_cast<const uint32_t*>(s + b);
+        }
+    }
+}
+
+}  // namespace bgl
+
+using namespace bgl;
+
+extern "C" {
+
+size_t bgl_partition_workspace(int64_t max_n, int32_t num_homes) {
+    return (size_t)std::max<int64_t>(1, ceil_div(max_n, kXTile)) * num_homes * 8 + 256;
+}
+
+int bgl_partition_by_home(const int32_t* ids, const int64_t* n_dev, int64_t max_n, int32_t num_homes,
+                          int32_t* out_ids, int32_t* out_pos, int64_t* counts_dev, void* workspace, void* stream) {
+    BGL_CHECK_ARG(num_homes >= 1 && num_homes <= kXMaxHomes, "num_homes must be in [1, 64]");
+    BGL_CHECK_ARG(ids && n_dev && out_ids && out_pos && counts_dev && workspace, "bgl_partition_by_home: null");
+    cudaStream_t st = as_stream(stream);
+    const int64_t ntiles = std::max<int64_t>(1, ceil_div(max_n, kXTile));
+    int64_t* tc = reinterpret_cast<int64_t*>(workspace);
+    home_count_kernel<<<(unsigned)ntiles, kXThreads, 0, st>>>(ids, n_dev, num_homes, tc);
+    BGL_TRY(launch_status("home_count_kernel"));
+    home_scan_kernel<<<1, kXThreads, 0, st>>>(tc, ntiles, num_homes, counts_dev);
+    BGL_TRY(launch_status("home_scan_kernel"));
+    home_scatter_kernel<<<(unsigned)ntiles, kXThreads, 0, st>>>(ids, n_dev, num_homes, tc, out_ids, out_pos);
+    return launch_status("home_scatter_kernel");
+}
+
+int bgl_scatter_rows(const int32_t* pos, const int64_t* n_dev, int64_t max_n, const void* rows, int64_t row_bytes,
+                     void* out, void* stream) {
+    BGL_CHECK_ARG(pos && n_dev && rows && out, "bgl_scatter_rows: null pointer");
+    BGL_CHECK_ARG(row_bytes > 0 && row_bytes % 4 == 0, "row_bytes must be a positive multiple of 4");
+    if (max_n <= 0) return BGL_OK;
+    scatter_rows_kernel<<<grid_for(max_n * 32, 256, 8), 256, 0, as_stream(stream)>>>(
+        pos, n_dev, (const unsigned char*)rows, row_bytes, (unsigned char*)out);
+    return launch_status("scatter_rows_kernel");
+}
+
+}  // extern "C"

@@ -57,7 +57,10 @@ class FeatureCacheEngine:
     engine places shard h on GPU h (see pipeline.py).
     """
 
-    def __init__(self, cfg: CacheConfig, features: torch.Tensor, max_batch: int):
+    def __init__(self, cfg: CacheConfig, features: torch.Tensor, max_batch: int,
+                 shard: tuple[int, int] | None = None):
+        """shard = (rank, world): this engine is home shard `rank` of a
+        node-ID-sharded cache over `world` GPUs (see distributed.py)."""
         if cfg.policy != "fifo":
             raise NotImplementedError("only BGL's FIFO cache runs on the device")
         if features.dim() != 2 or not features.is_contiguous():
@@ -69,6 +72,10 @@ class FeatureCacheEngine:
         self.table = table_pointer(features)
         self.dev = FifoCacheDevice(cfg, self.num_nodes, self.row_bytes)
         self.dev.reserve(self.num_nodes, max_batch)
+        if shard is not None:
+            if cfg.num_devices != 1:
+                raise ValueError("a shard engine holds one device level (num_devices=1)")
+            _lib.check(_lib.load().bgl_cache_set_shard(self.dev.handle, int(shard[0]), int(shard[1])))
         self.state = CacheEngineState(cfg=cfg, engine=self.dev, policy="fifo")
         self.max_batch = int(max_batch)
         self.codes = torch.empty(max(max_batch, 1), dtype=torch.uint8, device="cuda")
@@ -83,17 +90,19 @@ class FeatureCacheEngine:
 
     def retrieve_device(self, ids: torch.Tensor, n_dev: torch.Tensor, max_n: int, worker: int,
                         counters: torch.Tensor | None = None, stream=None, out: torch.Tensor | None = None,
-                        events=None):
+                        events=None, codes: torch.Tensor | None = None):
         """Fully device-resident step: ids = sorted distinct int32 node IDs
         (e.g. BatchSampler.uniq) with the live count in n_dev. Rows land in
-        `out` (default self.out) in batch order; codes in self.codes."""
+        `out` (default self.out) in batch order; codes in `codes` (default
+        self.codes)."""
         lib = _lib.load()
         st = _lib.stream_ptr(stream)
         cnt = (self.counters if counters is None else counters).data_ptr()
         out = self.out if out is None else out
+        codes = self.codes if codes is None else codes
         h = self.dev.handle
         _lib.check(lib.bgl_cache_lookup(h, ids.data_ptr(), n_dev.data_ptr(), max_n, worker, ids.data_ptr(),
-                                        n_dev.data_ptr(), max_n, self.codes.data_ptr(), self.src_row.data_ptr(),
+                                        n_dev.data_ptr(), max_n, codes.data_ptr(), self.src_row.data_ptr(),
                                         cnt, st))
         if events is not None:
             events[0].record()
