@@ -36,6 +36,11 @@ CONFIGS = {
                         "FIFO cache 10% of nodes in HBM, proximity (BFS, S=4) ordering",
                n=2_400_000, avg_degree=51, dim=100, labels=47, train=0.08, fanouts=(15, 10, 5), b=1024,
                cache_frac=0.10, S=4),
+    "c3": dict(workload="ogbn-papers100M-shaped synthetic power-law graph (111M nodes, ~1.55B undirected edges), "
+                        "128-d fp32 features (56.9 GB) in pinned host memory, fanout [15,10,5], batch 1024, "
+                        "FIFO cache 10% of nodes (11.1M rows) in HBM, proximity (BFS, S=4) ordering; 1 GPU",
+               n=111_059_956, avg_degree=29, dim=128, labels=172, train=0.0108, fanouts=(15, 10, 5), b=1024,
+               cache_frac=0.10, S=4),
     "c1": dict(workload="synthetic power-law graph 100K nodes / 1M edges, 128-d fp32 features in pinned host "
                         "memory, fanout [10,5], batch 1024, FIFO cache 10% of nodes, BFS ordering",
                n=100_000, avg_degree=20, dim=128, labels=64, train=0.10, fanouts=(10, 5), b=1024,

@@ -201,7 +201,20 @@ def power_law_csr(n: int, avg_degree: int, seed: int, train_fraction: float, num
     src, dst = src[keep], dst[keep]
     key = torch.cat([src * n + dst, dst * n + src])
     del src, dst, keep
-    key = torch.unique(key)              # sorted, deduplicated (symmetric CSR, graph.py:88-107)
+    # sorted, deduplicated (symmetric CSR, graph.py:88-107); CUB sorts < 2^31
+    # items, so large graphs are deduplicated per source-node range
+    limit = 1 << 30
+    if key.numel() <= limit:
+        key = torch.unique(key)
+    else:
+        pieces = []
+        nchunks = (key.numel() + limit - 1) // limit * 2
+        for c in range(nchunks):
+            lo, hi = c * n // nchunks, (c + 1) * n // nchunks
+            pieces.append(torch.unique(key[(key >= lo * n) & (key < hi * n)]))
+        del key
+        key = torch.cat(pieces)
+        del pieces
     row = key // n
     col = (key - row * n).to(torch.int32)
     del key
