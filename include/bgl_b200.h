@@ -233,6 +233,11 @@ int bgl_stage_batch(const int32_t* order, int64_t total, int64_t batch_size, int
                     const uint64_t* tables, int64_t* batch_counter, int32_t* seeds_out,
                     int64_t* seed_count_out, uint64_t* table_out, int64_t* batch_index_out,
                     const int64_t* fed_count_dev, void* stream);
+/* Sync-free result hand-off: host_ids[0..n) = ids[0..*n_dev) and host_meta =
+ * {n, counters[0..8)} written straight into mapped pinned host memory
+ * (device aliases from bgl_host_device_pointer). counters may be NULL. */
+int bgl_d2h_result(const int32_t* ids, const int64_t* n_dev, int64_t max_n, const int64_t* counters,
+                   int32_t* host_ids, int64_t* host_meta, void* stream);
 
 #ifdef __cplusplus
 }

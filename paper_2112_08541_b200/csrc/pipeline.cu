@@ -1,6 +1,8 @@
 // Per-step staging for the CUDA-graph-captured mini-batch pipeline: the
 // batch index lives on the device, so one captured graph replays every step
 // of an epoch without host-side arguments.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace bgl {
@@ -24,6 +26,26 @@ __global__ void stage_batch_kernel(const int32_t* __restrict__ order, int64_t to
     }
 }
 
+// Result hand-off to the host without a host sync: the distinct IDs of the
+// batch (count known only on the device) and an 8-word counter block are
+// stored straight into mapped pinned host memory (posted PCIe writes).
+__global__ void d2h_result_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ n_dev,
+                                  const int64_t* __restrict__ counters, int32_t* __restrict__ host_ids,
+                                  int64_t* __restrict__ host_meta) {
+    const int64_t n = *n_dev;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nv = n >> 2;
+    const int4* src4 = reinterpret_cast<const int4*>(ids);
+    int4* dst4 = reinterpret_cast<int4*>(host_ids);
+    for (int64_t i = t0; i < nv; i += stride) dst4[i] = src4[i];
+    for (int64_t i = (nv << 2) + t0; i < n; i += stride) host_ids[i] = ids[i];
+    if (t0 == 0) {
+        host_meta[0] = n;
+        for (int k = 0; k < 8; ++k) host_meta[1 + k] = counters ? counters[k] : 0;
+    }
+}
+
 }  // namespace bgl
 
 using namespace bgl;
@@ -41,6 +63,15 @@ int bgl_stage_batch(const int32_t* order, int64_t total, int64_t batch_size, int
                                                           batch_counter, seeds_out, seed_count_out, table_out,
                                                           batch_index_out, fed_count_dev);
     return launch_status("stage_batch_kernel");
+}
+
+int bgl_d2h_result(const int32_t* ids, const int64_t* n_dev, int64_t max_n, const int64_t* counters,
+                   int32_t* host_ids, int64_t* host_meta, void* stream) {
+    BGL_CHECK_ARG(ids && n_dev && host_ids && host_meta, "bgl_d2h_result: null pointer");
+    BGL_CHECK_ARG(((uintptr_t)ids & 15) == 0 && ((uintptr_t)host_ids & 15) == 0, "buffers must be 16-byte aligned");
+    d2h_result_kernel<<<grid_for(std::max<int64_t>(max_n / 4, 1), 256, 2), 256, 0, as_stream(stream)>>>(
+        ids, n_dev, counters, host_ids, host_meta);
+    return launch_status("d2h_result_kernel");
 }
 
 }  // extern "C"

@@ -57,6 +57,12 @@ class MiniBatchPipeline:
         self.counters = torch.zeros(8, dtype=torch.int64, device="cuda")
         self.fed_seeds = torch.empty(self.b, dtype=torch.int32, device="cuda")
         self.fed_count = torch.zeros(1, dtype=torch.int64, device="cuda")
+        # host-fed mode results: distinct IDs + {n, counters} of each batch land
+        # in pinned host memory by zero-copy stores (no host sync per step)
+        self.host_ids = [torch.empty(self.max_uniq, dtype=torch.int32, pin_memory=True) for _ in range(2)]
+        self.host_meta = [torch.zeros(16, dtype=torch.int64, pin_memory=True) for _ in range(2)]
+        self._host_ids_dev = [_lib.host_device_pointer(t) for t in self.host_ids]
+        self._host_meta_dev = [_lib.host_device_pointer(t) for t in self.host_meta]
         # the cache/gather chain is the critical path (host link): its blocks are
         # dispatched ahead of the sampler's when both are pending
         self.s_stream = torch.cuda.Stream(priority=0)
@@ -100,6 +106,11 @@ class MiniBatchPipeline:
             self._sample(1 - parity, stream=self.s_stream, fed=fed)
         with torch.cuda.stream(self.c_stream):
             self._cache(parity, stream=self.c_stream)
+            if fed:
+                s = self.samplers[parity]
+                _lib.call("bgl_d2h_result", s.uniq.data_ptr(), s.num_uniq.data_ptr(), s.max_uniq,
+                          self.counters.data_ptr(), self._host_ids_dev[parity], self._host_meta_dev[parity],
+                          _lib.stream_ptr(self.c_stream))
         cur.wait_stream(self.s_stream)
         cur.wait_stream(self.c_stream)
 
@@ -146,6 +157,12 @@ class MiniBatchPipeline:
         self.prime(fed)
         g.replay()
         self.k += 1
+
+    def host_result(self, slot: int):
+        """(distinct IDs, counters) of the last host-fed batch that used
+        `slot`, read from pinned host memory (valid after a sync)."""
+        n = int(self.host_meta[slot][0])
+        return self.host_ids[slot][:n], self.host_meta[slot][1:9]
 
     # -- views of the last batch through the cache -----------------------------
     def last_slot(self) -> int:
