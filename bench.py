@@ -242,25 +242,28 @@ def run_bgl(args, cfg):
 
     # stage breakdown + gather roofline (serialised steps with events, after the timed region)
     R = 10
-    st_times = {k: [] for k in ("sample", "dedup", "lookup", "gather", "insert")}
-    g_bytes_host, g_ms, g_rows = [], [], []
+    st_times = {k: [] for k in ("sample", "dedup", "lookup_insert", "miss_gather", "hit_gather", "row_copy")}
+    g_bytes_host, g_ms, hbm_bytes, hbm_ms = [], [], [], []
+    prev_hits = None
     for _ in range(R):
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
         cb = pipe.counters.clone()
         flush.zero_()
-        pipe.step_serial(evs)
+        pipe.step_serial(evs)                  # sample(k+2) | front(k+1) | back(k)
         torch.cuda.synchronize()
-        ca = (pipe.counters - cb).cpu().tolist()
-        t = [evs[i].elapsed_time(evs[i + 1]) for i in range(5)]
+        ca = (pipe.counters - cb).cpu().tolist()   # lookup counters of batch k+1
+        t = [evs[i].elapsed_time(evs[i + 1]) for i in range(6)]
         for k, v in zip(st_times, t):
             st_times[k].append(v)
-        misses = ca[3] + ca[4]                 # H + M rows come from the feature store
+        misses = ca[3] + ca[4]                 # H + M rows of batch k+1 come from the feature store
         g_bytes_host.append(misses * rb)
-        g_rows.append(ca[0])
         g_ms.append(t[3])
+        if prev_hits is not None:              # hits of batch k were counted in the previous step
+            hbm_bytes.append(2 * prev_hits * rb)
+            hbm_ms.append(t[4])
+        prev_hits = ca[1] + ca[2]
     gather_ms = statistics.mean(g_ms)
     host_bytes = statistics.mean(g_bytes_host)
-    rows_mean = statistics.mean(g_rows)
     if args.features == "host":
         achieved = host_bytes / (gather_ms * 1e-3) / 1e9
         roof = {"bound": "host_link", "achieved": round(achieved, 2), "peak": round(peak_host, 2), "unit": "GB/s",
@@ -271,11 +274,13 @@ def run_bgl(args, cfg):
     else:
         hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
             if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
-        alg = 2 * rows_mean * rb
-        achieved = alg / (gather_ms * 1e-3) / 1e9
+        # both gathers read HBM here: misses (front) and hits (back), 2 x rows x rb each
+        alg = statistics.mean(g_bytes_host) * 2 + statistics.mean(hbm_bytes)
+        t_g = gather_ms + statistics.mean(hbm_ms)
+        achieved = alg / (t_g * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved / hbm, 3), "traffic": None, "kernel": "gather_v4_kernel",
-                "algorithmic_bytes_per_launch": int(alg)}
+                "frac": round(achieved / hbm, 3), "traffic": None, "kernel": "gather_v4_kernel (miss + hit)",
+                "algorithmic_bytes_per_launch": int(alg / 2)}
     prof = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{args.features}.json")
     if os.path.exists(prof):
         tr = json.load(open(prof))
@@ -304,8 +309,7 @@ def run_bgl(args, cfg):
         return (hi - lo) * 4
 
     pipe.reset()
-    feed(0)
-    pipe.prime(fed=True)
+    pipe.prime(fed=True, feed=feed)
     torch.cuda.synchronize()
     n_e2e = max(3, min(args.steps, 100))
     ce0 = pipe.counters.clone()
@@ -314,7 +318,7 @@ def run_bgl(args, cfg):
     for k in range(n_e2e):
         flush.zero_()
         eev[k][0].record()
-        h2d += feed(k + 1)             # H2D: next batch's seeds from pinned host memory
+        h2d += feed(k + pipe.lookahead)   # H2D: seeds of the batch sampled in this step, from pinned host
         pipe.step(fed=True)            # graph also stores this batch's distinct IDs + counters into pinned host
         eev[k][1].record()
     torch.cuda.synchronize()

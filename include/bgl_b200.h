@@ -156,6 +156,17 @@ int bgl_cache_lookup(bgl_cache_t cache, const int32_t* ids, const int64_t* n_dev
  * (aligned with sorted_ids) is copied into the slot its node lands in. */
 int bgl_cache_insert(bgl_cache_t cache, const int32_t* sorted_ids, int64_t max_sorted,
                      const void* batch_rows, int64_t* counters, void* stream);
+/* The same insert split in two for software pipelining: bgl_cache_insert_plan
+ * updates rings, indices, tails and counters now and records every device-
+ * level survivor as plan[y][r] = (batch position, slot) (int32 pairs, stride
+ * bgl_cache_plan_stride) with plan_count[y] survivors; bgl_cache_copy_rows
+ * later copies the survivors' rows (once the misses have arrived and the
+ * batch's hits have been read). */
+int64_t bgl_cache_plan_stride(bgl_cache_t cache, int64_t max_sorted);
+int bgl_cache_insert_plan(bgl_cache_t cache, const int32_t* sorted_ids, int64_t max_sorted,
+                          int32_t* plan, int64_t* plan_count, int64_t* counters, void* stream);
+int bgl_cache_copy_rows(bgl_cache_t cache, const int32_t* plan, const int64_t* plan_count,
+                        int64_t max_sorted, const void* batch_rows, void* stream);
 /* Synchronous export of the ring contents (int64, -1 = empty) and tails, in
  * the layout of FifoLevel.slots / .tail (cachesim.py:273-275). Any pointer may
  * be NULL. dev_slots: [num_shards][shard_capacity]; dev_tails: [num_shards]. */

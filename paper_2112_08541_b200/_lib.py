@@ -47,7 +47,10 @@ PROTOTYPES = {
     "bgl_cache_set_shard": (ctypes.c_int, [c_vp, c_i32, c_i32]),
     "bgl_cache_lookup": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "bgl_cache_insert": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
-    "bgl_cache_export": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "bgl_cache_plan_stride": (c_i64, [c_vp, c_i64]),
+    "bgl_cache_insert_plan": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "bgl_cache_copy_rows": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "bgl_cache_export":(ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "bgl_gather_rows": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_i32, c_i32, c_vp]),
     "bgl_synthetic_features": (ctypes.c_int, [c_i64, c_i64, c_i32, c_u64, c_vp, c_vp]),
     "bgl_bfs_workspace": (c_sz, [c_i64]),

@@ -293,7 +293,8 @@ __global__ void insert_kernel(const int32_t* __restrict__ sorted_ids, int32_t d,
                               int32_t* __restrict__ hslot_of, const int64_t* __restrict__ tails,
                               const int64_t* __restrict__ mcount, const int32_t* __restrict__ lists, int64_t list_cap,
                               const unsigned char* __restrict__ batch_rows, unsigned char* __restrict__ rows,
-                              int64_t rb, int64_t* __restrict__ counters) {
+                              int64_t rb, int64_t* __restrict__ counters, int32_t* __restrict__ plan,
+                              int64_t plan_stride) {
     const int y = blockIdx.y;
     const bool host = (y == d);
     const int64_t cap = host ? Ch : C;
@@ -321,8 +322,12 @@ __global__ void insert_kernel(const int32_t* __restrict__ sorted_ids, int32_t d,
             }
             ring[slot] = v;
             index[v] = (int32_t)slot;
+            if (!host && plan != nullptr) {   // deferred row copy (bgl_cache_copy_rows)
+                plan[2 * ((int64_t)y * plan_stride + r)] = pos;
+                plan[2 * ((int64_t)y * plan_stride + r) + 1] = (int32_t)slot;
+            }
         }
-        if (!host && batch_rows != nullptr) {
+        if (!host && batch_rows != nullptr && plan == nullptr) {
             const unsigned char* src = batch_rows + (int64_t)pos * rb;
             unsigned char* dst = rows + ((int64_t)y * C + slot) * rb;
             if ((rb & 15) == 0) {
@@ -338,19 +343,45 @@ __global__ void insert_kernel(const int32_t* __restrict__ sorted_ids, int32_t d,
 }
 
 __global__ void insert_finalize_kernel(int32_t d, int64_t C, int64_t Ch, int64_t* __restrict__ tails,
-                                       const int64_t* __restrict__ mcount, int64_t* __restrict__ counters) {
+                                       const int64_t* __restrict__ mcount, int64_t* __restrict__ counters,
+                                       int64_t* __restrict__ plan_count) {
     if (threadIdx.x != 0) return;
     int64_t ins = 0, ev = 0;
     for (int y = 0; y <= d; ++y) {
         const int64_t cap = (y == d) ? Ch : C;
-        if (cap == 0) continue;
         const int64_t M = mcount[y];
+        if (plan_count && y < d) plan_count[y] = M < cap ? M : cap;
+        if (cap == 0) continue;
         tails[y] = (tails[y] + M) % cap;
         ins += M;
         ev += M > cap ? M - cap : 0;
     }
     counters[5] += ins;
     counters[6] += ev;
+}
+
+// deferred survivor row copy: plan[y][r] = (batch position, ring slot)
+__global__ void copy_rows_kernel(const int32_t* __restrict__ plan, const int64_t* __restrict__ plan_count,
+                                 int64_t stride, int64_t C, const unsigned char* __restrict__ batch_rows,
+                                 unsigned char* __restrict__ rows, int64_t rb) {
+    const int y = blockIdx.y;
+    const int64_t cnt = plan_count[y];
+    const int lane = lane_id();
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = gw; r < cnt; r += nw) {
+        const int32_t pos = plan[2 * ((int64_t)y * stride + r)];
+        const int32_t slot = plan[2 * ((int64_t)y * stride + r) + 1];
+        const unsigned char* src = batch_rows + (int64_t)pos * rb;
+        unsigned char* dst = rows + ((int64_t)y * C + slot) * rb;
+        if ((rb & 15) == 0) {
+            for (int64_t b = (int64_t)lane * 16; b < rb; b += 32 * 16)
+                *reinterpret_cast<uint4*>(dst + b) = *reinterpret_cast<const uint4*>(src + b);
+        } else {
+            for (int64_t b = (int64_t)lane * 4; b < rb; b += 32 * 4)
+                *reinterpret_cast<uint32_t*>(dst + b) = *reinterpret_cast<const uint32_t*>(src + b);
+        }
+    }
 }
 
 }  // namespace bgl
@@ -523,11 +554,44 @@ int bgl_cache_insert(bgl_cache_t c, const int32_t* sorted_ids, int64_t max_sorte
         dim3 grid(gx, c->d + 1);
         insert_kernel<<<grid, threads, 0, st>>>(sorted_ids, c->d, c->C, c->Ch, c->rings, c->hring, c->slot_of,
                                                 c->hslot_of, c->tails, c->mcount, c->lists, c->list_cap,
-                                                (const unsigned char*)batch_rows, c->rows, c->rb, counters);
+                                                (const unsigned char*)batch_rows, c->rows, c->rb, counters, nullptr, 0);
         BGL_TRY(launch_status("insert_kernel"));
     }
-    insert_finalize_kernel<<<1, 32, 0, st>>>(c->d, c->C, c->Ch, c->tails, c->mcount, counters);
+    insert_finalize_kernel<<<1, 32, 0, st>>>(c->d, c->C, c->Ch, c->tails, c->mcount, counters, nullptr);
     return launch_status("insert_finalize_kernel");
+}
+
+int64_t bgl_cache_plan_stride(bgl_cache_t c, int64_t max_sorted) {
+    return c ? std::max<int64_t>(1, std::min<int64_t>(max_sorted, c->C)) : 0;
+}
+
+int bgl_cache_insert_plan(bgl_cache_t c, const int32_t* sorted_ids, int64_t max_sorted, int32_t* plan,
+                          int64_t* plan_count, int64_t* counters, void* stream) {
+    BGL_CHECK_ARG(c && sorted_ids && plan && plan_count && counters, "bgl_cache_insert_plan: null pointer");
+    cudaStream_t st = as_stream(stream);
+    const int64_t stride = bgl_cache_plan_stride(c, max_sorted);
+    const int64_t work = std::min<int64_t>(max_sorted, std::max(c->C, c->Ch));
+    if (work > 0) {
+        dim3 grid(grid_for(work * 32, 256, 8), c->d + 1);
+        insert_kernel<<<grid, 256, 0, st>>>(sorted_ids, c->d, c->C, c->Ch, c->rings, c->hring, c->slot_of,
+                                            c->hslot_of, c->tails, c->mcount, c->lists, c->list_cap, nullptr,
+                                            c->rows, c->rb, counters, plan, stride);
+        BGL_TRY(launch_status("insert_kernel"));
+    }
+    insert_finalize_kernel<<<1, 32, 0, st>>>(c->d, c->C, c->Ch, c->tails, c->mcount, counters, plan_count);
+    return launch_status("insert_finalize_kernel");
+}
+
+int bgl_cache_copy_rows(bgl_cache_t c, const int32_t* plan, const int64_t* plan_count, int64_t max_sorted,
+                        const void* batch_rows, void* stream) {
+    BGL_CHECK_ARG(c && plan && plan_count && batch_rows, "bgl_cache_copy_rows: null pointer");
+    BGL_CHECK_ARG(c->rb > 0, "cache was created without feature rows");
+    const int64_t stride = bgl_cache_plan_stride(c, max_sorted);
+    if (c->C == 0 || max_sorted <= 0) return BGL_OK;
+    dim3 grid(grid_for(stride * 32, 256, 8), c->d);
+    copy_rows_kernel<<<grid, 256, 0, as_stream(stream)>>>(plan, plan_count, stride, c->C,
+                                                          (const unsigned char*)batch_rows, c->rows, c->rb);
+    return launch_status("copy_rows_kernel");
 }
 
 int bgl_cache_export(bgl_cache_t c, int64_t* dev_slots_host, int64_t* dev_tails_host, int64_t* host_slots_host,

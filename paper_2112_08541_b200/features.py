@@ -124,6 +124,46 @@ class FeatureCacheEngine:
             events[2].record()
         return out
 
+    # -- split form for the software-pipelined step (pipeline.py) ----------------
+    def plan_buffers(self):
+        """(plan int32 [d, stride, 2], plan_count int64 [d]) for front/back."""
+        stride = int(_lib.load().bgl_cache_plan_stride(self.dev.handle, self.max_batch))
+        plan = torch.empty((self.cfg.num_devices, stride, 2), dtype=torch.int32, device="cuda")
+        return plan, torch.zeros(self.cfg.num_devices, dtype=torch.int64, device="cuda")
+
+    def front(self, ids, n_dev, max_n, worker, out, codes, src_row, plan, plan_count, counters, stream=None,
+              events=None):
+        """Lookup, insert-after-batch (indices/rings only, rows deferred to
+        back()), then the misses' rows from the feature store into `out`."""
+        lib = _lib.load()
+        st = _lib.stream_ptr(stream)
+        h = self.dev.handle
+        _lib.check(lib.bgl_cache_lookup(h, ids.data_ptr(), n_dev.data_ptr(), max_n, worker, ids.data_ptr(),
+                                        n_dev.data_ptr(), max_n, codes.data_ptr(), src_row.data_ptr(),
+                                        counters.data_ptr(), st))
+        _lib.check(lib.bgl_cache_insert_plan(h, ids.data_ptr(), max_n, plan.data_ptr(), plan_count.data_ptr(),
+                                             counters.data_ptr(), st))
+        if events is not None:
+            events[0].record()
+        ctas = 0 if self.features.is_cuda else self.miss_ctas
+        _lib.check(lib.bgl_gather_rows(ids.data_ptr(), src_row.data_ptr(), n_dev.data_ptr(), max_n,
+                                       self.dev.rows_ptr() or None, self.table, self.row_bytes, out.data_ptr(), 2,
+                                       ctas, st))
+
+    def back(self, ids, n_dev, max_n, out, src_row, plan, plan_count, stream=None, events=None):
+        """Hits' rows from the HBM ring, then the survivors' rows into the
+        ring (after the hits were read: the same-batch eviction hazard)."""
+        lib = _lib.load()
+        st = _lib.stream_ptr(stream)
+        _lib.check(lib.bgl_gather_rows(ids.data_ptr(), src_row.data_ptr(), n_dev.data_ptr(), max_n,
+                                       self.dev.rows_ptr() or None, self.table, self.row_bytes, out.data_ptr(), 1,
+                                       0, st))
+        if events is not None:
+            events[0].record()
+        if self.dev.rows_ptr():
+            _lib.check(lib.bgl_cache_copy_rows(self.dev.handle, plan.data_ptr(), plan_count.data_ptr(), max_n,
+                                               out.data_ptr(), st))
+
     def retrieve(self, batch_ids, batch_index: int):
         """rows = F[batch_ids] for one sorted distinct batch; returns
         (rows [U, dim] on the device, outcome codes uint8 [U])."""

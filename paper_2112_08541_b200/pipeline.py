@@ -1,25 +1,30 @@
 """The fused per-mini-batch preprocessing pipeline on one B200.
 
 One mini-batch of BGL's data path:
-    stage seeds  (device-resident proximity schedule, bgl_stage_batch)
-    sample       H hops, PCG64 replay, fused dedup mark (bgl_sample_hop x H)
-    dedup        sorted distinct set                    (bgl_unique_sorted)
-    lookup       FIFO cache, pre-batch state            (bgl_cache_lookup)
-    gather       hits from HBM ring slots, misses zero-copy from pinned host
-                 (bgl_gather_rows)
-    insert       insert-after-batch + row copy into the ring (bgl_cache_insert)
+    stage   seeds + PCG64 table of the batch (bgl_stage_batch)
+    sample  H hops, PCG64 replay, fused dedup mark (bgl_sample_hop x H)
+    dedup   sorted distinct set                    (bgl_unique_sorted)
+    front   FIFO lookup vs the pre-batch state (bgl_cache_lookup), insert-
+            after-batch of indices/rings (bgl_cache_insert_plan), misses'
+            rows zero-copy from pinned host memory over the host link
+            (bgl_gather_rows, misses only)
+    back    hits' rows from the HBM ring slots (bgl_gather_rows, hits only),
+            then the survivors' rows into their new slots (bgl_cache_copy_rows)
 
-Software pipelining (the paper's overlap of sampling with feature retrieval,
-PAPER.md:536-576): sampling is cache-independent (its rng is keyed by the
-batch index, sampler.py:138), so step k runs cache+gather of batch k on one
-stream while batch k+1 is sampled on another, with double-buffered sampler
-and row buffers. The cache state machine still sees batches strictly in
-order. Every step is captured once per buffer parity in a CUDA graph and
-replayed; counts, batch index and PCG64 tables stay on the device.
-
-Outputs of batch i (distinct IDs, rows, outcome codes, counters) equal the
-reference's `simulate_epoch` trace / `simulate` report rows and
-`F[trace.batches[i]]`.
+Software pipeline (the paper overlaps sampling with feature retrieval,
+PAPER.md:536-576). Step k runs, as three concurrent branches,
+    back(k)  ||  front(k+1)  ||  sample(k+2)
+so the host link (front) streams misses back to back while the ring-row work
+of the previous batch and the sampling of the next ones run beside it.
+Correctness: front(k+1) only needs front(k)'s index update (previous step);
+back(k) needs front(k) (previous step) and back(k-1)'s row copy (previous
+step); within back(k) the hits are read before any survivor row is written
+(the same-batch eviction hazard of SURVEY.md §7). Sampling is cache-
+independent (rng keyed by the batch index, sampler.py:138). The cache state
+machine therefore sees batches strictly in order and every output equals the
+reference's. Buffers: samplers by batch % 3, rows / codes / src rows / insert
+plans by batch % 2; the step is captured once per phase (k % 6) in a CUDA
+graph and replayed.
 """
 
 from __future__ import annotations
@@ -32,11 +37,16 @@ from .features import FeatureCacheEngine
 from .graph import DeviceGraph
 from .sampler import BatchSampler, pcg_states, pcg_tables
 
+NS, NB = 3, 2          # sampler buffers, row/plan buffers
+PHASES = 6             # lcm(NS, NB)
+
 
 class MiniBatchPipeline:
+    lookahead = 2      # batch k+2 is sampled during step k
+
     def __init__(self, dg: DeviceGraph, fanouts, batch_size: int, order: torch.Tensor, seed: int,
                  cache_cfg: CacheConfig, features: torch.Tensor, num_batches: int | None = None,
-                 sampler_ctas: int | None = None):
+                 sampler_ctas: int = 0):
         if cache_cfg.num_devices != 1:
             raise ValueError("single-GPU pipeline: one cache shard (num_devices=1)")
         self.dg = dg
@@ -44,40 +54,41 @@ class MiniBatchPipeline:
         self.order = order.to(device="cuda", dtype=torch.int32).contiguous()
         total = int(self.order.numel())
         self.num_batches = int(num_batches or (total + self.b - 1) // self.b)
-        if sampler_ctas is None:
-            sampler_ctas = 0          # the miss gather takes only 2 warps per SM
-        self.samplers = [BatchSampler(dg, fanouts, self.b, max_ctas=sampler_ctas) for _ in range(2)]
+        self.samplers = [BatchSampler(dg, fanouts, self.b, max_ctas=sampler_ctas) for _ in range(NS)]
         self.max_uniq = self.samplers[0].max_uniq
         self.engine = FeatureCacheEngine(cache_cfg, features, max_batch=self.max_uniq)
-        self.outs = [self.engine.out, torch.empty_like(self.engine.out)]
+        self.outs = [self.engine.out] + [torch.empty_like(self.engine.out) for _ in range(NB - 1)]
+        self.codes_buf = [torch.empty(self.max_uniq, dtype=torch.uint8, device="cuda") for _ in range(NB)]
+        self.src_row = [torch.empty(self.max_uniq, dtype=torch.int64, device="cuda") for _ in range(NB)]
+        self.plans = [self.engine.plan_buffers() for _ in range(NB)]
         self.tables = pcg_tables(pcg_states(seed, range(self.num_batches)))
-        self.table_stage = [torch.empty((65, 4), dtype=torch.int64, device="cuda") for _ in range(2)]
+        self.table_stage = [torch.empty((65, 4), dtype=torch.int64, device="cuda") for _ in range(NS)]
         self.batch_counter = torch.zeros(1, dtype=torch.int64, device="cuda")
-        self.batch_index = torch.zeros(2, dtype=torch.int64, device="cuda")
+        self.batch_index = torch.zeros(NS, dtype=torch.int64, device="cuda")
         self.counters = torch.zeros(8, dtype=torch.int64, device="cuda")
         self.fed_seeds = torch.empty(self.b, dtype=torch.int32, device="cuda")
         self.fed_count = torch.zeros(1, dtype=torch.int64, device="cuda")
-        # host-fed mode results: distinct IDs + {n, counters} of each batch land
-        # in pinned host memory by zero-copy stores (no host sync per step)
-        self.host_ids = [torch.empty(self.max_uniq, dtype=torch.int32, pin_memory=True) for _ in range(2)]
-        self.host_meta = [torch.zeros(16, dtype=torch.int64, pin_memory=True) for _ in range(2)]
+        # host-fed results: distinct IDs + {n, counters} of each batch stored
+        # into pinned host memory by zero-copy writes (no host sync per step)
+        self.host_ids = [torch.empty(self.max_uniq, dtype=torch.int32, pin_memory=True) for _ in range(NB)]
+        self.host_meta = [torch.zeros(16, dtype=torch.int64, pin_memory=True) for _ in range(NB)]
         self._host_ids_dev = [_lib.host_device_pointer(t) for t in self.host_ids]
         self._host_meta_dev = [_lib.host_device_pointer(t) for t in self.host_meta]
-        # the cache/gather chain is the critical path (host link): its blocks are
-        # dispatched ahead of the sampler's when both are pending
-        self.s_stream = torch.cuda.Stream(priority=0)
-        self.c_stream = torch.cuda.Stream(priority=-5)
+        import os
+        fp = int(os.environ.get("BGL_FRONT_PRIORITY", "0"))
+        # back, front (host-link critical path), sample
+        self.streams = [torch.cuda.Stream(), torch.cuda.Stream(priority=fp), torch.cuda.Stream()]
         self.graphs: dict = {}
-        self.k = 0              # batches that went through the cache
-        self.primed = False     # batch k already sampled into samplers[k % 2]
+        self.k = 0                # batches completed (rows ready)
+        self.primed = False
         s = self.samplers[0]
-        hops = 3 * s.H                                  # scan + warp + heavy per hop
-        gathers = 1 if features.is_cuda else 2
-        # stage, hops, dedup (mark seeds, emit, reset), lookup (fused), gather(s), insert + finalize
-        self.kernels_per_step = 1 + hops + 3 + 1 + gathers + 2
+        # stage + H x (scan, warp, heavy) + dedup (mark seeds, emit, reset) + lookup + insert(2)
+        # + miss gather + hit gather + row copy
+        self.kernels_per_step = 1 + 3 * s.H + 3 + 1 + 2 + 1 + 1 + 1
 
-    # -- building blocks ------------------------------------------------------------
-    def _sample(self, slot: int, stream=None, fed: bool = False, hooks=None) -> None:
+    # -- stages ------------------------------------------------------------------
+    def _sample(self, batch: int, stream=None, fed: bool = False, hooks=None) -> None:
+        slot = batch % NS
         s = self.samplers[slot]
         order = self.fed_seeds if fed else self.order
         _lib.call("bgl_stage_batch", order.data_ptr(), self.order.numel(), self.b, self.num_batches,
@@ -86,98 +97,120 @@ class MiniBatchPipeline:
                   self.fed_count.data_ptr() if fed else None, _lib.stream_ptr(stream))
         s.run(self.table_stage[slot], stream=stream, hooks=hooks)
 
-    def _cache(self, slot: int, stream=None, events=None) -> None:
-        s = self.samplers[slot]
-        self.engine.retrieve_device(s.uniq, s.num_uniq, s.max_uniq, 0, counters=self.counters, stream=stream,
-                                    out=self.outs[slot], events=events)
+    def _front(self, batch: int, stream=None, events=None) -> None:
+        s = self.samplers[batch % NS]
+        j = batch % NB
+        plan, pcount = self.plans[j]
+        self.engine.front(s.uniq, s.num_uniq, s.max_uniq, 0, self.outs[j], self.codes_buf[j], self.src_row[j],
+                          plan, pcount, self.counters, stream=stream, events=events)
 
-    def prime(self, fed: bool = False) -> None:
-        """Sample the first batch (pipeline prologue, untimed)."""
-        if not self.primed:
-            self._sample(self.k % 2, fed=fed)
-            self.primed = True
+    def _back(self, batch: int, stream=None, fed: bool = False, events=None) -> None:
+        s = self.samplers[batch % NS]
+        j = batch % NB
+        plan, pcount = self.plans[j]
+        self.engine.back(s.uniq, s.num_uniq, s.max_uniq, self.outs[j], self.src_row[j], plan, pcount,
+                         stream=stream, events=events)
+        if fed:
+            _lib.call("bgl_d2h_result", s.uniq.data_ptr(), s.num_uniq.data_ptr(), s.max_uniq,
+                      self.counters.data_ptr(), self._host_ids_dev[j], self._host_meta_dev[j],
+                      _lib.stream_ptr(stream))
 
-    # -- one overlapped step: cache(k) || sample(k+1) ------------------------------
-    def _overlapped(self, parity: int, fed: bool, stream=None) -> None:
+    def prime(self, fed: bool = False, feed=None) -> None:
+        """Prologue (untimed): sample batches k, k+1 and run front(k).
+        In host-fed mode `feed(i)` must load batch i's seeds."""
+        if self.primed:
+            return
+        for i in (self.k, self.k + 1):
+            if fed and feed is not None:
+                feed(i)
+            self._sample(i, fed=fed)
+        self._front(self.k)
+        self.primed = True
+
+    # -- one overlapped step: back(k) || front(k+1) || sample(k+2) ----------------
+    def _overlapped(self, k: int, fed: bool, stream=None) -> None:
         cur = torch.cuda.current_stream() if stream is None else stream
-        self.s_stream.wait_stream(cur)
-        self.c_stream.wait_stream(cur)
-        with torch.cuda.stream(self.s_stream):
-            self._sample(1 - parity, stream=self.s_stream, fed=fed)
-        with torch.cuda.stream(self.c_stream):
-            self._cache(parity, stream=self.c_stream)
-            if fed:
-                s = self.samplers[parity]
-                _lib.call("bgl_d2h_result", s.uniq.data_ptr(), s.num_uniq.data_ptr(), s.max_uniq,
-                          self.counters.data_ptr(), self._host_ids_dev[parity], self._host_meta_dev[parity],
-                          _lib.stream_ptr(self.c_stream))
-        cur.wait_stream(self.s_stream)
-        cur.wait_stream(self.c_stream)
+        sb, sf, ss = self.streams
+        for s in self.streams:
+            s.wait_stream(cur)
+        with torch.cuda.stream(sf):
+            self._front(k + 1, stream=sf)
+        with torch.cuda.stream(ss):
+            self._sample(k + 2, stream=ss, fed=fed)
+        with torch.cuda.stream(sb):
+            self._back(k, stream=sb, fed=fed)
+        for s in self.streams:
+            cur.wait_stream(s)
 
     def step_eager(self, fed: bool = False) -> None:
         self.prime(fed)
-        self._overlapped(self.k % 2, fed)
+        self._overlapped(self.k, fed)
         self.k += 1
 
     def step_serial(self, events) -> None:
-        """Same work, serialised on the current stream with 6 events recorded
-        around sample(k+1), dedup, lookup, gather and insert of batch k
-        (stage breakdown; not used for the headline number)."""
+        """The same work serialised on the current stream, 7 events:
+        [sample | dedup | lookup+insert index | miss gather | hit gather |
+        row copy] of the step (stage breakdown only)."""
         self.prime()
-        parity = self.k % 2
-        s = self.samplers[1 - parity]
+        k = self.k
+        s = self.samplers[(k + 2) % NS]
         events[0].record()
-        self._sample(1 - parity, hooks=lambda h: events[1].record() if h == s.H - 1 else None)
+        self._sample(k + 2, hooks=lambda h: events[1].record() if h == s.H - 1 else None)
         events[2].record()
-        self._cache(parity, events=events[3:6])
+        self._front(k + 1, events=events[3:4])
+        events[4].record()
+        self._back(k, events=events[5:6])
+        events[6].record()
         self.k += 1
 
     def capture(self, fed: bool = False) -> None:
-        """Capture the overlapped step for both buffer parities."""
+        """Capture the overlapped step for every phase k % 6."""
         self.prime(fed)
         torch.cuda.synchronize()
         saved = self.batch_counter.clone()
-        for parity in (0, 1):
+        for phase in range(PHASES):
             g = torch.cuda.CUDAGraph()
             cs = torch.cuda.Stream()
             cs.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(cs):
                 with torch.cuda.graph(g, stream=cs):
-                    self._overlapped(parity, fed, stream=cs)
+                    self._overlapped(phase, fed, stream=cs)
             torch.cuda.current_stream().wait_stream(cs)
-            self.graphs[(parity, fed)] = g
+            self.graphs[(phase, fed)] = g
         torch.cuda.synchronize()
         self.batch_counter.copy_(saved)        # capture does not execute; keep the counter exact
 
     def step(self, fed: bool = False) -> None:
-        g = self.graphs.get((self.k % 2, fed))
-        if g is None:
+        g = self.graphs.get((self.k % PHASES, fed))
+        if g is None or not self.primed:
             self.step_eager(fed)
             return
-        self.prime(fed)
         g.replay()
         self.k += 1
 
-    def host_result(self, slot: int):
-        """(distinct IDs, counters) of the last host-fed batch that used
-        `slot`, read from pinned host memory (valid after a sync)."""
-        n = int(self.host_meta[slot][0])
-        return self.host_ids[slot][:n], self.host_meta[slot][1:9]
+    # -- results of the last completed batch (k - 1) -----------------------------
+    def last_batch(self) -> int:
+        return self.k - 1
 
-    # -- views of the last batch through the cache -----------------------------
     def last_slot(self) -> int:
-        return (self.k - 1) % 2
+        return (self.k - 1) % NB
 
     def distinct(self) -> torch.Tensor:
-        return self.samplers[self.last_slot()].distinct()
+        return self.samplers[(self.k - 1) % NS].distinct()
 
     def rows(self) -> torch.Tensor:
-        n = int(self.samplers[self.last_slot()].num_uniq.item())
-        return self.outs[self.last_slot()][:n]
+        n = int(self.samplers[(self.k - 1) % NS].num_uniq.item())
+        return self.outs[(self.k - 1) % NB][:n]
 
     def codes(self) -> torch.Tensor:
-        n = int(self.samplers[self.last_slot()].num_uniq.item())
-        return self.engine.codes[:n]
+        n = int(self.samplers[(self.k - 1) % NS].num_uniq.item())
+        return self.codes_buf[(self.k - 1) % NB][:n]
+
+    def host_result(self, slot: int):
+        """(distinct IDs, counters) stored into pinned host memory by the last
+        host-fed batch that used row slot `slot` (valid after a sync)."""
+        n = int(self.host_meta[slot][0])
+        return self.host_ids[slot][:n], self.host_meta[slot][1:9]
 
     def reset(self) -> None:
         """Cold cache, batch 0 next (graphs stay valid)."""

@@ -1,5 +1,6 @@
-"""GPU parity of the fused, graph-captured pipeline: every batch's distinct
-set, cache outcome counters and gathered rows vs the CPU oracle."""
+"""GPU parity of the fused, software-pipelined, graph-captured pipeline:
+every batch's distinct set, cache outcome codes, counters and gathered rows
+vs the CPU oracle."""
 
 import numpy as np
 import pytest
@@ -14,7 +15,8 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("use_graph", [False, True])
-def test_pipeline_matches_oracle(use_graph):
+@pytest.mark.parametrize("where", ["host", "hbm"])
+def test_pipeline_matches_oracle(use_graph, where):
     from paper_2112_08541_b200.cachesim import CacheConfig
     from paper_2112_08541_b200.features import synthetic_features
     from paper_2112_08541_b200.graph import generate_power_law_device
@@ -27,46 +29,44 @@ def test_pipeline_matches_oracle(use_graph):
     order, _ = proximity_schedule_device(dg, 4, b, seed=seed)
     ref_batches = oo.proximity_schedule(hg.row_offsets, hg.col_indices, hg.train_mask, 4, b, seed)
     assert np.array_equal(order.cpu().numpy(), np.concatenate(ref_batches))
-    feats = synthetic_features(n, dim, seed=2)
+    feats = synthetic_features(n, dim, seed=2, device_resident=(where == "hbm"))
     cap = n // 10
+    nb = 12
+    distinct = [so.sample_batch(hg.row_offsets, hg.col_indices, ref_batches[i], fan, seed, i)[2]
+                for i in range(nb + 1)]
+    ref_cnt, ref_codes = co.FifoEngine(cap, 0, 1).run(distinct)
+    cum = np.cumsum(ref_cnt, axis=0)
+
     pipe = MiniBatchPipeline(dg, fan, b, order, seed, CacheConfig(device_capacity=cap, feature_bytes_per_node=400),
                              feats)
     if use_graph:
         pipe.capture()
-    fifo = co.FifoEngine(cap, 0, 1)
-    nb = 12
-    prev = np.zeros(8, np.int64)
     for i in range(nb):
         pipe.step()
         torch.cuda.synchronize()
-        _, _, distinct, _ = so.sample_batch(hg.row_offsets, hg.col_indices, ref_batches[i], fan, seed, i)
-        got = pipe.distinct().cpu().numpy()
-        assert np.array_equal(got, distinct), i
-        rows = pipe.rows().cpu().numpy()
-        assert np.array_equal(rows, fo.synthetic_features(distinct, dim, seed=2)), i
-        c, codes = fifo.run([distinct], [0])
-        assert np.array_equal(pipe.codes().cpu().numpy(), codes[0])
-        now = pipe.counters.cpu().numpy()
-        assert np.array_equal(now[:7] - prev[:7], c[0]), i
-        prev = now
-    # reset -> the same epoch again from a cold cache, host-fed seeds
+        assert pipe.last_batch() == i
+        assert np.array_equal(pipe.distinct().cpu().numpy(), distinct[i]), i
+        assert np.array_equal(pipe.rows().cpu().numpy(), fo.synthetic_features(distinct[i], dim, seed=2)), i
+        assert np.array_equal(pipe.codes().cpu().numpy(), ref_codes[i]), i
+        # the front of batch i+1 (lookup + insert) already ran in this step
+        assert np.array_equal(pipe.counters.cpu().numpy()[:7], cum[i + 1]), i
+
+    # reset -> the same epoch again from a cold cache, host-fed seeds, results in pinned host memory
     if use_graph:
         pipe.capture(fed=True)
     pipe.reset()
-    fifo = co.FifoEngine(cap, 0, 1)
 
     def feed(i):
         sb = torch.from_numpy(ref_batches[i].astype(np.int32))
         pipe.fed_seeds[: len(sb)].copy_(sb)
         pipe.fed_count.fill_(len(sb))
 
-    feed(0)
-    pipe.prime(fed=True)
+    pipe.prime(fed=True, feed=feed)
     for i in range(4):
-        feed(i + 1)
+        feed(i + pipe.lookahead)
         pipe.step(fed=True)
         torch.cuda.synchronize()
-        _, _, distinct, _ = so.sample_batch(hg.row_offsets, hg.col_indices, ref_batches[i], fan, seed, i)
-        assert np.array_equal(pipe.distinct().cpu().numpy(), distinct), i
-        _, codes = fifo.run([distinct], [0])
-        assert np.array_equal(pipe.codes().cpu().numpy(), codes[0])
+        ids_h, cnt_h = pipe.host_result(pipe.last_slot())
+        assert np.array_equal(ids_h.numpy(), distinct[i]), i
+        assert np.array_equal(pipe.codes().cpu().numpy(), ref_codes[i])
+        assert np.array_equal(pipe.rows().cpu().numpy(), fo.synthetic_features(distinct[i], dim, seed=2)), i
