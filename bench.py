@@ -244,24 +244,25 @@ def run_bgl(args, cfg):
     R = 10
     st_times = {k: [] for k in ("sample", "dedup", "lookup_insert", "miss_gather", "hit_gather", "row_copy")}
     g_bytes_host, g_ms, hbm_bytes, hbm_ms = [], [], [], []
-    prev_hits = None
+    hist = []                                  # lookup counters per step: batch k+2 of step k
     for _ in range(R):
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
         cb = pipe.counters.clone()
         flush.zero_()
-        pipe.step_serial(evs)                  # sample(k+2) | front(k+1) | back(k)
+        pipe.step_serial(evs)                  # sample(k+3) | LI(k+2) | miss(k+1) | back(k)
         torch.cuda.synchronize()
-        ca = (pipe.counters - cb).cpu().tolist()   # lookup counters of batch k+1
+        hist.append((pipe.counters - cb).cpu().tolist())
         t = [evs[i].elapsed_time(evs[i + 1]) for i in range(6)]
         for k, v in zip(st_times, t):
             st_times[k].append(v)
-        misses = ca[3] + ca[4]                 # H + M rows of batch k+1 come from the feature store
-        g_bytes_host.append(misses * rb)
-        g_ms.append(t[3])
-        if prev_hits is not None:              # hits of batch k were counted in the previous step
-            hbm_bytes.append(2 * prev_hits * rb)
+        if len(hist) >= 2:                     # miss(k+1): H + M rows of batch k+1 (looked up last step)
+            ca = hist[-2]
+            g_bytes_host.append((ca[3] + ca[4]) * rb)
+            g_ms.append(t[3])
+        if len(hist) >= 3:                     # back(k): D + P rows of batch k (looked up two steps ago)
+            ca = hist[-3]
+            hbm_bytes.append(2 * (ca[1] + ca[2]) * rb)
             hbm_ms.append(t[4])
-        prev_hits = ca[1] + ca[2]
     gather_ms = statistics.mean(g_ms)
     host_bytes = statistics.mean(g_bytes_host)
     if args.features == "host":

@@ -135,6 +135,12 @@ class FeatureCacheEngine:
               events=None):
         """Lookup, insert-after-batch (indices/rings only, rows deferred to
         back()), then the misses' rows from the feature store into `out`."""
+        self.lookup_insert(ids, n_dev, max_n, worker, codes, src_row, plan, plan_count, counters, stream)
+        if events is not None:
+            events[0].record()
+        self.miss_gather(ids, n_dev, max_n, out, src_row, stream)
+
+    def lookup_insert(self, ids, n_dev, max_n, worker, codes, src_row, plan, plan_count, counters, stream=None):
         lib = _lib.load()
         st = _lib.stream_ptr(stream)
         h = self.dev.handle
@@ -143,8 +149,10 @@ class FeatureCacheEngine:
                                         counters.data_ptr(), st))
         _lib.check(lib.bgl_cache_insert_plan(h, ids.data_ptr(), max_n, plan.data_ptr(), plan_count.data_ptr(),
                                              counters.data_ptr(), st))
-        if events is not None:
-            events[0].record()
+
+    def miss_gather(self, ids, n_dev, max_n, out, src_row, stream=None):
+        lib = _lib.load()
+        st = _lib.stream_ptr(stream)
         ctas = 0 if self.features.is_cuda else self.miss_ctas
         _lib.check(lib.bgl_gather_rows(ids.data_ptr(), src_row.data_ptr(), n_dev.data_ptr(), max_n,
                                        self.dev.rows_ptr() or None, self.table, self.row_bytes, out.data_ptr(), 2,

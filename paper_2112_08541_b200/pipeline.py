@@ -4,27 +4,31 @@ One mini-batch of BGL's data path:
     stage   seeds + PCG64 table of the batch (bgl_stage_batch)
     sample  H hops, PCG64 replay, fused dedup mark (bgl_sample_hop x H)
     dedup   sorted distinct set                    (bgl_unique_sorted)
-    front   FIFO lookup vs the pre-batch state (bgl_cache_lookup), insert-
-            after-batch of indices/rings (bgl_cache_insert_plan), misses'
-            rows zero-copy from pinned host memory over the host link
-            (bgl_gather_rows, misses only)
+    LI      FIFO lookup vs the pre-batch state (bgl_cache_lookup) and the
+            insert-after-batch of indices/rings (bgl_cache_insert_plan)
+    miss    misses' rows zero-copy from pinned host memory over the host
+            link (bgl_gather_rows, misses only)
     back    hits' rows from the HBM ring slots (bgl_gather_rows, hits only),
             then the survivors' rows into their new slots (bgl_cache_copy_rows)
 
 Software pipeline (the paper overlaps sampling with feature retrieval,
-PAPER.md:536-576). Step k runs, as three concurrent branches,
-    back(k)  ||  front(k+1)  ||  sample(k+2)
-so the host link (front) streams misses back to back while the ring-row work
-of the previous batch and the sampling of the next ones run beside it.
-Correctness: front(k+1) only needs front(k)'s index update (previous step);
-back(k) needs front(k) (previous step) and back(k-1)'s row copy (previous
-step); within back(k) the hits are read before any survivor row is written
-(the same-batch eviction hazard of SURVEY.md §7). Sampling is cache-
-independent (rng keyed by the batch index, sampler.py:138). The cache state
-machine therefore sees batches strictly in order and every output equals the
-reference's. Buffers: samplers by batch % 3, rows / codes / src rows / insert
-plans by batch % 2; the step is captured once per phase (k % 6) in a CUDA
-graph and replayed.
+PAPER.md:536-576). Step k runs four concurrent branches
+
+    back(k)  ||  miss(k+1)  ||  LI(k+2)  ||  sample(k+3)
+
+so the host link streams misses back to back while the cache bookkeeping of
+the next batch, the ring-row work of the previous one and the sampling of
+later ones run beside it. Dependencies all point to earlier steps: LI(k+2)
+needs LI(k+1) (index state) and sample(k+2); miss(k+1) needs LI(k+1);
+back(k) needs miss(k) and back(k-1); within back(k) the hits are read before
+any survivor row is written (the same-batch eviction hazard). A
+later LI may re-assign a slot whose row back(k) is still writing: the row is
+fixed by that batch's own back() before any batch can hit the new occupant.
+Sampling is cache-independent (rng keyed by the batch index,
+sampler.py:138). The cache state machine therefore sees batches strictly in
+order and every output equals the reference's. Buffers: samplers by batch %
+4, rows / codes / src rows / insert plans by batch % 3; the step is captured
+once per phase (k % 12) in a CUDA graph and replayed.
 """
 
 from __future__ import annotations
@@ -37,12 +41,12 @@ from .features import FeatureCacheEngine
 from .graph import DeviceGraph
 from .sampler import BatchSampler, pcg_states, pcg_tables
 
-NS, NB = 3, 2          # sampler buffers, row/plan buffers
-PHASES = 6             # lcm(NS, NB)
+NS, NB = 4, 3          # sampler buffers, row/plan buffers
+PHASES = 12            # lcm(NS, NB)
 
 
 class MiniBatchPipeline:
-    lookahead = 2      # batch k+2 is sampled during step k
+    lookahead = 3      # batch k+3 is sampled during step k
 
     def __init__(self, dg: DeviceGraph, fanouts, batch_size: int, order: torch.Tensor, seed: int,
                  cache_cfg: CacheConfig, features: torch.Tensor, num_batches: int | None = None,
@@ -74,10 +78,7 @@ class MiniBatchPipeline:
         self.host_meta = [torch.zeros(16, dtype=torch.int64, pin_memory=True) for _ in range(NB)]
         self._host_ids_dev = [_lib.host_device_pointer(t) for t in self.host_ids]
         self._host_meta_dev = [_lib.host_device_pointer(t) for t in self.host_meta]
-        import os
-        fp = int(os.environ.get("BGL_FRONT_PRIORITY", "0"))
-        # back, front (host-link critical path), sample
-        self.streams = [torch.cuda.Stream(), torch.cuda.Stream(priority=fp), torch.cuda.Stream()]
+        self.streams = [torch.cuda.Stream() for _ in range(4)]     # back, miss, LI, sample
         self.graphs: dict = {}
         self.k = 0                # batches completed (rows ready)
         self.primed = False
@@ -97,12 +98,17 @@ class MiniBatchPipeline:
                   self.fed_count.data_ptr() if fed else None, _lib.stream_ptr(stream))
         s.run(self.table_stage[slot], stream=stream, hooks=hooks)
 
-    def _front(self, batch: int, stream=None, events=None) -> None:
+    def _li(self, batch: int, stream=None) -> None:
         s = self.samplers[batch % NS]
         j = batch % NB
         plan, pcount = self.plans[j]
-        self.engine.front(s.uniq, s.num_uniq, s.max_uniq, 0, self.outs[j], self.codes_buf[j], self.src_row[j],
-                          plan, pcount, self.counters, stream=stream, events=events)
+        self.engine.lookup_insert(s.uniq, s.num_uniq, s.max_uniq, 0, self.codes_buf[j], self.src_row[j], plan,
+                                  pcount, self.counters, stream=stream)
+
+    def _miss(self, batch: int, stream=None) -> None:
+        s = self.samplers[batch % NS]
+        j = batch % NB
+        self.engine.miss_gather(s.uniq, s.num_uniq, s.max_uniq, self.outs[j], self.src_row[j], stream=stream)
 
     def _back(self, batch: int, stream=None, fed: bool = False, events=None) -> None:
         s = self.samplers[batch % NS]
@@ -116,29 +122,33 @@ class MiniBatchPipeline:
                       _lib.stream_ptr(stream))
 
     def prime(self, fed: bool = False, feed=None) -> None:
-        """Prologue (untimed): sample batches k, k+1 and run front(k).
+        """Prologue (untimed): sample k..k+2, LI(k), miss(k), LI(k+1).
         In host-fed mode `feed(i)` must load batch i's seeds."""
         if self.primed:
             return
-        for i in (self.k, self.k + 1):
+        for i in range(self.k, self.k + self.lookahead):
             if fed and feed is not None:
                 feed(i)
             self._sample(i, fed=fed)
-        self._front(self.k)
+        self._li(self.k)
+        self._miss(self.k)
+        self._li(self.k + 1)
         self.primed = True
 
-    # -- one overlapped step: back(k) || front(k+1) || sample(k+2) ----------------
+    # -- one overlapped step: back(k) || miss(k+1) || LI(k+2) || sample(k+3) -------
     def _overlapped(self, k: int, fed: bool, stream=None) -> None:
         cur = torch.cuda.current_stream() if stream is None else stream
-        sb, sf, ss = self.streams
+        sb, sm, sl, ss = self.streams
         for s in self.streams:
             s.wait_stream(cur)
-        with torch.cuda.stream(sf):
-            self._front(k + 1, stream=sf)
-        with torch.cuda.stream(ss):
-            self._sample(k + 2, stream=ss, fed=fed)
+        with torch.cuda.stream(sm):
+            self._miss(k + 1, stream=sm)
+        with torch.cuda.stream(sl):
+            self._li(k + 2, stream=sl)
         with torch.cuda.stream(sb):
             self._back(k, stream=sb, fed=fed)
+        with torch.cuda.stream(ss):
+            self._sample(k + 3, stream=ss, fed=fed)
         for s in self.streams:
             cur.wait_stream(s)
 
@@ -149,22 +159,24 @@ class MiniBatchPipeline:
 
     def step_serial(self, events) -> None:
         """The same work serialised on the current stream, 7 events:
-        [sample | dedup | lookup+insert index | miss gather | hit gather |
-        row copy] of the step (stage breakdown only)."""
+        [sample | dedup | LI | miss gather | hit gather | row copy] of one
+        step (stage breakdown only)."""
         self.prime()
         k = self.k
-        s = self.samplers[(k + 2) % NS]
+        s = self.samplers[(k + 3) % NS]
         events[0].record()
-        self._sample(k + 2, hooks=lambda h: events[1].record() if h == s.H - 1 else None)
+        self._sample(k + 3, hooks=lambda h: events[1].record() if h == s.H - 1 else None)
         events[2].record()
-        self._front(k + 1, events=events[3:4])
+        self._li(k + 2)
+        events[3].record()
+        self._miss(k + 1)
         events[4].record()
         self._back(k, events=events[5:6])
         events[6].record()
         self.k += 1
 
     def capture(self, fed: bool = False) -> None:
-        """Capture the overlapped step for every phase k % 6."""
+        """Capture the overlapped step for every phase k % 12."""
         self.prime(fed)
         torch.cuda.synchronize()
         saved = self.batch_counter.clone()
