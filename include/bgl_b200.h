@@ -173,6 +173,27 @@ int bgl_cache_copy_rows(bgl_cache_t cache, const int32_t* plan, const int64_t* p
 int bgl_cache_export(bgl_cache_t cache, int64_t* dev_slots_host, int64_t* dev_tails_host,
                      int64_t* host_slots_host, int64_t* host_tail_host);
 
+/* ---------------------------------------------------------------- static-degree policy
+ * gnnio.cachesim.warm_static (cachesim.py:392-410): per shard the capacity
+ * highest-degree nodes (ties to the lower ID), then the host level from the
+ * rest; lookups then run through bgl_cache_lookup and nothing is inserted.
+ * hist: int64 [num_shards][max_degree+1] (degrees clamped), nodes flagged in
+ * `exclude` (may be NULL) skipped. select flags: mode 0 -> deg == thresh[v % d]
+ * (tie candidates), mode 1 -> deg > thresh[v % d] or tie_sel[v]. compact:
+ * ascending IDs of the flagged nodes. warm: rings/indices filled with the
+ * chosen nodes (dev_nodes concatenated shard by shard, dev_counts_host per
+ * shard, host array). */
+int bgl_degree_histogram(const int64_t* indptr, int64_t num_nodes, int32_t num_shards, int64_t max_degree,
+                         const uint8_t* exclude, int64_t* hist, void* stream);
+int bgl_select_flags(const int64_t* indptr, int64_t num_nodes, int32_t num_shards, const int64_t* thresh,
+                     const uint8_t* exclude, const uint8_t* tie_sel, int32_t mode, uint8_t* flags,
+                     void* stream);
+size_t bgl_compact_workspace(int64_t num_nodes);
+int bgl_compact_flags(const uint8_t* flags, int64_t num_nodes, int32_t* out_ids, int64_t* count_dev,
+                      void* workspace, void* stream);
+int bgl_cache_warm(bgl_cache_t cache, const int32_t* dev_nodes, const int64_t* dev_counts_host,
+                   const int32_t* host_nodes, int64_t n_host, void* stream);
+
 /* ---------------------------------------------------------------- feature gather
  * Net-new (the reference only counts bytes, cachesim.py:447-458):
  * out[i] = src_row[i] >= 0 ? ring_rows[src_row[i]] : table[ids[i]], 128-bit

@@ -157,3 +157,47 @@ def simulate_batched(batches, device_capacity, host_capacity, num_devices,
         counters[i] = (batch.size, counts[0], counts[1], counts[2], counts[3], ins, ev)
         codes_all.append(codes)
     return counters, codes_all, (dev_slots, dev_tails, host_slots, host_tail)
+
+
+# -- static-degree baseline (cachesim.py:250-265, 392-410) ----------------------------
+
+def static_warm(row_offsets, device_capacity, host_capacity, num_devices):
+    """Per device the `device_capacity` highest-degree owned nodes (ties to the
+    lower ID), then the host level from the rest. Returns (list of device
+    arrays, host array), each in selection order."""
+    degs = np.diff(np.asarray(row_offsets, dtype=np.int64))
+    n = degs.size
+    taken = np.zeros(n, dtype=bool)
+    dev = []
+    for h in range(num_devices):
+        owned = np.arange(h, n, num_devices, dtype=np.int64)
+        chosen = owned[np.lexsort((owned, -degs[owned]))][:device_capacity]
+        taken[chosen] = True
+        dev.append(chosen)
+    rest = np.flatnonzero(~taken)
+    host = rest[np.lexsort((rest, -degs[rest]))][:host_capacity]
+    return dev, host
+
+
+def static_run(batches, dev_sets, host_set, num_devices, batch_devices=None):
+    """Lookups only (static levels never change): (counters [nb, 7], codes)."""
+    d = num_devices
+    dev_member = [set(int(x) for x in s) for s in dev_sets]
+    host_member = set(int(x) for x in host_set)
+    counters = np.zeros((len(batches), 7), dtype=np.int64)
+    codes_all = []
+    for i, batch in enumerate(batches):
+        worker = batch_devices[i] if batch_devices is not None else i % d
+        codes = np.empty(len(batch), dtype=np.uint8)
+        for j, v in enumerate(batch):
+            v = int(v)
+            if v in dev_member[v % d]:
+                codes[j] = CODE_D if v % d == worker else CODE_P
+            elif v in host_member:
+                codes[j] = CODE_H
+            else:
+                codes[j] = CODE_M
+        c = np.bincount(codes, minlength=4)
+        counters[i] = (len(batch), c[0], c[1], c[2], c[3], 0, 0)
+        codes_all.append(codes)
+    return counters, codes_all

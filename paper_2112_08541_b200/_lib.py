@@ -51,7 +51,12 @@ PROTOTYPES = {
     "bgl_cache_insert_plan": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "bgl_cache_copy_rows": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "bgl_cache_export":(ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
-    "bgl_gather_rows": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_i32, c_i32, c_vp]),
+    "bgl_degree_histogram": (ctypes.c_int, [c_vp, c_i64, c_i32, c_i64, c_vp, c_vp, c_vp]),
+    "bgl_select_flags": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp]),
+    "bgl_compact_workspace": (c_sz, [c_i64]),
+    "bgl_compact_flags": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "bgl_cache_warm": (ctypes.c_int, [c_vp, c_vp, p_i64, c_vp, c_i64, c_vp]),
+    "bgl_gather_rows":(ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_i32, c_i32, c_vp]),
     "bgl_synthetic_features": (ctypes.c_int, [c_i64, c_i64, c_i32, c_u64, c_vp, c_vp]),
     "bgl_bfs_workspace": (c_sz, [c_i64]),
     "bgl_bfs_level": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64,

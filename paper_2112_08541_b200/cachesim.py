@@ -13,10 +13,12 @@ host ring. Results (outcome codes, counters, ring contents and tails) are
 bit-exact with the reference. The state lives in HBM and persists across
 `simulate` calls exactly like the reference's in-place-mutated state.
 
-LRU/LFU are not BGL's path (the paper rejects them) and
-static-degree is its comparison baseline (SURVEY.md §8f "next" #1): they are
-not implemented on the device and raise NotImplementedError -- there is no
-CPU fallback.
+The static-degree policy -- the paper's comparison baseline (SURVEY.md §8f
+"next" #1) -- also runs on the device: `warm_static` selects each shard's
+top-degree nodes with a sort-free histogram + ascending compaction and fills
+the same rings, lookups use the same kernel and nothing is inserted.
+LRU/LFU are not BGL's path (the paper rejects them): they
+raise NotImplementedError -- there is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -129,6 +131,12 @@ class FifoLevelView:
         return self._snap()[1]
 
     @property
+    def resident(self) -> frozenset:
+        """Resident node set (StaticLevel.resident, cachesim.py:255)."""
+        s = self.slots
+        return frozenset(int(v) for v in s[s >= 0])
+
+    @property
     def residency(self) -> dict[int, int]:
         s = self.slots
         return {int(v): i for i, v in enumerate(s) if v >= 0}
@@ -167,10 +175,77 @@ def cold_state(cfg: CacheConfig, num_nodes: int = 1, row_bytes: int = 0) -> Cach
     return CacheEngineState(cfg=cfg, engine=FifoCacheDevice(cfg, num_nodes, row_bytes), policy="fifo")
 
 
-def warm_static(g, cfg: CacheConfig):
+def _top_degree(dg, num_shards: int, capacity: int, exclude: torch.Tensor | None):
+    """Per shard (v % num_shards) the `capacity` highest-degree nodes, ties to
+    the lower ID (np.lexsort((owned, -degs[owned])), cachesim.py:403-404),
+    without a sort: degree histogram -> threshold degree t_h and the number
+    of degree-t_h nodes still needed; ties ranked by ascending ID.
+    Returns (device int32 nodes, shard by shard, each ascending; counts)."""
+    lib = _lib.load()
+    st = _lib.stream_ptr()
+    n, md = dg.num_nodes, max(dg.max_degree, 0)
+    xp = None if exclude is None else exclude.data_ptr()
+    hist = torch.empty((num_shards, md + 1), dtype=torch.int64, device="cuda")
+    _lib.check(lib.bgl_degree_histogram(dg.indptr.data_ptr(), n, num_shards, md, xp, hist.data_ptr(), st))
+    h = hist.cpu().numpy()
+    thresh = np.full(num_shards, np.iinfo(np.int64).max, dtype=np.int64)   # select nothing
+    need = np.zeros(num_shards, dtype=np.int64)
+    for s in range(num_shards):
+        cum = np.cumsum(h[s][::-1])          # nodes with degree >= md - i
+        if capacity <= 0:
+            continue
+        if capacity >= cum[-1]:
+            thresh[s] = -1                   # the whole shard fits
+            continue
+        i = int(np.searchsorted(cum, capacity))
+        thresh[s] = md - i
+        need[s] = capacity - (int(cum[i - 1]) if i > 0 else 0)
+    th = torch.from_numpy(thresh).cuda()
+    flags = torch.empty(n, dtype=torch.uint8, device="cuda")
+    ids = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ws = torch.empty(int(lib.bgl_compact_workspace(n)), dtype=torch.uint8, device="cuda")
+    from .distributed import GpuShardOps
+    ops = GpuShardOps(num_shards, n, 4)
+    tie_sel = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    if need.any():
+        _lib.check(lib.bgl_select_flags(dg.indptr.data_ptr(), n, num_shards, th.data_ptr(), xp, None, 0,
+                                        flags.data_ptr(), st))
+        _lib.check(lib.bgl_compact_flags(flags.data_ptr(), n, ids.data_ptr(), cnt.data_ptr(), ws.data_ptr(), st))
+        ties = ids[: int(cnt.item())]
+        part, _, counts = ops.partition(ties)
+        offs = np.concatenate([[0], np.cumsum(counts.cpu().numpy())])
+        for s in range(num_shards):
+            if need[s]:
+                tie_sel[part[offs[s]:offs[s] + need[s]].long()] = 1
+    _lib.check(lib.bgl_select_flags(dg.indptr.data_ptr(), n, num_shards, th.data_ptr(), xp, tie_sel.data_ptr(), 1,
+                                    flags.data_ptr(), st))
+    _lib.check(lib.bgl_compact_flags(flags.data_ptr(), n, ids.data_ptr(), cnt.data_ptr(), ws.data_ptr(), st))
+    chosen = ids[: int(cnt.item())]
+    part, _, counts = ops.partition(chosen)
+    return part.clone(), counts.cpu().numpy().astype(np.int64)
+
+
+def warm_static(g, cfg: CacheConfig) -> CacheEngineState:
+    """Pre-load every device level with the highest-degree nodes it owns and
+    the host level with the next-highest-degree nodes (cachesim.py:392-410),
+    computed on the device; the levels never change afterwards."""
     if cfg.policy != "static-degree":
         raise ValueError("warm_static requires policy='static-degree'")
-    raise _not_on_device(cfg.policy)
+    from .graph import device_graph
+    dg = device_graph(g)
+    d = cfg.num_devices
+    dev_nodes, dev_counts = _top_degree(dg, d, cfg.device_capacity, None)
+    host_nodes = torch.empty(0, dtype=torch.int32, device="cuda")
+    if cfg.host_capacity > 0:
+        resident = torch.zeros(dg.num_nodes, dtype=torch.uint8, device="cuda")
+        resident[dev_nodes.long()] = 1
+        host_nodes, hc = _top_degree(dg, 1, cfg.host_capacity, resident)
+    eng = FifoCacheDevice(cfg, dg.num_nodes)
+    _lib.check(_lib.load().bgl_cache_warm(eng.handle, dev_nodes.data_ptr(), (_lib.c_i64 * d)(*dev_counts.tolist()),
+                                          host_nodes.data_ptr() if host_nodes.numel() else None,
+                                          int(host_nodes.numel()), _lib.stream_ptr()))
+    return CacheEngineState(cfg=cfg, engine=eng, policy="static-degree")
 
 
 @dataclass
@@ -251,15 +326,17 @@ def simulate(trace, cfg: CacheConfig, g=None, batch_devices=None, state: CacheEn
              record_outcomes: bool = False) -> CacheSimReport:
     """Replay an access trace through the two-level multi-device cache
     (cachesim.py:461-549)."""
-    if cfg.policy == "static-degree":
-        if state is None and g is None:
-            raise ValueError("static policy needs the graph for degree warmup")
-        if state is not None and state.policy != "static-degree":
+    static = cfg.policy == "static-degree"
+    if static:
+        if state is None:
+            if g is None:
+                raise ValueError("static policy needs the graph for degree warmup")
+            state = warm_static(g, cfg)
+        elif state.policy != "static-degree":
             raise ValueError("state/policy mismatch")
-        raise _not_on_device(cfg.policy)
-    if state is not None and state.policy != cfg.policy:
+    elif state is not None and state.policy != cfg.policy:
         raise ValueError("state/policy mismatch")
-    if cfg.policy != "fifo":
+    if cfg.policy not in ("fifo", "static-degree"):
         raise _not_on_device(cfg.policy)
 
     batches = [np.asarray(b, dtype=np.int64).ravel() for b in trace.batches]
@@ -305,7 +382,8 @@ def simulate(trace, cfg: CacheConfig, g=None, batch_devices=None, state: CacheEn
                                         scratch.count.data_ptr(), n,
                                         None if codes is None else codes.data_ptr() + int(offs[i]),
                                         None, cptr, st))
-        _lib.check(lib.bgl_cache_insert(eng.handle, scratch.uniq.data_ptr(), n, None, cptr, st))
+        if not static:                         # static levels never change (StaticLevel.insert, cachesim.py:260-261)
+            _lib.check(lib.bgl_cache_insert(eng.handle, scratch.uniq.data_ptr(), n, None, cptr, st))
         _lib.check(lib.bgl_unique_reset(scratch.ws.data_ptr(), eng.num_nodes, scratch.uniq.data_ptr(),
                                         scratch.count.data_ptr(), n, st))
     host_counters = counters[:nb].cpu().numpy()
@@ -327,10 +405,10 @@ def amortized_update_ops(report: CacheSimReport) -> dict[str, float]:
     }
 
 
-def compare_policies(g, trace, capacities, policies=("fifo",), num_devices: int = 1, host_capacity: int = 0,
+def compare_policies(g, trace, capacities, policies=("static-degree", "fifo"), num_devices: int = 1, host_capacity: int = 0,
                      feature_bytes_per_node: int = 512) -> list[dict]:
     """Hit-ratio table over a (policy x capacity) sweep (cachesim.py:564-595).
-    Only the FIFO cells run on the device; the default sweeps FIFO only."""
+    The device runs the static-degree and FIFO cells (the default sweep)."""
     rows = []
     for policy in policies:
         for cap in capacities:

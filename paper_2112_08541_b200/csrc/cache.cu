@@ -628,3 +628,39 @@ extern "C" int bgl_cache_set_shard(bgl_cache_t c, int32_t shard_index, int32_t n
     c->global_shards = num_global_shards;
     return BGL_OK;
 }
+
+namespace bgl {
+// ring[r] = nodes[r], index[nodes[r]] = r (static warm-up: rings filled once)
+__global__ void warm_kernel(const int32_t* __restrict__ nodes, int64_t count, int32_t* __restrict__ ring,
+                            int32_t* __restrict__ index) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = nodes[r];
+        ring[r] = v;
+        index[v] = (int32_t)r;
+    }
+}
+}  // namespace bgl
+
+extern "C" int bgl_cache_warm(bgl_cache_t c, const int32_t* dev_nodes, const int64_t* dev_counts_host,
+                              const int32_t* host_nodes, int64_t n_host, void* stream) {
+    BGL_CHECK_ARG(c, "null cache");
+    cudaStream_t st = as_stream(stream);
+    BGL_TRY(bgl_cache_reset(c, stream));
+    int64_t off = 0;
+    for (int h = 0; h < c->d; ++h) {
+        const int64_t cnt = dev_counts_host ? dev_counts_host[h] : 0;
+        BGL_CHECK_ARG(cnt >= 0 && cnt <= c->C, "more warm nodes than shard capacity");
+        if (cnt > 0) {
+            warm_kernel<<<grid_for(cnt, 256), 256, 0, st>>>(dev_nodes + off, cnt, c->rings + (int64_t)h * c->C,
+                                                            c->slot_of);
+            BGL_TRY(launch_status("warm_kernel"));
+        }
+        off += cnt;
+    }
+    BGL_CHECK_ARG(n_host >= 0 && n_host <= c->Ch, "more warm nodes than host capacity");
+    if (n_host > 0) {
+        warm_kernel<<<grid_for(n_host, 256), 256, 0, st>>>(host_nodes, n_host, c->hring, c->hslot_of);
+        BGL_TRY(launch_status("warm_kernel"));
+    }
+    return BGL_OK;
+}

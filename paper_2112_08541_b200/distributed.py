@@ -57,6 +57,9 @@ class GpuShardOps:
 
     def partition(self, ids: torch.Tensor):
         n = int(ids.numel())
+        if n == 0:                      # (an empty tensor's data_ptr is NULL)
+            self.counts.zero_()
+            return self.part[:0], self.pos[:0], self.counts
         self.n.fill_(n)
         _lib.call("bgl_partition_by_home", ids.data_ptr(), self.n.data_ptr(), n, self.world, self.part.data_ptr(),
                   self.pos.data_ptr(), self.counts.data_ptr(), self.ws.data_ptr(), _lib.stream_ptr())
@@ -64,6 +67,8 @@ class GpuShardOps:
 
     def scatter(self, pos: torch.Tensor, rows: torch.Tensor, out: torch.Tensor) -> None:
         n = int(pos.numel())
+        if n == 0:
+            return
         self.n.fill_(n)
         _lib.call("bgl_scatter_rows", pos.data_ptr(), self.n.data_ptr(), n, rows.data_ptr(), self.row_bytes,
                   out.data_ptr(), _lib.stream_ptr())

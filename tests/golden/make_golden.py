@@ -276,10 +276,43 @@ def make_ordering(gs):
     np.savez_compressed(os.path.join(HERE, "ordering.npz"), **out)
 
 
+def make_static(gs):
+    out = {}
+    for name, g in gs.items():
+        store_graph(out, name, g)
+    out["graph_names"] = np.array(list(gs))
+    rng = np.random.default_rng(31)
+    meta, dev_sets, host_sets, counters, codes, batches_all = [], [], [], [], [], []
+    for gname in ("planted", "dense", "star6", "isolated"):
+        g = gs[gname]
+        n = g.num_nodes
+        for d, cap, hcap in ((1, 0, 0), (1, 2, 0), (1, n // 10, n // 20), (2, 7, 3), (4, n // 8, 0), (3, n, n),
+                             (4, 1, 5)):
+            cfg = cs.CacheConfig(device_capacity=cap, host_capacity=hcap, num_devices=d, policy="static-degree")
+            state = cs.warm_static(g, cfg)
+            batches = [np.unique(rng.integers(0, n, size=int(rng.integers(1, max(2, n // 4))))) for _ in range(6)]
+            rep = cs.simulate(AccessTrace(batches=batches), cfg, g=g, record_outcomes=True)
+            meta.append((list(gs).index(gname), d, cap, hcap, len(batches)))
+            dev_sets.extend(sorted(lv.resident) for lv in state.devices)
+            host_sets.append(sorted(state.host.resident))
+            counters.extend(zip(rep.batch_queries, rep.batch_own_hits, rep.batch_peer_hits, rep.batch_host_hits,
+                                rep.batch_misses, rep.batch_insertions, rep.batch_evictions))
+            codes.extend(np.array(["DPHM".index(c) for c in oc], dtype=np.int64) for oc in rep.outcomes)
+            batches_all.extend(batches)
+    out["meta"] = np.array(meta, dtype=np.int64)
+    put(out, "dev_sets", dev_sets)
+    put(out, "host_sets", host_sets)
+    put(out, "batches", batches_all)
+    put(out, "codes", codes, np.int8)
+    out["counters"] = np.array(counters, dtype=np.int64)
+    np.savez_compressed(os.path.join(HERE, "static.npz"), **out)
+
+
 if __name__ == "__main__":
     gs = graphs()
     make_sampler(gs)
     make_cache()
     make_ordering(gs)
-    for f in ("sampler.npz", "cache.npz", "ordering.npz"):
+    make_static(gs)
+    for f in ("sampler.npz", "cache.npz", "ordering.npz", "static.npz"):
         print(f, os.path.getsize(os.path.join(HERE, f)))

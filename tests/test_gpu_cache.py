@@ -131,3 +131,32 @@ def test_feature_retrieval_bit_exact(where, d):
     _lib.call("bgl_gather_rows", ids.data_ptr(), src.data_ptr(), nd.data_ptr(), len(slots), eng.dev.rows_ptr(),
               eng.table, dim * 4, out.data_ptr(), 0, 0, _lib.stream_ptr())
     assert np.array_equal(out.cpu().numpy(), ref_table[flat[slots]])
+
+
+def test_static_degree_policy_matches_reference(golden):
+    from conftest import golden_graph
+    from test_oracle_golden import _static_cases
+
+    from paper_2112_08541_b200 import cachesim as cs
+    from paper_2112_08541_b200.sampler import AccessTrace
+
+    class G:
+        def __init__(self, off, col):
+            self.row_offsets, self.col_indices, self.num_nodes = off, col, len(off) - 1
+
+    npz = golden("static")
+    for gname, d, cap, hcap, dsets, hset, batches, codes, cnt in _static_cases(npz):
+        off, col, _ = golden_graph(npz, gname)
+        g = G(off, col)
+        cfg = cs.CacheConfig(device_capacity=cap, host_capacity=hcap, num_devices=d, policy="static-degree")
+        state = cs.warm_static(g, cfg)
+        assert [sorted(lv.resident) for lv in state.devices] == [x.tolist() for x in dsets], (gname, d, cap)
+        assert sorted(state.host.resident) == hset.tolist()
+        rep = cs.simulate(AccessTrace(batches=batches), cfg, g=g, record_outcomes=True)
+        got = np.array([rep.batch_queries, rep.batch_own_hits, rep.batch_peer_hits, rep.batch_host_hits,
+                        rep.batch_misses, rep.batch_insertions, rep.batch_evictions]).T
+        assert np.array_equal(got, cnt)
+        assert rep.outcomes == [["DPHM"[c] for c in cd] for cd in codes]
+        assert sum(rep.batch_metadata_updates) == 0
+    with pytest.raises(ValueError):
+        cs.cold_state(cs.CacheConfig(device_capacity=2, policy="static-degree"))

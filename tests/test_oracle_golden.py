@@ -178,3 +178,30 @@ def test_feature_hash_properties():
     assert np.all(a >= -0.5) and np.all(a < 0.5)
     assert np.array_equal(a, fo.synthetic_features(np.array([0, 1, 123456789]), 100, seed=3))
     assert not np.array_equal(a, fo.synthetic_features(np.array([0, 1, 123456789]), 100, seed=4))
+
+
+def _static_cases(npz):
+    names = list(npz["graph_names"])
+    dev_sets = get(npz, "dev_sets")
+    host_sets = get(npz, "host_sets")
+    batches = get(npz, "batches")
+    codes = get(npz, "codes")
+    cnt = npz["counters"]
+    di = b0 = 0
+    for ci, (gi, d, cap, hcap, nb) in enumerate(npz["meta"]):
+        yield (names[gi], int(d), int(cap), int(hcap), dev_sets[di:di + d], host_sets[ci], batches[b0:b0 + nb],
+               codes[b0:b0 + nb], cnt[b0:b0 + nb])
+        di += d
+        b0 += nb
+
+
+def test_static_oracle_matches_reference(golden):
+    npz = golden("static")
+    for gname, d, cap, hcap, dsets, hset, batches, codes, cnt in _static_cases(npz):
+        off, _, _ = golden_graph(npz, gname)
+        dev, host = co.static_warm(off, cap, hcap, d)
+        assert [sorted(x.tolist()) for x in dev] == [x.tolist() for x in dsets]
+        assert sorted(host.tolist()) == hset.tolist()
+        c, cd = co.static_run(batches, dev, host, d)
+        assert np.array_equal(c, cnt)
+        assert all(np.array_equal(a, b) for a, b in zip(cd, codes))
