@@ -10,33 +10,34 @@
 // the pair packs into one 64-bit key (m << 11 | t).
 //
 // Kernels per hop:
-//   hop_scan     decoupled look-back prefix of deg (draw offsets) and k
-//                (output offsets); writes the chained draw base of the next
-//                hop and the output count, and lists the "heavy" parents
-//                (deg > 2048 or k > 32) for the block kernel.
-//   sample_warp  light parents: one warp walks a contiguous run of parents;
-//                lanes hold PCG64 states for 32 consecutive draws and keep a
-//                running top-k as a warp-distributed sorted list. A chunk of
-//                32 draws is merged by bitonic sort+merge when many lanes beat
-//                the current k-th key, else by per-candidate insertion. The
-//                stream is handed from one parent to the next with a lane
-//                rotation (no per-parent jump-ahead).
+//   sample_fused light parents: a warp claims a run of parents (atomic
+//                ticket), resolves the run's draw and output offsets with a
+//                warp-level decoupled look-back over runs (prefix of deg and
+//                of k = min(fanout, deg); the last run writes the chained draw
+//                base of the next hop and the output count), lists the heavy
+//                parents (deg > 2048 or k > 32), then walks its parents: lanes
+//                hold PCG64 states for 32 consecutive draws and keep a running
+//                top-k as a warp-distributed sorted list; a chunk of 32 draws is
+//                merged by bitonic sort+merge when many lanes beat the current
+//                k-th key, else by per-candidate insertion. The stream is handed
+//                from one parent to the next with a lane rotation (one
+//                jump-ahead per run, not per parent).
 //   sample_heavy one CTA per heavy parent: k <= 32 -> 8 warps each keep a
 //                top-k over a strided share of the chunks, merged in smem;
 //                k > 32 -> chunked bitonic sort in smem (KCAP <= 4096).
 // Only the k selected neighbours are read from col: the draws need deg, not
 // the neighbour IDs, so col traffic is k * 4 B per parent, not deg * 4 B.
 // Optionally every output is also marked in the dedup bitmap (fused K2 mark).
+#include <algorithm>
+
 #include "common.cuh"
 #include "pcg64.cuh"
 #include "scan.cuh"
 
 namespace bgl {
 
-constexpr int kScanThreads = 256;
-constexpr int kScanItems = 8;
-constexpr int kScanTile = kScanThreads * kScanItems;
 constexpr int64_t kNarrowMaxDeg = 2048;   // t fits 11 bits next to the 53-bit draw
+constexpr int kRun = 32;                  // parents per look-back run of the fused kernel
 
 struct HopWorkspace {
     int64_t* deg_prefix;   // [max_parents]
@@ -59,7 +60,7 @@ static HopWorkspace carve_hop_ws(void* ws, int64_t max_parents) {
     p += align256(m * 8);
     w.heavy = reinterpret_cast<int32_t*>(p);
     p += align256(m * 4);
-    w.max_tiles = ceil_div(m, kScanTile);
+    w.max_tiles = m;                          // look-back runs of the fused kernel (run length >= 1)
     w.scan = p;
     p += align256(scan_state_bytes(2, w.max_tiles));
     w.heavy_count = reinterpret_cast<int64_t*>(p);   // zeroed with the scan state (contiguous)
@@ -70,83 +71,6 @@ __device__ __forceinline__ void mark_bit(uint32_t* bitmap, int32_t v) {
     uint32_t bit = 1u << (v & 31);
     uint32_t* w = bitmap + (v >> 5);
     if (!(ld_volatile(w) & bit)) atomicOr(w, bit);
-}
-
-__global__ void __launch_bounds__(kScanThreads)
-hop_scan_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ parents,
-                const int64_t* __restrict__ num_parents_dev, int32_t fanout, ScanState ss,
-                int64_t* __restrict__ deg_prefix, int64_t* __restrict__ k_prefix, int32_t* __restrict__ heavy,
-                int64_t* __restrict__ heavy_count, int64_t* __restrict__ draw_base, int64_t* __restrict__ num_out) {
-    __shared__ int64_t s_deg[kScanTile];
-    __shared__ int32_t s_k[kScanTile];
-    __shared__ int64_t s_red[kScanThreads / 32 + 1];
-    __shared__ int64_t s_agg[2], s_pre[2], s_slot;
-
-    const int64_t n = *num_parents_dev;
-    const int64_t ntiles = n > 0 ? ceil_div(n, kScanTile) : 1;
-    const int64_t tile = claim_tile(ss, &s_slot);
-    if (tile >= ntiles) return;
-    const int64_t base = tile * kScanTile;
-
-    for (int i = threadIdx.x; i < kScanTile; i += kScanThreads) {
-        int64_t q = base + i;
-        int64_t d = 0;
-        if (q < n) {
-            int64_t p = parents[q];
-            d = indptr[p + 1] - indptr[p];
-        }
-        const int32_t k = (int32_t)(d < fanout ? d : fanout);
-        s_deg[i] = d;
-        s_k[i] = k;
-        const bool hv = k > 32 || d > kNarrowMaxDeg;
-        const unsigned m = __ballot_sync(0xffffffffu, hv);
-        if (m) {
-            int64_t slot = 0;
-            if (lane_id() == 0) slot = (int64_t)atomicAdd((unsigned long long*)heavy_count, (unsigned long long)__popc(m));
-            slot = __shfl_sync(0xffffffffu, slot, 0);
-            if (hv) heavy[slot + __popc(m & ((1u << lane_id()) - 1u))] = (int32_t)q;
-        }
-    }
-    __syncthreads();
-    int64_t my_d = 0, my_k = 0;
-    const int first = threadIdx.x * kScanItems;
-#pragma unroll
-    for (int j = 0; j < kScanItems; ++j) {
-        my_d += s_deg[first + j];
-        my_k += s_k[first + j];
-    }
-    int64_t tot_d, tot_k;
-    int64_t ex_d = block_excl_scan(my_d, s_red, &tot_d);
-    int64_t ex_k = block_excl_scan(my_k, s_red, &tot_k);
-    if (threadIdx.x == 0) {
-        s_agg[0] = tot_d;
-        s_agg[1] = tot_k;
-    }
-    __syncthreads();
-    lookback<2>(ss, tile, s_agg, s_pre);
-    const int64_t pd = s_pre[0], pk = s_pre[1];
-    int64_t rd = ex_d, rk = ex_k;
-#pragma unroll
-    for (int j = 0; j < kScanItems; ++j) {
-        int64_t d = s_deg[first + j];
-        int64_t k = s_k[first + j];
-        s_deg[first + j] = rd;
-        s_k[first + j] = (int32_t)rk;
-        rd += d;
-        rk += k;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < kScanTile; i += kScanThreads) {
-        int64_t q = base + i;
-        if (q < n) {
-            deg_prefix[q] = pd + s_deg[i];
-            k_prefix[q] = pk + s_k[i];
-        }
-    }
-    if (tile == ntiles - 1 && threadIdx.x == 0) {
-        draw_base[1] = draw_base[0] + pd + tot_d;
-        *num_out = pk + tot_k;
-    }
 }
 
 // ---------------------------------------------------------------- key types
@@ -242,65 +166,138 @@ __device__ __forceinline__ void fold_chunk(K& best, K& kth, K cand, int k) {
 
 constexpr int kWarpsPerBlock = 8;
 
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
-sample_warp_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                   const int32_t* __restrict__ parents, const int64_t* __restrict__ num_parents_dev,
-                   int32_t fanout, const uint64_t* __restrict__ table,
-                   const int64_t* __restrict__ draw_base, const int64_t* __restrict__ deg_prefix,
-                   const int64_t* __restrict__ k_prefix, int32_t* __restrict__ out_ids,
-                   int32_t* __restrict__ out_pidx, uint32_t* __restrict__ bitmap, int32_t run) {
-    const int64_t n = *num_parents_dev;
+// ---------------------------------------------------------------- fused scan + sample
+// Warp-level decoupled look-back over runs of `run` (<= kRun) parents: a warp
+// claims run r (atomic ticket, so every predecessor is already resident),
+// publishes the run's degree and k sums, resolves its exclusive prefix from
+// its predecessors, then samples the run. No separate scan pass: only heavy
+// parents get their offsets written out (for sample_heavy_kernel).
+__device__ __forceinline__ int64_t warp_lookback1(uint64_t* status, int64_t r, int64_t agg) {
     const int lane = lane_id();
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int64_t acc = 0;
+    if (r > 0) {
+        int64_t j = r - 1;
+        while (true) {
+            const int64_t idx = j - lane;
+            uint64_t w = kFlagInc;
+            if (idx >= 0) {
+                do { w = ld_volatile(status + idx); } while ((w >> 62) == 0);
+            }
+            const unsigned inc = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+            const int stop = inc ? __ffs(inc) - 1 : 31;
+            acc += warp_sum_i64(lane <= stop ? (int64_t)(w & kValMask) : 0);
+            if (inc) break;
+            j -= 32;
+        }
+    }
+    if (lane == 0)
+        atomicExch((unsigned long long*)(status + r), (unsigned long long)(kFlagInc | ((uint64_t)(acc + agg) & kValMask)));
+    return acc;
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+sample_fused_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                    const int32_t* __restrict__ parents, const int64_t* __restrict__ num_parents_dev,
+                    int32_t fanout, const uint64_t* __restrict__ table, int64_t* __restrict__ draw_base,
+                    ScanState ss, int64_t* __restrict__ deg_prefix, int64_t* __restrict__ k_prefix,
+                    int32_t* __restrict__ heavy, int64_t* __restrict__ heavy_count,
+                    int32_t* __restrict__ out_ids, int32_t* __restrict__ out_pidx, int64_t* __restrict__ num_out,
+                    uint32_t* __restrict__ bitmap, int32_t run) {
+    const int64_t n = *num_parents_dev;
+    const int64_t nruns = n > 0 ? ceil_div(n, run) : 1;
+    const int lane = lane_id();
+    const unsigned lt = (1u << lane) - 1u;
     const PcgTable T{table};
     const U128 A32 = T.A(5), C32 = T.C(5);
     const int64_t D0 = draw_base[0];
     const uint64_t INF = ~0ull;
-
-    for (int64_t q0 = warp * run; q0 < n; q0 += nwarps * run) {
-        const int64_t q1 = min(q0 + run, n);
+    while (true) {
+        int64_t r = 0;
+        if (lane == 0) r = (int64_t)atomicAdd(ss.ticket, 1u);
+        r = __shfl_sync(0xffffffffu, r, 0);
+        if (r >= nruns) break;
+        const int64_t q = r * run + lane;
+        const bool valid = lane < run && q < n;
+        const int32_t p = valid ? parents[q] : 0;
+        const int64_t off = valid ? indptr[p] : 0;
+        const int64_t deg = valid ? indptr[p + 1] - off : 0;
+        const int64_t k = deg < fanout ? deg : fanout;
+        // publish the run's aggregates first (successors never wait on a scan)
+        const int64_t incl_d = warp_incl_scan(deg);
+        const int64_t incl_k = warp_incl_scan(k);
+        const int64_t agg_d = __shfl_sync(0xffffffffu, incl_d, 31);
+        const int64_t agg_k = __shfl_sync(0xffffffffu, incl_k, 31);
+        if (lane == 0) {
+            const uint64_t f = r == 0 ? kFlagInc : kFlagAgg;
+            atomicExch((unsigned long long*)(ss.status + r), (unsigned long long)(f | ((uint64_t)agg_d & kValMask)));
+            atomicExch((unsigned long long*)(ss.status + ss.max_tiles + r),
+                       (unsigned long long)(f | ((uint64_t)agg_k & kValMask)));
+        }
+        const int64_t pre_d = warp_lookback1(ss.status, r, agg_d);
+        const int64_t pre_k = warp_lookback1(ss.status + ss.max_tiles, r, agg_k);
+        const int64_t ex_d = pre_d + incl_d - deg;   // draws before this parent (relative to D0)
+        const int64_t ex_k = pre_k + incl_k - k;     // outputs before this parent
+        const bool hv = valid && (k > 32 || deg > kNarrowMaxDeg);
+        const unsigned hm = __ballot_sync(0xffffffffu, hv);
+        if (hm) {
+            int64_t slot = 0;
+            if (lane == 0) slot = (int64_t)atomicAdd((unsigned long long*)heavy_count, (unsigned long long)__popc(hm));
+            slot = __shfl_sync(0xffffffffu, slot, 0);
+            if (hv) {
+                heavy[slot + __popc(hm & lt)] = (int32_t)q;
+                deg_prefix[q] = ex_d;
+                k_prefix[q] = ex_k;
+            }
+        }
+        if (r == nruns - 1 && lane == 31) {
+            draw_base[1] = D0 + pre_d + incl_d;
+            *num_out = pre_k + incl_k;
+        }
+        // sample the run's light parents in order, handing the stream along
         bool have = false;
         U128 s{0, 0};
-        int32_t p_next = parents[q0];
-        for (int64_t q = q0; q < q1; ++q) {
-            const int32_t p = p_next;
-            if (q + 1 < q1) p_next = parents[q + 1];
-            const int64_t off = indptr[p];
-            const int64_t deg = indptr[p + 1] - off;
-            if (deg == 0) continue;                  // consumes no draws (sampler.py:77-79)
-            const int k = (int)(deg < fanout ? deg : fanout);
-            if (k > 32 || deg > kNarrowMaxDeg) {     // sample_heavy_kernel's parent
+        const int cnt = (int)((n - r * run) < run ? (n - r * run) : run);
+        for (int i = 0; i < cnt; ++i) {
+            const int64_t dg = __shfl_sync(0xffffffffu, deg, i);
+            if (dg == 0) continue;                    // consumes no draws (sampler.py:77-79)
+            const int ki = (int)__shfl_sync(0xffffffffu, k, i);
+            if (ki > 32 || dg > kNarrowMaxDeg) {      // heavy: sample_heavy_kernel
                 have = false;
                 continue;
             }
             if (!have) {
-                s = T.at((uint64_t)(D0 + deg_prefix[q] + lane + 1));
+                s = T.at((uint64_t)(D0 + __shfl_sync(0xffffffffu, ex_d, i) + lane + 1));
                 have = true;
             }
             uint64_t best = INF, kth = INF;
-            const int64_t nc = (deg + 31) >> 5;
+            const int64_t nc = (dg + 31) >> 5;
             for (int64_t c = 0; c < nc; ++c) {
                 if (c > 0) s = affine(A32, C32, s);
                 const int64_t t = (c << 5) + lane;
-                const uint64_t cand = t < deg ? make_key(draw_of_state(s), (uint32_t)t, (uint64_t*)nullptr) : INF;
-                fold_chunk(best, kth, cand, k);
+                const uint64_t cand = t < dg ? make_key(draw_of_state(s), (uint32_t)t, (uint64_t*)nullptr) : INF;
+                if (c == 0) {
+                    // first chunk: the sorted chunk is the list (no merge with an empty list)
+                    best = warp_bitonic_sort(cand);
+                    kth = shfl(best, ki - 1);
+                } else {
+                    fold_chunk(best, kth, cand, ki);
+                }
             }
-            // hand the stream to the next parent: it starts at relative draw deg
             {
-                const int64_t x = deg + lane;
+                const int64_t x = dg + lane;
                 const int src = (int)(x & 31);
-                U128 r;
-                r.hi = __shfl_sync(0xffffffffu, s.hi, src);
-                r.lo = __shfl_sync(0xffffffffu, s.lo, src);
-                if (x >= (nc << 5)) r = affine(A32, C32, r);
-                s = r;
+                U128 rr;
+                rr.hi = __shfl_sync(0xffffffffu, s.hi, src);
+                rr.lo = __shfl_sync(0xffffffffu, s.lo, src);
+                if (x >= (nc << 5)) rr = affine(A32, C32, rr);
+                s = rr;
             }
-            if (lane < k) {
-                const int64_t o = k_prefix[q] + lane;
-                const int32_t v = indices[off + key_t(best)];
-                out_ids[o] = v;
-                out_pidx[o] = (int32_t)q;
+            const int64_t oi = __shfl_sync(0xffffffffu, ex_k, i);
+            const int64_t offi = __shfl_sync(0xffffffffu, off, i);
+            if (lane < ki) {
+                const int32_t v = indices[offi + key_t(best)];
+                out_ids[oi + lane] = v;
+                out_pidx[oi + lane] = (int32_t)(r * run + i);
                 if (bitmap) mark_bit(bitmap, v);
             }
         }
@@ -420,7 +417,7 @@ extern "C" {
 
 size_t bgl_sample_hop_workspace(int64_t max_parents) {
     int64_t m = max_parents > 0 ? max_parents : 1;
-    return align256(m * 8) * 2 + align256(m * 4) + align256(scan_state_bytes(2, ceil_div(m, kScanTile))) + 256;
+    return align256(m * 8) * 2 + align256(m * 4) + align256(scan_state_bytes(2, m)) + 256;
 }
 
 int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t* parents,
@@ -438,25 +435,23 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     // scan state + heavy counter are contiguous: one memset
     BGL_TRY(cuda_status(cudaMemsetAsync(w.scan, 0, align256(scan_state_bytes(2, w.max_tiles)) + 8, st),
                         "hop workspace reset"));
-    ScanState ss = make_scan_state(w.scan, 2, w.max_tiles);
     uint32_t* bm = reinterpret_cast<uint32_t*>(mark_bitmap);
-    hop_scan_kernel<<<(unsigned)w.max_tiles, kScanThreads, 0, st>>>(
-        indptr, parents, num_parents_dev, fanout, ss, w.deg_prefix, w.k_prefix, w.heavy, w.heavy_count,
-        draw_base, num_out_dev);
-    BGL_TRY(launch_status("hop_scan_kernel"));
+    // fused scan + sample over runs of `run` parents: short runs when the hop is
+    // small (enough warps for hop 1), up to kRun (one per lane) when it is large
+    const int64_t want_runs = (int64_t)kNumSMs * 48 * 2;
+    int64_t run = ceil_div(std::max<int64_t>(max_parents, 1), want_runs);
+    run = std::min<int64_t>(std::max<int64_t>(run, 1), kRun);
+    const int64_t runs = std::max<int64_t>(1, ceil_div(max_parents, run));
+    ScanState ss = make_scan_state(w.scan, 2, w.max_tiles);
+    unsigned blocks = (unsigned)ceil_div(runs, kWarpsPerBlock);
+    const unsigned cap_blocks = (unsigned)kNumSMs * 8;
+    if (blocks > cap_blocks) blocks = cap_blocks;               // runs are claimed dynamically
+    if (max_ctas > 0 && blocks > (unsigned)max_ctas) blocks = (unsigned)max_ctas;
+    sample_fused_kernel<<<blocks, kWarpsPerBlock * 32, 0, st>>>(
+        indptr, indices, parents, num_parents_dev, fanout, table, draw_base, ss, w.deg_prefix, w.k_prefix, w.heavy,
+        w.heavy_count, out_ids, out_parent_idx, num_out_dev, bm, (int32_t)run);
+    BGL_TRY(launch_status("sample_fused_kernel"));
     if (max_parents == 0) return BGL_OK;
-    // contiguous runs of parents per warp; ~4 runs per resident warp
-    const int64_t resident_warps = (int64_t)kNumSMs * 48;
-    int64_t run = ceil_div(max_parents, resident_warps * 4);
-    if (run < 1) run = 1;
-    if (run > 64) run = 64;
-    int64_t warps = ceil_div(max_parents, run);
-    unsigned blocks = (unsigned)ceil_div(warps, kWarpsPerBlock);
-    if (max_ctas > 0 && blocks > (unsigned)max_ctas) blocks = (unsigned)max_ctas;   // grid-stride covers the rest
-    sample_warp_kernel<<<blocks, kWarpsPerBlock * 32, 0, st>>>(
-        indptr, indices, parents, num_parents_dev, fanout, table, draw_base, w.deg_prefix, w.k_prefix,
-        out_ids, out_parent_idx, bm, (int32_t)run);
-    BGL_TRY(launch_status("sample_warp_kernel"));
     int kcap = 32;
     if (fanout > 32) {
         kcap = 64;
