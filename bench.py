@@ -381,7 +381,8 @@ def run_sharded(args, cfg):
     One step = one round = N mini-batches (one per GPU)."""
     import torch
     import torch.distributed as dist
-    from paper_2112_08541_b200.distributed import GpuShardEngine, GpuShardOps, ShardedFeatureCache
+    from paper_2112_08541_b200.distributed import (GpuShardEngine, GpuShardOps, PeerPushFeatureCache,
+                                                   ShardedFeatureCache)
     from paper_2112_08541_b200.sampler import BatchSampler, pcg_states, pcg_tables
 
     if "RANK" not in os.environ:            # single process without torchrun (--sharded at N=1)
@@ -397,7 +398,12 @@ def run_sharded(args, cfg):
     sampler = BatchSampler(dg, cfg["fanouts"], b)
     engine = GpuShardEngine(rank, world, cap, feats, sampler.max_uniq)
     ops = GpuShardOps(world, sampler.max_uniq, rb)
-    sc = ShardedFeatureCache(rank, world, engine, ops, dim)
+    if args.exchange == "push":
+        # IDs by NCCL all-to-all, rows stored by the homes' gather straight into
+        # the worker GPU's buffer over NVLink (CUDA IPC, bgl_gather_rows_push)
+        sc = PeerPushFeatureCache(rank, world, engine, ops, dim, sampler.max_uniq)
+    else:
+        sc = ShardedFeatureCache(rank, world, engine, ops, dim)
     tables = pcg_tables(pcg_states(RUN_SEED, range(nb_total)))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     order_host = order.cpu().numpy().astype(np.int32)
@@ -461,7 +467,9 @@ def run_sharded(args, cfg):
         "config": {"workload": cfg["workload"], "num_nodes": cfg["n"], "csr_entries": dg.num_edges,
                    "feature_dim": cfg["dim"], "fanouts": list(cfg["fanouts"]), "batch": b,
                    "cache_rows_per_gpu": cap, "features": args.features,
-                   "parallelism": f"dp{world} + node-ID-sharded FIFO cache (home = v % {world}), NCCL all-to-all",
+                   "parallelism": f"dp{world} + node-ID-sharded FIFO cache (home = v % {world}); IDs by NCCL "
+                                  f"all-to-all, rows by " + ("home-push over NVLink (CUDA IPC)" if args.exchange == "push"
+                                                             else "NCCL all-to-all"),
                    "l2": "flushed between timed steps (256 MB write, outside the events)",
                    "step": f"one round = {world} mini-batches (one per GPU)"},
         "feature_gbs": round(q * rb / (total_ms * 1e-3) / 1e9, 2),
@@ -530,6 +538,8 @@ def main():
     ap.add_argument("--features", choices=["host", "hbm"], default="host")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="use the multi-GPU sharded engine even at N=1")
+    ap.add_argument("--exchange", choices=["push", "nccl"], default="push",
+                    help="multi-GPU row exchange: home-push over peer memory or NCCL all-to-all")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

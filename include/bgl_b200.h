@@ -252,6 +252,20 @@ int bgl_partition_by_home(const int32_t* ids, const int64_t* n_dev, int64_t max_
                           void* stream);
 int bgl_scatter_rows(const int32_t* pos, const int64_t* n_dev, int64_t max_n, const void* rows,
                      int64_t row_bytes, void* out, void* stream);
+/* Home-push gather (the row exchange fused into the gather): rows as in
+ * bgl_gather_rows go to the local `out` (kept for the ring insert) AND to
+ * push_out + push_pos[i] * row_bytes -- the worker GPU's output buffer,
+ * mapped into this process with bgl_ipc_open_handle, written over NVLink. */
+int bgl_gather_rows_push(const int32_t* ids, const int64_t* src_row, const int64_t* n_dev, int64_t max_n,
+                         const void* ring_rows, const void* table, int64_t row_bytes, void* out,
+                         void* push_out, const int32_t* push_pos, int32_t mode, int32_t ctas,
+                         void* stream);
+/* CUDA IPC of device buffers between the per-GPU processes (64-byte handles).
+ * The handle names the whole allocation; *offset_out is dev_ptr's offset in
+ * it (add it to the pointer bgl_ipc_open_handle returns). */
+int bgl_ipc_get_handle(void* dev_ptr, void* handle_out, int64_t* offset_out);
+int bgl_ipc_open_handle(const void* handle, void** dev_ptr_out);
+int bgl_ipc_close(void* dev_ptr);
 
 /* ---------------------------------------------------------------- pipeline staging
  * Step staging for the CUDA-graph-captured pipeline (no reference

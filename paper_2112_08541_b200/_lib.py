@@ -66,6 +66,11 @@ PROTOTYPES = {
     "bgl_partition_workspace": (c_sz, [c_i64, c_i32]),
     "bgl_partition_by_home": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "bgl_scatter_rows": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp]),
+    "bgl_gather_rows_push": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i32,
+                                             c_i32, c_vp]),
+    "bgl_ipc_get_handle": (ctypes.c_int, [c_vp, c_vp, ctypes.POINTER(c_i64)]),
+    "bgl_ipc_open_handle": (ctypes.c_int, [c_vp, ctypes.POINTER(c_vp)]),
+    "bgl_ipc_close": (ctypes.c_int, [c_vp]),
     "bgl_d2h_result": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "bgl_stage_batch":(ctypes.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
 }

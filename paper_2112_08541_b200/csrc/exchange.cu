@@ -4,7 +4,10 @@
 //              (the insert order each home needs, cachesim.py:527-528) and the
 //              position of every bucketed ID in the batch;
 //   scatter    rows returned by the homes back into batch order.
+#include <dlfcn.h>
+
 #include <algorithm>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -106,6 +109,8 @@ __global__ void scatter_rows_kernel(const int32_t* __restrict__ pos, const int64
         if ((rb & 15) == 0) {
             for (int64_t b = (int64_t)lane * 16; b < rb; b += 32 * 16)
                 *reinterpret_cast<uint4*>(d + b) = *reinterpret_cast<const uint4*>(s + b);
+        } else if ((rb & 3) != 0) {
+            for (int64_t b = lane; b < rb; b += 32) d[b] = s[b];
         } else {
             for (int64_t b = (int64_t)lane * 4; b < rb; b += 32 * 4)
                 *reinterpret_cast<uint32_t*>(d + b) = *reinterpret_cast<const uint32_t*>(s + b);
@@ -141,11 +146,43 @@ int bgl_partition_by_home(const int32_t* ids, const int64_t* n_dev, int64_t max_
 int bgl_scatter_rows(const int32_t* pos, const int64_t* n_dev, int64_t max_n, const void* rows, int64_t row_bytes,
                      void* out, void* stream) {
     BGL_CHECK_ARG(pos && n_dev && rows && out, "bgl_scatter_rows: null pointer");
-    BGL_CHECK_ARG(row_bytes > 0 && row_bytes % 4 == 0, "row_bytes must be a positive multiple of 4");
+    BGL_CHECK_ARG(row_bytes > 0, "row_bytes must be positive");
     if (max_n <= 0) return BGL_OK;
     scatter_rows_kernel<<<grid_for(max_n * 32, 256, 8), 256, 0, as_stream(stream)>>>(
         pos, n_dev, (const unsigned char*)rows, row_bytes, (unsigned char*)out);
     return launch_status("scatter_rows_kernel");
+}
+
+int bgl_ipc_get_handle(void* dev_ptr, void* handle_out, int64_t* offset_out) {
+    BGL_CHECK_ARG(dev_ptr && handle_out && offset_out, "bgl_ipc_get_handle: null pointer");
+    // The handle names the whole allocation (a caching allocator hands out
+    // sub-ranges): report the offset of dev_ptr inside it. Driver API via
+    // dlsym so the library has no link-time dependency on libcuda.
+    using range_fn = int (*)(unsigned long long*, size_t*, unsigned long long);
+    static range_fn fn = nullptr;
+    if (!fn) {
+        void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libcuda.so.1", RTLD_NOW);
+        if (h) fn = reinterpret_cast<range_fn>(dlsym(h, "cuMemGetAddressRange_v2"));
+        BGL_CHECK_ARG(fn != nullptr, "bgl_ipc_get_handle: cuMemGetAddressRange unavailable");
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    BGL_CHECK_ARG(fn(&base, &size, (unsigned long long)dev_ptr) == 0, "cuMemGetAddressRange failed");
+    *offset_out = (int64_t)((unsigned long long)dev_ptr - base);
+    return cuda_status(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle_out), dev_ptr),
+                       "cudaIpcGetMemHandle");
+}
+
+int bgl_ipc_open_handle(const void* handle, void** dev_ptr_out) {
+    BGL_CHECK_ARG(handle && dev_ptr_out, "bgl_ipc_open_handle: null pointer");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    return cuda_status(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+}
+
+int bgl_ipc_close(void* dev_ptr) {
+    return cuda_status(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
 }
 
 }  // extern "C"

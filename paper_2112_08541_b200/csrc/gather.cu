@@ -44,7 +44,8 @@ constexpr int kRows = 4;
 __global__ void __launch_bounds__(kGThreads)
 gather_v4_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ src_row,
                  const int64_t* __restrict__ n_dev, const unsigned char* __restrict__ ring,
-                 const unsigned char* __restrict__ table, int64_t rb, unsigned char* __restrict__ out, int mode) {
+                 const unsigned char* __restrict__ table, int64_t rb, unsigned char* __restrict__ out, int mode,
+                 unsigned char* __restrict__ push_out, const int32_t* __restrict__ push_pos) {
     const int64_t n = *n_dev;
     const int cpr = (int)(rb >> 4);
     const int lane = lane_id();
@@ -70,6 +71,12 @@ gather_v4_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ sr
 #pragma unroll
             for (int u = 0; u < kRows; ++u)
                 if (src[u]) st_na_v4(out + (r0 + u) * rb + c * 16, v[u]);
+            if (push_out) {   // home-push: the same row straight into the worker GPU's output (peer memory)
+#pragma unroll
+                for (int u = 0; u < kRows; ++u)
+                    if (src[u])
+                        st_na_v4(push_out + (int64_t)__ldg(push_pos + r0 + u) * rb + c * 16, v[u]);
+            }
         }
     }
 }
@@ -138,7 +145,7 @@ int bgl_gather_rows(const int32_t* ids, const int64_t* src_row, const int64_t* n
         }
         gather_v4_kernel<<<grid, threads, 0, st>>>(ids, src_row, n_dev, (const unsigned char*)ring_rows,
                                                      (const unsigned char*)table, row_bytes, (unsigned char*)out,
-                                                     mode);
+                                                     mode, nullptr, nullptr);
         return launch_status("gather_v4_kernel");
     }
     int64_t chunks = max_n * (row_bytes / 4);
@@ -146,6 +153,28 @@ int bgl_gather_rows(const int32_t* ids, const int64_t* src_row, const int64_t* n
         ids, src_row, n_dev, (const unsigned char*)ring_rows, (const unsigned char*)table, row_bytes,
         (unsigned char*)out, mode);
     return launch_status("gather_v1_kernel");
+}
+
+int bgl_gather_rows_push(const int32_t* ids, const int64_t* src_row, const int64_t* n_dev, int64_t max_n,
+                         const void* ring_rows, const void* table, int64_t row_bytes, void* out, void* push_out,
+                         const int32_t* push_pos, int32_t mode, int32_t ctas, void* stream) {
+    BGL_CHECK_ARG(mode >= 0 && mode <= 2, "gather mode must be 0 (all), 1 (hits) or 2 (misses)");
+    BGL_CHECK_ARG(ids && n_dev && table && out && push_out && push_pos, "bgl_gather_rows_push: null pointer");
+    BGL_CHECK_ARG(src_row == nullptr || ring_rows != nullptr, "bgl_gather_rows_push: src_row without ring rows");
+    BGL_CHECK_ARG(row_bytes % 16 == 0 && (uintptr_t)table % 16 == 0 && (uintptr_t)out % 16 == 0 &&
+                      (uintptr_t)push_out % 16 == 0,
+                  "bgl_gather_rows_push: 16-byte aligned rows required");
+    if (max_n <= 0) return BGL_OK;
+    unsigned grid = grid_for(ceil_div(max_n, kRows) * 32, kGThreads, 4);
+    int threads = kGThreads;
+    if (ctas > 0) {
+        grid = (unsigned)ctas;
+        threads = 256;
+    }
+    gather_v4_kernel<<<grid, threads, 0, as_stream(stream)>>>(
+        ids, src_row, n_dev, (const unsigned char*)ring_rows, (const unsigned char*)table, row_bytes,
+        (unsigned char*)out, mode, (unsigned char*)push_out, push_pos);
+    return launch_status("gather_v4_kernel(push)");
 }
 
 int bgl_synthetic_features(int64_t first_node, int64_t num_nodes, int32_t dim, uint64_t seed, float* out,

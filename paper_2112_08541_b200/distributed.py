@@ -93,6 +93,18 @@ class GpuShardEngine:
             return
         self.eng.retrieve_device(ids, self.n, c, worker, counters=self.counters, out=rows_out, codes=codes_out)
 
+    def serve_push(self, ids: torch.Tensor, worker: int, pos: torch.Tensor, peer_rows: int, peer_codes: int,
+                   staging_rows: torch.Tensor, staging_codes: torch.Tensor) -> None:
+        """Serve worker `worker`'s bucket and push rows + codes straight into
+        its output buffers (peer pointers) at `pos`."""
+        c = int(ids.numel())
+        if c == 0:
+            return
+        self.n.fill_(c)
+        self.eng.retrieve_push(ids, self.n, c, worker, staging_rows, staging_codes, peer_rows, pos, self.counters)
+        _lib.call("bgl_scatter_rows", pos.data_ptr(), self.n.data_ptr(), c, staging_codes.data_ptr(), 1, peer_codes,
+                  _lib.stream_ptr())
+
 
 class ShardedFeatureCache:
     """Collective per-round retrieval through the node-ID-sharded cache."""
@@ -142,3 +154,88 @@ class ShardedFeatureCache:
         c = self.engine.counters.clone()
         dist.all_reduce(c, group=self.group)
         return c
+
+
+class PeerPushFeatureCache(ShardedFeatureCache):
+    """Same protocol with the row exchange fused into the homes' gather: every
+    rank exposes its batch output buffers through CUDA IPC; a home gathers a
+    worker's rows (HBM ring hits, host-link misses) and stores each row
+    directly into that worker's buffer over NVLink (bgl_gather_rows_push), so
+    only IDs and positions travel through the collective. `cpu_collectives`
+    routes the small ID exchange through host tensors (gloo), which lets the
+    whole data path run with several processes on one GPU for testing."""
+
+    def __init__(self, rank: int, world: int, engine: GpuShardEngine, ops: GpuShardOps, dim: int, max_batch: int,
+                 group=None, cpu_collectives: bool = False):
+        super().__init__(rank, world, engine, ops, dim, group=group)
+        self.cpu = cpu_collectives
+        self.out_rows = torch.empty((max(max_batch, 1), dim), dtype=torch.float32, device="cuda")
+        self.out_codes = torch.empty(max(max_batch, 16), dtype=torch.uint8, device="cuda")
+        self.staging_rows = torch.empty_like(self.out_rows)
+        self.staging_codes = torch.empty_like(self.out_codes)
+        lib = _lib.load()
+        mine = []
+        for t in (self.out_rows, self.out_codes):
+            h = (_lib.ctypes.c_char * 64)()
+            off = _lib.c_i64()
+            _lib.check(lib.bgl_ipc_get_handle(t.data_ptr(), h, _lib.ctypes.byref(off)))
+            mine.append((bytes(h), off.value))
+        handles = [None] * world
+        dist.all_gather_object(handles, mine, group=group)
+        self.peer_rows, self.peer_codes, self._opened = [], [], []
+        for w in range(world):
+            if w == rank:
+                self.peer_rows.append(self.out_rows.data_ptr())
+                self.peer_codes.append(self.out_codes.data_ptr())
+                continue
+            ptrs = []
+            for hb, off in handles[w]:
+                p = _lib.c_vp()
+                _lib.check(lib.bgl_ipc_open_handle(_lib.ctypes.create_string_buffer(hb, 64), _lib.ctypes.byref(p)))
+                ptrs.append(p.value + off)
+                self._opened.append(p.value)
+            self.peer_rows.append(ptrs[0])
+            self.peer_codes.append(ptrs[1])
+
+    def close(self) -> None:
+        lib = _lib.load()
+        for p in self._opened:
+            lib.bgl_ipc_close(p)
+        self._opened = []
+
+    def _a2a_any(self, out, inp, out_splits, in_splits):
+        if self.cpu:
+            o = torch.empty(out.shape, dtype=out.dtype)
+            dist.all_to_all_single(o, inp.cpu(), out_splits, in_splits, group=self.group)
+            out.copy_(o)
+        else:
+            dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
+
+    def step(self, ids: torch.Tensor):
+        part, pos, counts = self.ops.partition(ids)
+        send_counts = counts.to(torch.int64)
+        if self.cpu:
+            recv_counts = torch.empty(self.world, dtype=torch.int64)
+            dist.all_to_all_single(recv_counts, send_counts.cpu(), group=self.group)
+        else:
+            recv_counts = torch.empty_like(send_counts)
+            dist.all_to_all_single(recv_counts, send_counts, group=self.group)
+        sc = send_counts.cpu().tolist()
+        rc = recv_counts.cpu().tolist()
+        recv_ids = torch.empty(sum(rc), dtype=torch.int32, device=ids.device)
+        recv_pos = torch.empty(sum(rc), dtype=torch.int32, device=ids.device)
+        self._a2a_any(recv_ids, part.contiguous(), rc, sc)
+        self._a2a_any(recv_pos, pos.contiguous(), rc, sc)
+        off = 0
+        for w in range(self.world):           # worker order == global batch order of the round
+            c = rc[w]
+            # staging is reused per bucket: stream order puts this bucket's ring
+            # insert (which reads it) before the next bucket's gather
+            self.engine.serve_push(recv_ids[off:off + c], w, recv_pos[off:off + c], self.peer_rows[w],
+                                   self.peer_codes[w], self.staging_rows[:c], self.staging_codes[:c])
+            off += c
+        # every home's pushes into this rank's buffers must have landed
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        n = int(ids.numel())
+        return self.out_rows[:n], self.out_codes[:n]

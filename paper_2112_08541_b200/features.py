@@ -124,6 +124,25 @@ class FeatureCacheEngine:
             events[2].record()
         return out
 
+    def retrieve_push(self, ids, n_dev, max_n, worker, out, codes, push_rows, push_pos, counters, stream=None):
+        """Home-side step of the sharded multi-GPU cache: lookup, gather with
+        every row also stored straight into the worker GPU's output at
+        push_pos (peer memory, bgl_gather_rows_push), insert-after-batch with
+        the ring rows copied from the local `out`."""
+        lib = _lib.load()
+        st = _lib.stream_ptr(stream)
+        h = self.dev.handle
+        _lib.check(lib.bgl_cache_lookup(h, ids.data_ptr(), n_dev.data_ptr(), max_n, worker, ids.data_ptr(),
+                                        n_dev.data_ptr(), max_n, codes.data_ptr(), self.src_row.data_ptr(),
+                                        counters.data_ptr(), st))
+        ring = self.dev.rows_ptr() or None
+        passes = [(0, 0)] if self.features.is_cuda else [(1, 0), (2, self.miss_ctas)]
+        for mode, ctas in passes:
+            _lib.check(lib.bgl_gather_rows_push(ids.data_ptr(), self.src_row.data_ptr(), n_dev.data_ptr(), max_n,
+                                                ring, self.table, self.row_bytes, out.data_ptr(), push_rows,
+                                                push_pos.data_ptr(), mode, ctas, st))
+        _lib.check(lib.bgl_cache_insert(h, ids.data_ptr(), max_n, out.data_ptr(), counters.data_ptr(), st))
+
     # -- split form for the software-pipelined step (pipeline.py) ----------------
     def plan_buffers(self):
         """(plan int32 [d, stride, 2], plan_count int64 [d]) for front/back."""
