@@ -240,6 +240,16 @@ int bgl_select_pending(const int32_t* shard, int64_t len, const uint8_t* flags, 
 int bgl_interleave(const int32_t* seq_concat, const int64_t* seq_off, const int64_t* shift,
                    int32_t S, int64_t total, int32_t* out, void* stream);
 
+/* Shuffling error of a schedule (gnnio.ordering.shuffling_error,
+ * ordering.py:157-186): tv_out[i] = 0.5 * sum_c |cnt_i[c]/len_i - cnt[c]/total|
+ * in fp64 for the batches order[batch_off[i] .. batch_off[i+1]) (device
+ * int64[num_batches+1]); labels[v] in [0, num_classes), else *bad_label_dev
+ * = 1. workspace: bgl_shuffling_workspace(num_classes) bytes. */
+size_t bgl_shuffling_workspace(int32_t num_classes);
+int bgl_shuffling_tv(const int32_t* labels, const int32_t* order, int64_t total, const int64_t* batch_off,
+                     int64_t num_batches, int32_t num_classes, void* workspace, double* tv_out,
+                     int32_t* bad_label_dev, void* stream);
+
 /* ---------------------------------------------------------------- multi-GPU exchange
  * Node-ID sharding of the cache across GPUs (home of v = v % H,
  * cachesim.py:505-506). Stable split of a sorted batch into H ascending

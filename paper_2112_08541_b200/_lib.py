@@ -63,6 +63,8 @@ PROTOTYPES = {
                                      c_vp, c_vp, c_vp, c_vp]),
     "bgl_select_pending": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "bgl_interleave": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp]),
+    "bgl_shuffling_workspace": (c_sz, [c_i32]),
+    "bgl_shuffling_tv": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "bgl_partition_workspace": (c_sz, [c_i64, c_i32]),
     "bgl_partition_by_home": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "bgl_scatter_rows": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp]),

@@ -194,6 +194,100 @@ def random_shuffle_schedule(g, b: int, seed: int = 0) -> BatchSchedule:
     return BatchSchedule(batches=_slice(perm, b), batch_size=b, policy="random")
 
 
+# ----------------------------------------------------------------------------- shuffling error
+
+@dataclass
+class ShufflingErrorReport:
+    """ordering.py:35-46."""
+
+    epsilon: float
+    threshold: float
+    num_sequences: int
+    per_batch_tv: np.ndarray
+    max_tv: float = 0.0
+    threshold_met: bool = True
+
+    def __post_init__(self):
+        if len(self.per_batch_tv):
+            self.max_tv = float(np.max(self.per_batch_tv))
+
+
+def shuffling_error_threshold(b: int, M: int, n: int) -> float:
+    """Convergence-safe bound sqrt(b*M)/n (ordering.py:49-51)."""
+    import math
+    return math.sqrt(b * M) / n
+
+
+def _device_labels(labels) -> tuple[torch.Tensor, int]:
+    if isinstance(labels, torch.Tensor):
+        lab = labels.to(device="cuda", dtype=torch.int32)
+        return lab, int(lab.max().item()) + 1 if lab.numel() else 1
+    lab = np.asarray(labels)
+    return torch.from_numpy(lab.astype(np.int32)).cuda(), int(lab.max()) + 1 if lab.size else 1
+
+
+def batch_tv_device(labels_dev: torch.Tensor, num_classes: int, order: torch.Tensor,
+                    batch_off: torch.Tensor) -> torch.Tensor:
+    """Per-batch TV distances (fp64, device) of a flat schedule (bgl_shuffling_tv)."""
+    nb = int(batch_off.numel()) - 1
+    total = int(order.numel())
+    tv = torch.empty(max(nb, 1), dtype=torch.float64, device="cuda")
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ws = torch.empty(int(_lib.load().bgl_shuffling_workspace(num_classes)), dtype=torch.uint8, device="cuda")
+    _lib.call("bgl_shuffling_tv", labels_dev.data_ptr(), order.data_ptr(), total, batch_off.data_ptr(), nb,
+              num_classes, ws.data_ptr(), tv.data_ptr(), bad.data_ptr(), _lib.stream_ptr())
+    if int(bad.item()):
+        raise ValueError("scheduled node without a label")
+    return tv[:nb]
+
+
+def _epsilon(tvs: np.ndarray, lens: np.ndarray, batch_size: int) -> float:
+    full = lens == batch_size
+    return float(tvs[full].mean()) if full.any() else float(tvs.mean())
+
+
+def shuffling_error(schedule: BatchSchedule, labels, threshold: float = 0.0,
+                    num_sequences: int = 1) -> ShufflingErrorReport:
+    """Per-batch total-variation distance of label frequencies vs the whole
+    schedule's; epsilon = mean over full-size batches (ordering.py:157-186)."""
+    lens = np.array([len(b) for b in schedule.batches], dtype=np.int64)
+    lab, ncls = _device_labels(labels)
+    order = torch.from_numpy(schedule.all_nodes().astype(np.int32)).cuda()
+    off = torch.from_numpy(np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)).cuda()
+    tvs = batch_tv_device(lab, ncls, order, off).cpu().numpy()
+    eps = _epsilon(tvs, lens, schedule.batch_size)
+    return ShufflingErrorReport(epsilon=eps, threshold=threshold, num_sequences=num_sequences, per_batch_tv=tvs,
+                                threshold_met=eps <= threshold if threshold > 0 else True)
+
+
+def select_num_sequences(g, b: int, M: int, S_max: int, seed: int = 0) -> tuple[int, ShufflingErrorReport]:
+    """Smallest S in [1, S_max] whose shifted-BFS schedule keeps the shuffling
+    error within sqrt(b*M)/n (ordering.py:210-231); every candidate schedule
+    and its error are computed on the device."""
+    if S_max < 1:
+        raise ValueError("S_max must be >= 1")
+    labels = getattr(g, "labels", None)
+    if labels is None:
+        raise ValueError("graph has no labels")
+    n = len(_train_ids(g))
+    threshold = shuffling_error_threshold(b, M, n)
+    lab, ncls = _device_labels(labels)
+    last = None
+    for S in range(1, S_max + 1):
+        flat, _ = proximity_schedule_device(g, S, b, seed=seed)
+        total = int(flat.numel())
+        lens = np.array([min(b, total - i) for i in range(0, total, b)], dtype=np.int64)
+        off = torch.arange(0, total + b, b, dtype=torch.int64, device="cuda").clamp_max(total)[: len(lens) + 1]
+        tvs = batch_tv_device(lab, ncls, flat, off).cpu().numpy()
+        eps = _epsilon(tvs, lens, b)
+        last = ShufflingErrorReport(epsilon=eps, threshold=threshold, num_sequences=S, per_batch_tv=tvs)
+        if eps <= threshold:
+            last.threshold_met = True
+            return S, last
+    last.threshold_met = False
+    return S_max, last
+
+
 def save_schedule(schedule: BatchSchedule, path) -> None:
     with open(path, "w") as f:
         f.write(f"# policy {schedule.policy} batch_size {schedule.batch_size}\n")

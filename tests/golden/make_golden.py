@@ -308,11 +308,45 @@ def make_static(gs):
     np.savez_compressed(os.path.join(HERE, "static.npz"), **out)
 
 
+def make_shuffle(gs):
+    """shuffling_error / select_num_sequences (ordering.py:157-231)."""
+    out = {}
+    graphs = {"planted": gs["planted"], "dense": gs["dense"],
+              "one_label": generate_power_law(2000, 8, seed=4, train_fraction=0.1, num_labels=1),
+              "two_comm": generate_power_law(5000, 10, seed=3, train_fraction=0.1, num_labels=2)}
+    for name, g in graphs.items():
+        store_graph(out, name, g)
+        out[f"g_{name}_labels"] = g.labels.astype(np.int64)
+    out["graph_names"] = np.array(list(graphs))
+    meta, tvs, eps = [], [], []
+    for gi, (name, g) in enumerate(graphs.items()):
+        for kind, S, b, seed in (("prox", 1, 50, 0), ("prox", 3, 25, 1), ("prox", 4, 64, 2), ("rand", 0, 50, 3),
+                                 ("rand", 0, 2000, 0)):
+            sched = od.proximity_schedule(g, S, b, seed=seed) if kind == "prox" else \
+                od.random_shuffle_schedule(g, b, seed=seed)
+            rep = od.shuffling_error(sched, g.labels)
+            meta.append((gi, 0 if kind == "prox" else 1, S, b, seed))
+            tvs.append(rep.per_batch_tv)
+            eps.append(rep.epsilon)
+    sel = []
+    for gi, (name, g) in enumerate(graphs.items()):
+        for b, M, S_max, seed in ((50, 4, 8, 0), (250, 4, 10, 0), (25, 2, 5, 1)):
+            S, rep = od.select_num_sequences(g, b, M, S_max, seed=seed)
+            sel.append((gi, b, M, S_max, seed, S, int(rep.threshold_met)))
+            eps.append(rep.epsilon)
+    out["meta"] = np.array(meta, dtype=np.int64)
+    put(out, "tvs", tvs, np.float64)
+    out["eps"] = np.array(eps, dtype=np.float64)
+    out["select"] = np.array(sel, dtype=np.int64)
+    np.savez_compressed(os.path.join(HERE, "shuffle.npz"), **out)
+
+
 if __name__ == "__main__":
     gs = graphs()
     make_sampler(gs)
     make_cache()
     make_ordering(gs)
     make_static(gs)
-    for f in ("sampler.npz", "cache.npz", "ordering.npz", "static.npz"):
+    make_shuffle(gs)
+    for f in ("sampler.npz", "cache.npz", "ordering.npz", "static.npz", "shuffle.npz"):
         print(f, os.path.getsize(os.path.join(HERE, f)))
