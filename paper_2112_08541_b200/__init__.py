@@ -9,15 +9,26 @@ CPU fallback.
 """
 
 from . import cachesim, features, graph, ordering, sampler  # noqa: F401
-from .cachesim import CacheConfig, CacheSimReport, amortized_update_ops, compare_policies, simulate  # noqa: F401
+from .cachesim import (  # noqa: F401
+    CacheConfig,
+    CacheSimReport,
+    amortized_update_ops,
+    compare_policies,
+    simulate,
+    warm_static,
+)
 from .graph import DeviceGraph, Graph, generate_power_law_device  # noqa: F401
 from .ordering import (  # noqa: F401
     BatchSchedule,
+    ShufflingErrorReport,
     form_batches,
     generate_bfs_sequences,
     proximity_schedule,
     random_shift,
     random_shuffle_schedule,
+    select_num_sequences,
+    shuffling_error,
+    shuffling_error_threshold,
 )
 from .sampler import AccessTrace, EpochCommReport, SamplingConfig, sample_batch, simulate_epoch  # noqa: F401
 
