@@ -202,7 +202,7 @@ sample_fused_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
                     ScanState ss, int64_t* __restrict__ deg_prefix, int64_t* __restrict__ k_prefix,
                     int32_t* __restrict__ heavy, int64_t* __restrict__ heavy_count,
                     int32_t* __restrict__ out_ids, int32_t* __restrict__ out_pidx, int64_t* __restrict__ num_out,
-                    uint32_t* __restrict__ bitmap, int32_t run) {
+                    uint32_t* __restrict__ bitmap, int32_t run, int64_t heavy_deg) {
     const int64_t n = *num_parents_dev;
     const int64_t nruns = n > 0 ? ceil_div(n, run) : 1;
     const int lane = lane_id();
@@ -237,7 +237,7 @@ sample_fused_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
         const int64_t pre_k = warp_lookback1(ss.status + ss.max_tiles, r, agg_k);
         const int64_t ex_d = pre_d + incl_d - deg;   // draws before this parent (relative to D0)
         const int64_t ex_k = pre_k + incl_k - k;     // outputs before this parent
-        const bool hv = valid && (k > 32 || deg > kNarrowMaxDeg);
+        const bool hv = valid && (k > 32 || deg > heavy_deg);
         const unsigned hm = __ballot_sync(0xffffffffu, hv);
         if (hm) {
             int64_t slot = 0;
@@ -261,7 +261,7 @@ sample_fused_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
             const int64_t dg = __shfl_sync(0xffffffffu, deg, i);
             if (dg == 0) continue;                    // consumes no draws (sampler.py:77-79)
             const int ki = (int)__shfl_sync(0xffffffffu, k, i);
-            if (ki > 32 || dg > kNarrowMaxDeg) {      // heavy: sample_heavy_kernel
+            if (ki > 32 || dg > heavy_deg) {          // heavy: sample_heavy_kernel
                 have = false;
                 continue;
             }
@@ -442,6 +442,9 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     int64_t run = ceil_div(std::max<int64_t>(max_parents, 1), want_runs);
     run = std::min<int64_t>(std::max<int64_t>(run, 1), kRun);
     const int64_t runs = std::max<int64_t>(1, ceil_div(max_parents, run));
+    // parents above this degree go to the 8-warp CTA kernel (lower thresholds
+    // for the small hops were measured slower: the CTA kernel runs after it)
+    const int64_t heavy_deg = kNarrowMaxDeg;
     ScanState ss = make_scan_state(w.scan, 2, w.max_tiles);
     unsigned blocks = (unsigned)ceil_div(runs, kWarpsPerBlock);
     const unsigned cap_blocks = (unsigned)kNumSMs * 8;
@@ -449,7 +452,7 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     if (max_ctas > 0 && blocks > (unsigned)max_ctas) blocks = (unsigned)max_ctas;
     sample_fused_kernel<<<blocks, kWarpsPerBlock * 32, 0, st>>>(
         indptr, indices, parents, num_parents_dev, fanout, table, draw_base, ss, w.deg_prefix, w.k_prefix, w.heavy,
-        w.heavy_count, out_ids, out_parent_idx, num_out_dev, bm, (int32_t)run);
+        w.heavy_count, out_ids, out_parent_idx, num_out_dev, bm, (int32_t)run, heavy_deg);
     BGL_TRY(launch_status("sample_fused_kernel"));
     if (max_parents == 0) return BGL_OK;
     int kcap = 32;

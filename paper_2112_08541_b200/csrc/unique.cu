@@ -13,7 +13,7 @@
 namespace bgl {
 
 constexpr int kUThreads = 256;
-constexpr int kUWordsPerThread = 8;
+constexpr int kUWordsPerThread = 2;   // small tiles: ~150 CTAs at the products shape
 constexpr int kUTileWords = kUThreads * kUWordsPerThread;
 
 struct UniqueWs {
@@ -29,7 +29,7 @@ static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 static UniqueWs carve_unique(void* ws, int64_t num_nodes) {
     UniqueWs u;
     u.nwords = ceil_div(num_nodes > 0 ? num_nodes : 1, 32);
-    u.nwords = ceil_div(u.nwords, kUWordsPerThread) * kUWordsPerThread;   // whole uint4 pairs
+    u.nwords = ceil_div(u.nwords, kUWordsPerThread) * kUWordsPerThread;   // whole uint2 loads
     char* p = reinterpret_cast<char*>(ws);
     u.bitmap = reinterpret_cast<uint32_t*>(p);
     p += al256(u.nwords * 4);
@@ -97,10 +97,9 @@ emit_kernel(const uint32_t* __restrict__ bitmap, int64_t nwords, ScanState ss,
     const int64_t w0 = tile * kUTileWords + (int64_t)threadIdx.x * kUWordsPerThread;
     uint32_t w[kUWordsPerThread];
     if (w0 < nwords) {
-        const uint4* p = reinterpret_cast<const uint4*>(bitmap + w0);
-        uint4 a = p[0], b = p[1];
-        w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
-        w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+        const uint2 a = *reinterpret_cast<const uint2*>(bitmap + w0);
+        w[0] = a.x;
+        w[1] = a.y;
     } else {
 #pragma unroll
         for (int j = 0; j < kUWordsPerThread; ++j) w[j] = 0;
