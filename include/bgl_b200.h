@@ -150,6 +150,14 @@ int bgl_cache_lookup(bgl_cache_t cache, const int32_t* ids, const int64_t* n_dev
                      int32_t worker, const int32_t* sorted_ids, const int64_t* n_sorted_dev,
                      int64_t max_sorted, uint8_t* codes, int64_t* src_row, int64_t* counters,
                      void* stream);
+/* The single-shard fused lookup (d == 1, ids sorted and distinct, as
+ * bgl_cache_lookup with sorted_ids == ids) that also writes the ascending
+ * batch positions of every device miss (H and M: rows that must come from the
+ * feature store) into caller-owned miss_pos[0..*miss_count) -- the compacted
+ * list bgl_gather_list consumes. */
+int bgl_cache_lookup_misses(bgl_cache_t cache, const int32_t* ids, const int64_t* n_dev, int64_t max_n,
+                            int32_t worker, uint8_t* codes, int64_t* src_row, int64_t* counters,
+                            int32_t* miss_pos, int64_t* miss_count, void* stream);
 /* Insert-after-batch (cachesim.py:527-530): device-missed into their home
  * ring, full misses into the host ring, ascending; counters[5..6] +=
  * insertions, evictions. When batch_rows != NULL, row i of the batch output
@@ -201,12 +209,20 @@ int bgl_cache_warm(bgl_cache_t cache, const int32_t* dev_nodes, const int64_t* d
  * device alias of pinned host memory (zero-copy miss path). src_row NULL:
  * plain gather out[i] = table[ids[i]]. row_bytes % 4 == 0. mode: 0 = every row,
  * 1 = only hits (src_row >= 0), 2 = only misses (src_row < 0). ctas > 0:
- * launch exactly ctas CTAs of two warps (the host-link miss path needs only
+ * launch exactly ctas CTAs of eight warps (the host-link miss path needs only
  * ~150 warps in flight, the rest of the GPU stays free for the sampler);
  * 0 = fill the GPU (HBM rows). */
 int bgl_gather_rows(const int32_t* ids, const int64_t* src_row, const int64_t* n_dev, int64_t max_n,
                     const void* ring_rows, const void* table, int64_t row_bytes, void* out,
                     int32_t mode, int32_t ctas, void* stream);
+/* Compacted gather: out[pos[j]] = table[ids[pos[j]]] for j < *count_dev
+ * (pos from bgl_cache_lookup_misses). rows_in_flight (0 = 4, or 2/4/8) rows
+ * per warp are loaded before any is stored; ctas > 0 launches exactly that
+ * many 8-warp CTAs. push_out/push_pos (both or neither): every row is also
+ * stored at push_out + push_pos[pos[j]] * row_bytes (home-push, peer memory). */
+int bgl_gather_list(const int32_t* pos, const int64_t* count_dev, int64_t max_n, const int32_t* ids,
+                    const void* table, int64_t row_bytes, void* out, void* push_out, const int32_t* push_pos,
+                    int32_t rows_in_flight, int32_t ctas, void* stream);
 /* Fill rows of the deterministic synthetic feature table (oracle/features_oracle.py). */
 int bgl_synthetic_features(int64_t first_node, int64_t num_nodes, int32_t dim, uint64_t seed,
                            float* out, void* stream);

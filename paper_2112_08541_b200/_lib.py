@@ -46,6 +46,7 @@ PROTOTYPES = {
     "bgl_cache_rows": (c_vp, [c_vp]),
     "bgl_cache_set_shard": (ctypes.c_int, [c_vp, c_i32, c_i32]),
     "bgl_cache_lookup": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "bgl_cache_lookup_misses": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "bgl_cache_insert": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "bgl_cache_plan_stride": (c_i64, [c_vp, c_i64]),
     "bgl_cache_insert_plan": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
@@ -57,6 +58,7 @@ PROTOTYPES = {
     "bgl_compact_flags": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "bgl_cache_warm": (ctypes.c_int, [c_vp, c_vp, p_i64, c_vp, c_i64, c_vp]),
     "bgl_gather_rows":(ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_i32, c_i32, c_vp]),
+    "bgl_gather_list": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),
     "bgl_synthetic_features": (ctypes.c_int, [c_i64, c_i64, c_i32, c_u64, c_vp, c_vp]),
     "bgl_bfs_workspace": (c_sz, [c_i64]),
     "bgl_bfs_level": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64,

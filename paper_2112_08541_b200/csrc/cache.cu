@@ -204,7 +204,8 @@ lookup_fused_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__
                     int64_t C,
                     const int32_t* __restrict__ slot_of, const int32_t* __restrict__ hslot_of,
                     uint8_t* __restrict__ codes, int64_t* __restrict__ src_row, int64_t* __restrict__ counters,
-                    ScanState ss, int32_t* __restrict__ lists, int64_t list_cap, int64_t* __restrict__ mcount) {
+                    ScanState ss, int32_t* __restrict__ lists, int64_t list_cap, int64_t* __restrict__ mcount,
+                    int32_t* __restrict__ miss_pos, int64_t* __restrict__ miss_count) {
     constexpr int NW = kCThreads / 32;
     __shared__ int32_t s_w[2][kCRounds][NW];
     __shared__ int64_t s_c[4];
@@ -274,7 +275,10 @@ lookup_fused_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__
             pd += s_w[0][r][w];
             pf += s_w[1][r][w];
         }
-        if ((bm_d[r] >> lane) & 1u) lists[pd] = (int32_t)e;
+        if ((bm_d[r] >> lane) & 1u) {
+            lists[pd] = (int32_t)e;
+            if (miss_pos) miss_pos[pd] = (int32_t)e;   // caller-owned copy for the compacted miss gather
+        }
         if ((bm_f[r] >> lane) & 1u) lists[list_cap + pf] = (int32_t)e;
         for (int w = 0; w < NW; ++w) {
             run_d += s_w[0][r][w];
@@ -284,6 +288,7 @@ lookup_fused_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__
     if (tile == ntiles - 1 && threadIdx.x == 0) {
         mcount[0] = s_pre[0] + s_agg[0];
         mcount[1] = s_pre[1] + s_agg[1];
+        if (miss_count) *miss_count = s_pre[0] + s_agg[0];
     }
 }
 
@@ -522,7 +527,7 @@ int bgl_cache_lookup(bgl_cache_t c, const int32_t* ids, const int64_t* n_dev, in
         BGL_TRY(reset_scan_state(c->tile_counts, 2, ntiles, st));
         lookup_fused_kernel<<<(unsigned)ntiles, kCThreads, 0, st>>>(
             ids, n_dev, worker, c->shard_index, c->C, c->slot_of, c->hslot_of, codes, src_row, counters,
-            make_scan_state(c->tile_counts, 2, ntiles), c->lists, c->list_cap, c->mcount);
+            make_scan_state(c->tile_counts, 2, ntiles), c->lists, c->list_cap, c->mcount, nullptr, nullptr);
         return launch_status("lookup_fused_kernel");
     }
     if (max_n > 0) {
@@ -539,6 +544,23 @@ int bgl_cache_lookup(bgl_cache_t c, const int32_t* ids, const int64_t* n_dev, in
     miss_scatter_kernel<<<(unsigned)ntiles, kCThreads, 0, st>>>(sorted_ids, n_sorted_dev, c->d, c->slot_of,
                                                                 c->hslot_of, c->tile_counts, c->lists, c->list_cap);
     return launch_status("miss_scatter_kernel");
+}
+
+int bgl_cache_lookup_misses(bgl_cache_t c, const int32_t* ids, const int64_t* n_dev, int64_t max_n, int32_t worker,
+                            uint8_t* codes, int64_t* src_row, int64_t* counters, int32_t* miss_pos,
+                            int64_t* miss_count, void* stream) {
+    BGL_CHECK_ARG(c && ids && n_dev && counters && miss_pos && miss_count, "bgl_cache_lookup_misses: null pointer");
+    BGL_CHECK_ARG(c->d == 1, "bgl_cache_lookup_misses: single-shard handles only (use bgl_cache_lookup)");
+    const int32_t nglobal = c->global_shards > 0 ? c->global_shards : c->d;
+    BGL_CHECK_ARG(worker >= 0 && worker < nglobal, "worker device out of range");
+    BGL_CHECK_ARG(max_n <= c->list_cap, "batch larger than reserved (call bgl_cache_reserve_batch)");
+    cudaStream_t st = as_stream(stream);
+    const int64_t ntiles = std::max<int64_t>(1, ceil_div(max_n, kCTile));
+    BGL_TRY(reset_scan_state(c->tile_counts, 2, ntiles, st));
+    lookup_fused_kernel<<<(unsigned)ntiles, kCThreads, 0, st>>>(
+        ids, n_dev, worker, c->shard_index, c->C, c->slot_of, c->hslot_of, codes, src_row, counters,
+        make_scan_state(c->tile_counts, 2, ntiles), c->lists, c->list_cap, c->mcount, miss_pos, miss_count);
+    return launch_status("lookup_fused_kernel");
 }
 
 int bgl_cache_insert(bgl_cache_t c, const int32_t* sorted_ids, int64_t max_sorted, const void* batch_rows,

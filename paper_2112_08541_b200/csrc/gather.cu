@@ -81,6 +81,54 @@ gather_v4_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ sr
     }
 }
 
+// Compacted miss list (bgl_cache_lookup_misses): row j of the list is batch
+// position pos[j]; out[pos[j]] = table[ids[pos[j]]]. Every warp keeps R real
+// rows in flight (the mode-2 pass above skips the ~2/3 hits of each group of
+// kRows and so has ~1.3 rows in flight per warp on the host link).
+template <int R>
+__global__ void __launch_bounds__(kGThreads)
+gather_list_kernel(const int32_t* __restrict__ pos, const int64_t* __restrict__ count_dev,
+                   const int32_t* __restrict__ ids, const unsigned char* __restrict__ table, int64_t rb,
+                   unsigned char* __restrict__ out, unsigned char* __restrict__ push_out,
+                   const int32_t* __restrict__ push_pos) {
+    const int64_t n = *count_dev;
+    const int cpr = (int)(rb >> 4);
+    const int lane = lane_id();
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j0 = w * R; j0 < n; j0 += nw * R) {
+        const unsigned char* src[R];
+        int64_t dst[R];
+        // one lane per row fetches (pos, id); broadcast by shuffle
+        int32_t my_p = -1, my_id = 0;
+        if (lane < R && j0 + lane < n) {
+            my_p = __ldg(pos + j0 + lane);
+            my_id = __ldg(ids + my_p);
+        }
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            const int32_t p = __shfl_sync(0xffffffffu, my_p, u);
+            const int32_t v = __shfl_sync(0xffffffffu, my_id, u);
+            src[u] = p >= 0 ? table + (int64_t)v * rb : nullptr;
+            dst[u] = p;
+        }
+        for (int c = lane; c < cpr; c += 32) {
+            uint4 v[R];
+#pragma unroll
+            for (int u = 0; u < R; ++u)
+                if (src[u]) v[u] = ld_nc_v4(src[u] + c * 16);
+#pragma unroll
+            for (int u = 0; u < R; ++u)
+                if (src[u]) st_na_v4(out + dst[u] * rb + c * 16, v[u]);
+            if (push_out) {
+#pragma unroll
+                for (int u = 0; u < R; ++u)
+                    if (src[u]) st_na_v4(push_out + (int64_t)__ldg(push_pos + dst[u]) * rb + c * 16, v[u]);
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kGThreads)
 gather_v1_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ src_row,
                  const int64_t* __restrict__ n_dev, const unsigned char* __restrict__ ring,
@@ -175,6 +223,29 @@ int bgl_gather_rows_push(const int32_t* ids, const int64_t* src_row, const int64
         ids, src_row, n_dev, (const unsigned char*)ring_rows, (const unsigned char*)table, row_bytes,
         (unsigned char*)out, mode, (unsigned char*)push_out, push_pos);
     return launch_status("gather_v4_kernel(push)");
+}
+
+int bgl_gather_list(const int32_t* pos, const int64_t* count_dev, int64_t max_n, const int32_t* ids,
+                    const void* table, int64_t row_bytes, void* out, void* push_out, const int32_t* push_pos,
+                    int32_t rows_in_flight, int32_t ctas, void* stream) {
+    BGL_CHECK_ARG(pos && count_dev && ids && table && out, "bgl_gather_list: null pointer");
+    BGL_CHECK_ARG((push_out == nullptr) == (push_pos == nullptr), "bgl_gather_list: push_out and push_pos go together");
+    BGL_CHECK_ARG(row_bytes % 16 == 0 && (uintptr_t)table % 16 == 0 && (uintptr_t)out % 16 == 0 &&
+                      (uintptr_t)push_out % 16 == 0,
+                  "bgl_gather_list: 16-byte aligned rows required");
+    BGL_CHECK_ARG(rows_in_flight == 0 || rows_in_flight == 2 || rows_in_flight == 4 || rows_in_flight == 8,
+                  "rows_in_flight must be 0 (default), 2, 4 or 8");
+    if (max_n <= 0) return BGL_OK;
+    const int R = rows_in_flight ? rows_in_flight : 4;
+    unsigned grid = ctas > 0 ? (unsigned)ctas : grid_for(ceil_div(max_n, R) * 32, kGThreads, 4);
+    cudaStream_t st = as_stream(stream);
+    auto T = (const unsigned char*)table;
+    auto O = (unsigned char*)out;
+    auto P = (unsigned char*)push_out;
+    if (R == 2) gather_list_kernel<2><<<grid, kGThreads, 0, st>>>(pos, count_dev, ids, T, row_bytes, O, P, push_pos);
+    else if (R == 8) gather_list_kernel<8><<<grid, kGThreads, 0, st>>>(pos, count_dev, ids, T, row_bytes, O, P, push_pos);
+    else gather_list_kernel<4><<<grid, kGThreads, 0, st>>>(pos, count_dev, ids, T, row_bytes, O, P, push_pos);
+    return launch_status("gather_list_kernel");
 }
 
 int bgl_synthetic_features(int64_t first_node, int64_t num_nodes, int32_t dim, uint64_t seed, float* out,

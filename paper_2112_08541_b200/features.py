@@ -15,6 +15,8 @@ device state, and `retrieve` returns the rows `F[batch]` byte-exactly:
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -86,7 +88,8 @@ class FeatureCacheEngine:
         # host-link miss gather: 74 CTAs x 8 warps saturate the link while
         # leaving half the SMs' load/store pipes to the overlapped sampler
         # (tools/gather_bench.cu, tools/overlap_probe*.py)
-        self.miss_ctas = 74
+        self.miss_ctas = int(os.environ.get("BGL_MISS_CTAS", 74))
+        self.miss_rows_in_flight = int(os.environ.get("BGL_MISS_ROWS", 2))
 
     def retrieve_device(self, ids: torch.Tensor, n_dev: torch.Tensor, max_n: int, worker: int,
                         counters: torch.Tensor | None = None, stream=None, out: torch.Tensor | None = None,
@@ -159,20 +162,33 @@ class FeatureCacheEngine:
             events[0].record()
         self.miss_gather(ids, n_dev, max_n, out, src_row, stream)
 
-    def lookup_insert(self, ids, n_dev, max_n, worker, codes, src_row, plan, plan_count, counters, stream=None):
+    def lookup_insert(self, ids, n_dev, max_n, worker, codes, src_row, plan, plan_count, counters, stream=None,
+                      miss_pos=None, miss_count=None):
+        """miss_pos/miss_count given (single-shard engines): the lookup also
+        writes the compacted list of device-miss positions for miss_gather."""
         lib = _lib.load()
         st = _lib.stream_ptr(stream)
         h = self.dev.handle
-        _lib.check(lib.bgl_cache_lookup(h, ids.data_ptr(), n_dev.data_ptr(), max_n, worker, ids.data_ptr(),
-                                        n_dev.data_ptr(), max_n, codes.data_ptr(), src_row.data_ptr(),
-                                        counters.data_ptr(), st))
+        if miss_pos is not None:
+            _lib.check(lib.bgl_cache_lookup_misses(h, ids.data_ptr(), n_dev.data_ptr(), max_n, worker,
+                                                   codes.data_ptr(), src_row.data_ptr(), counters.data_ptr(),
+                                                   miss_pos.data_ptr(), miss_count.data_ptr(), st))
+        else:
+            _lib.check(lib.bgl_cache_lookup(h, ids.data_ptr(), n_dev.data_ptr(), max_n, worker, ids.data_ptr(),
+                                            n_dev.data_ptr(), max_n, codes.data_ptr(), src_row.data_ptr(),
+                                            counters.data_ptr(), st))
         _lib.check(lib.bgl_cache_insert_plan(h, ids.data_ptr(), max_n, plan.data_ptr(), plan_count.data_ptr(),
                                              counters.data_ptr(), st))
 
-    def miss_gather(self, ids, n_dev, max_n, out, src_row, stream=None):
+    def miss_gather(self, ids, n_dev, max_n, out, src_row, stream=None, miss_pos=None, miss_count=None):
         lib = _lib.load()
         st = _lib.stream_ptr(stream)
         ctas = 0 if self.features.is_cuda else self.miss_ctas
+        if miss_pos is not None:     # compacted list: every warp keeps real rows in flight
+            _lib.check(lib.bgl_gather_list(miss_pos.data_ptr(), miss_count.data_ptr(), max_n, ids.data_ptr(),
+                                           self.table, self.row_bytes, out.data_ptr(), None, None,
+                                           self.miss_rows_in_flight, ctas, st))
+            return
         _lib.check(lib.bgl_gather_rows(ids.data_ptr(), src_row.data_ptr(), n_dev.data_ptr(), max_n,
                                        self.dev.rows_ptr() or None, self.table, self.row_bytes, out.data_ptr(), 2,
                                        ctas, st))

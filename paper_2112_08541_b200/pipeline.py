@@ -65,6 +65,10 @@ class MiniBatchPipeline:
         self.codes_buf = [torch.empty(self.max_uniq, dtype=torch.uint8, device="cuda") for _ in range(NB)]
         self.src_row = [torch.empty(self.max_uniq, dtype=torch.int64, device="cuda") for _ in range(NB)]
         self.plans = [self.engine.plan_buffers() for _ in range(NB)]
+        # compacted device-miss positions of each batch (written by the lookup)
+        self.miss_pos = [torch.empty(self.max_uniq, dtype=torch.int32, device="cuda") for _ in range(NB)]
+        self.miss_count = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in range(NB)]
+        self.compact_misses = True
         self.tables = pcg_tables(pcg_states(seed, range(self.num_batches)))
         self.table_stage = [torch.empty((65, 4), dtype=torch.int64, device="cuda") for _ in range(NS)]
         self.batch_counter = torch.zeros(1, dtype=torch.int64, device="cuda")
@@ -103,12 +107,17 @@ class MiniBatchPipeline:
         j = batch % NB
         plan, pcount = self.plans[j]
         self.engine.lookup_insert(s.uniq, s.num_uniq, s.max_uniq, 0, self.codes_buf[j], self.src_row[j], plan,
-                                  pcount, self.counters, stream=stream)
+                                  pcount, self.counters, stream=stream, miss_pos=self.miss_pos[j],
+                                  miss_count=self.miss_count[j])
 
     def _miss(self, batch: int, stream=None) -> None:
         s = self.samplers[batch % NS]
         j = batch % NB
-        self.engine.miss_gather(s.uniq, s.num_uniq, s.max_uniq, self.outs[j], self.src_row[j], stream=stream)
+        if self.compact_misses:
+            self.engine.miss_gather(s.uniq, s.num_uniq, s.max_uniq, self.outs[j], self.src_row[j], stream=stream,
+                                    miss_pos=self.miss_pos[j], miss_count=self.miss_count[j])
+        else:   # mode-2 pass over the whole batch (kept for comparison)
+            self.engine.miss_gather(s.uniq, s.num_uniq, s.max_uniq, self.outs[j], self.src_row[j], stream=stream)
 
     def _back(self, batch: int, stream=None, fed: bool = False, events=None) -> None:
         s = self.samplers[batch % NS]

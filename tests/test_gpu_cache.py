@@ -160,3 +160,61 @@ def test_static_degree_policy_matches_reference(golden):
         assert sum(rep.batch_metadata_updates) == 0
     with pytest.raises(ValueError):
         cs.cold_state(cs.CacheConfig(device_capacity=2, policy="static-degree"))
+
+
+@pytest.mark.parametrize("rows_in_flight", [2, 4, 8])
+@pytest.mark.parametrize("where", ["host", "hbm"])
+def test_compacted_miss_list_and_gather(rows_in_flight, where):
+    """bgl_cache_lookup_misses writes exactly the ascending positions of the
+    device misses; bgl_gather_list fills those rows (and only those) with
+    F[id], plus the home-push copy at push_pos; the hit rows come from the
+    ring after the insert. Three batches through one engine vs the oracle."""
+    from paper_2112_08541_b200 import _lib
+    from paper_2112_08541_b200.cachesim import CacheConfig
+    from paper_2112_08541_b200.features import FeatureCacheEngine, synthetic_features
+
+    rng = np.random.default_rng(7)
+    n, dim, cap = 50000, 100, 3000
+    feats = synthetic_features(n, dim, seed=3, device_resident=(where == "hbm"))
+    eng = FeatureCacheEngine(CacheConfig(device_capacity=cap, feature_bytes_per_node=dim * 4), feats, max_batch=8000)
+    fifo = co.FifoEngine(cap, 0, 1)
+    lib = _lib.load()
+    for bi in range(3):
+        ids_np = np.unique(rng.integers(0, n // 4 if bi else n, 6000))
+        _, ref_codes = fifo.run([ids_np], [0])
+        ids = torch.from_numpy(ids_np.astype(np.int32)).cuda()
+        m = len(ids_np)
+        eng.n_dev.fill_(m)
+        codes = torch.empty(m, dtype=torch.uint8, device="cuda")
+        src = torch.empty(m, dtype=torch.int64, device="cuda")
+        mpos = torch.full((m,), -7, dtype=torch.int32, device="cuda")
+        mcnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        cnt = torch.zeros(8, dtype=torch.int64, device="cuda")
+        out = torch.zeros((m, dim), dtype=torch.float32, device="cuda")
+        push = torch.zeros((m + 5, dim), dtype=torch.float32, device="cuda")
+        push_pos = torch.from_numpy(rng.permutation(m + 5)[:m].astype(np.int32)).cuda()
+        _lib.check(lib.bgl_cache_lookup_misses(eng.dev.handle, ids.data_ptr(), eng.n_dev.data_ptr(), m, 0,
+                                               codes.data_ptr(), src.data_ptr(), cnt.data_ptr(), mpos.data_ptr(),
+                                               mcnt.data_ptr(), _lib.stream_ptr()))
+        assert np.array_equal(codes.cpu().numpy(), ref_codes[0])
+        miss = np.flatnonzero(ref_codes[0] >= 2)
+        assert int(mcnt.item()) == len(miss)
+        assert np.array_equal(mpos[: len(miss)].cpu().numpy(), miss)
+        _lib.check(lib.bgl_gather_list(mpos.data_ptr(), mcnt.data_ptr(), m, ids.data_ptr(), eng.table,
+                                       eng.row_bytes, out.data_ptr(), push.data_ptr(), push_pos.data_ptr(),
+                                       rows_in_flight, 0 if where == "hbm" else 37, _lib.stream_ptr()))
+        torch.cuda.synchronize()
+        ref = fo.synthetic_features(ids_np, dim, seed=3)
+        o = out.cpu().numpy()
+        assert np.array_equal(o[miss], ref[miss])
+        hit = np.flatnonzero(ref_codes[0] < 2)
+        assert not o[hit].any()                      # only the listed rows were written
+        assert np.array_equal(push.cpu().numpy()[push_pos.cpu().numpy()[miss]], ref[miss])
+        # hits from the ring, then insert-after-batch with the rows
+        _lib.check(lib.bgl_gather_rows(ids.data_ptr(), src.data_ptr(), eng.n_dev.data_ptr(), m,
+                                       eng.dev.rows_ptr(), eng.table, eng.row_bytes, out.data_ptr(), 1, 0,
+                                       _lib.stream_ptr()))
+        _lib.check(lib.bgl_cache_insert(eng.dev.handle, ids.data_ptr(), m, out.data_ptr(), cnt.data_ptr(),
+                                        _lib.stream_ptr()))
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), ref)

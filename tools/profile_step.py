@@ -31,8 +31,12 @@ for _ in range(a.warm):          # graph replays: warm cache (ncu does not see t
     pipe.step()
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStart()
+miss_rows = []
 for _ in range(a.steps):
+    k = pipe.k
     pipe.step_eager()
-torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    miss_rows.append(int(pipe.miss_count[(k + 1) % len(pipe.miss_count)].item()))   # rows of miss(k+1)
 torch.cuda.cudart().cudaProfilerStop()
 print("profiled", a.steps, "steps; counters", pipe.counters.tolist())
+print("miss-gather rows per profiled step", miss_rows, "row bytes", cfg["dim"] * 4)
