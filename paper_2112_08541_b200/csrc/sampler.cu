@@ -29,6 +29,9 @@
 // the neighbour IDs, so col traffic is k * 4 B per parent, not deg * 4 B.
 // Optionally every output is also marked in the dedup bitmap (fused K2 mark).
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "pcg64.cuh"
@@ -304,6 +307,175 @@ sample_fused_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
     }
 }
 
+// ---------------------------------------------------------------- threshold-candidate sampling
+// Same look-back prologue and lane-aligned per-parent stream walk as
+// sample_fused_kernel, but without a running top-k: a draw is a candidate when
+// m < T(k, deg), a per-parent threshold that keeps ~mu = k + 2.5 sqrt(k) + 2
+// of the parent's deg draws. Candidates are appended to a per-warp smem list;
+// after the parent's last chunk each candidate's rank is counted by broadcast
+// comparisons and the k smallest are written at their rank. Exact: with
+// L >= k candidates every non-candidate has m >= T > every candidate's m, so
+// the k smallest (m, t) overall are the k smallest candidates. L < k or L > 64
+// (rare) sends the parent to sample_heavy_kernel (full top-k over its draws).
+constexpr int kCandCap = 64;
+
+__device__ __forceinline__ uint64_t cand_threshold(int64_t k, int64_t deg) {
+    if (deg <= k) return 1ull << 53;
+    const double mu = (double)k + 2.5 * sqrt((double)k) + 2.0;
+    if (mu >= (double)deg) return 1ull << 53;
+    return (uint64_t)(mu / (double)deg * 9007199254740992.0);
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+sample_cand_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                   const int32_t* __restrict__ parents, const int64_t* __restrict__ num_parents_dev,
+                   int32_t fanout, const uint64_t* __restrict__ table, int64_t* __restrict__ draw_base,
+                   ScanState ss, int64_t* __restrict__ deg_prefix, int64_t* __restrict__ k_prefix,
+                   int32_t* __restrict__ heavy, int64_t* __restrict__ heavy_count,
+                   int32_t* __restrict__ out_ids, int32_t* __restrict__ out_pidx, int64_t* __restrict__ num_out,
+                   uint32_t* __restrict__ bitmap, int32_t run, int64_t heavy_deg) {
+    __shared__ uint64_t s_cand[kWarpsPerBlock][kCandCap];
+    uint64_t* cand = s_cand[warp_id()];
+    const int64_t n = *num_parents_dev;
+    const int64_t nruns = n > 0 ? ceil_div(n, run) : 1;
+    const int lane = lane_id();
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned FULL = 0xffffffffu;
+    const PcgTable T{table};
+    const U128 A32 = T.A(5), C32 = T.C(5);
+    const int64_t D0 = draw_base[0];
+    while (true) {
+        int64_t r = 0;
+        if (lane == 0) r = (int64_t)atomicAdd(ss.ticket, 1u);
+        r = __shfl_sync(FULL, r, 0);
+        if (r >= nruns) break;
+        const int64_t q = r * run + lane;
+        const bool valid = lane < run && q < n;
+        const int32_t p = valid ? parents[q] : 0;
+        const int64_t off = valid ? indptr[p] : 0;
+        const int64_t deg = valid ? indptr[p + 1] - off : 0;
+        const int64_t k = deg < fanout ? deg : fanout;
+        const int64_t incl_d = warp_incl_scan(deg);
+        const int64_t incl_k = warp_incl_scan(k);
+        const int64_t agg_d = __shfl_sync(FULL, incl_d, 31);
+        const int64_t agg_k = __shfl_sync(FULL, incl_k, 31);
+        if (lane == 0) {
+            const uint64_t f = r == 0 ? kFlagInc : kFlagAgg;
+            atomicExch((unsigned long long*)(ss.status + r), (unsigned long long)(f | ((uint64_t)agg_d & kValMask)));
+            atomicExch((unsigned long long*)(ss.status + ss.max_tiles + r),
+                       (unsigned long long)(f | ((uint64_t)agg_k & kValMask)));
+        }
+        const int64_t pre_d = warp_lookback1(ss.status, r, agg_d);
+        const int64_t pre_k = warp_lookback1(ss.status + ss.max_tiles, r, agg_k);
+        const int64_t ex_d = pre_d + incl_d - deg;
+        const int64_t ex_k = pre_k + incl_k - k;
+        const bool hv = valid && (k > 32 || deg > heavy_deg);
+        const unsigned hm = __ballot_sync(FULL, hv);
+        if (hm) {
+            int64_t slot = 0;
+            if (lane == 0) slot = (int64_t)atomicAdd((unsigned long long*)heavy_count, (unsigned long long)__popc(hm));
+            slot = __shfl_sync(FULL, slot, 0);
+            if (hv) {
+                heavy[slot + __popc(hm & lt)] = (int32_t)q;
+                deg_prefix[q] = ex_d;
+                k_prefix[q] = ex_k;
+            }
+        }
+        if (r == nruns - 1 && lane == 31) {
+            draw_base[1] = D0 + pre_d + incl_d;
+            *num_out = pre_k + incl_k;
+        }
+        const uint64_t Tm = (valid && !hv) ? cand_threshold(k, deg) : 0;
+        bool have = false;
+        U128 s{0, 0};
+        const int cnt = (int)((n - r * run) < run ? (n - r * run) : run);
+        for (int i = 0; i < cnt; ++i) {
+            const int64_t dg = __shfl_sync(FULL, deg, i);
+            if (dg == 0) continue;                    // consumes no draws (sampler.py:77-79)
+            if ((hm >> i) & 1u) {                     // heavy: sample_heavy_kernel
+                have = false;
+                continue;
+            }
+            const int ki = (int)__shfl_sync(FULL, k, i);
+            const uint64_t tm = __shfl_sync(FULL, Tm, i);
+            if (!have) {
+                s = T.at((uint64_t)(D0 + __shfl_sync(FULL, ex_d, i) + lane + 1));
+                have = true;
+            }
+            const int nc = (int)((dg + 31) >> 5);
+            int L = 0;
+            U128 sn;
+            for (int c = 0; c < nc; ++c) {
+                const int t = (c << 5) + lane;
+                const uint64_t m = draw_of_state(s);
+                sn = affine(A32, C32, s);            // next chunk (the last one feeds the hand-off)
+                const bool pass = t < dg && m < tm;
+                const unsigned bm = __ballot_sync(FULL, pass);
+                if (bm) {
+                    const int pos = L + __popc(bm & lt);
+                    if (pass && pos < kCandCap) cand[pos] = (m << 11) | (uint64_t)t;
+                    L += __popc(bm);
+                }
+                if (c + 1 < nc) s = sn;
+            }
+            {   // hand the stream to the next parent: lane l gets draw (dg + l) of this parent's stream
+                const int x = (int)(dg & 31) + lane;                   // offset into chunk nc-1 (if <32) else chunk nc
+                const int src = x & 31;
+                const bool nxt = ((int64_t)((nc - 1) << 5) + x) >= ((int64_t)nc << 5);
+                const uint64_t ahi = __shfl_sync(FULL, s.hi, src), alo = __shfl_sync(FULL, s.lo, src);
+                const uint64_t bhi = __shfl_sync(FULL, sn.hi, src), blo = __shfl_sync(FULL, sn.lo, src);
+                // dg not a multiple of 32: lanes with dg%32 + lane < 32 stay in chunk nc-1
+                const bool use_next = (dg & 31) == 0 ? true : nxt;
+                s.hi = use_next ? bhi : ahi;
+                s.lo = use_next ? blo : alo;
+            }
+            __syncwarp();
+            const int64_t oi = __shfl_sync(FULL, ex_k, i);
+            const int64_t gq = r * run + i;
+            if (L < ki || L > kCandCap) {             // rare: exact top-k over all draws in the CTA kernel
+                const int64_t dq = __shfl_sync(FULL, ex_d, i);
+                if (lane == 0) {
+                    const int64_t slot = (int64_t)atomicAdd((unsigned long long*)heavy_count, 1ull);
+                    heavy[slot] = (int32_t)gq;
+                    deg_prefix[gq] = dq;
+                    k_prefix[gq] = oi;
+                }
+                __syncwarp();
+                continue;
+            }
+            const int64_t offi = __shfl_sync(FULL, off, i);
+            const uint64_t c0 = lane < L ? cand[lane] : ~0ull;
+            int r0 = 0;
+            if (L <= 32) {
+#pragma unroll 4
+                for (int j = 0; j < L; ++j) r0 += cand[j] < c0;
+            } else {
+                const uint64_t c1 = lane + 32 < L ? cand[32 + lane] : ~0ull;
+                int r1 = 0;
+#pragma unroll 4
+                for (int j = 0; j < L; ++j) {
+                    const uint64_t kj = cand[j];
+                    r0 += kj < c0;
+                    r1 += kj < c1;
+                }
+                if (lane + 32 < L && r1 < ki) {
+                    const int32_t v = indices[offi + (int64_t)(c1 & 2047u)];
+                    out_ids[oi + r1] = v;
+                    out_pidx[oi + r1] = (int32_t)gq;
+                    if (bitmap) mark_bit(bitmap, v);
+                }
+            }
+            if (lane < L && r0 < ki) {
+                const int32_t v = indices[offi + (int64_t)(c0 & 2047u)];
+                out_ids[oi + r0] = v;
+                out_pidx[oi + r0] = (int32_t)gq;
+                if (bitmap) mark_bit(bitmap, v);
+            }
+            __syncwarp();
+        }
+    }
+}
+
 // ---------------------------------------------------------------- heavy parents
 constexpr int kHeavyThreads = 256;
 constexpr int kHeavyWarps = kHeavyThreads / 32;
@@ -441,6 +613,12 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     const int64_t want_runs = (int64_t)kNumSMs * 48 * 2;
     int64_t run = ceil_div(std::max<int64_t>(max_parents, 1), want_runs);
     run = std::min<int64_t>(std::max<int64_t>(run, 1), kRun);
+    // threshold-candidate kernel for fanout <= 32 (BGL_SAMPLER=fused: running top-k kernel)
+    static const int cand_env = [] {
+        const char* e = getenv("BGL_SAMPLER");
+        return (e && std::string(e) == "fused") ? 0 : 1;
+    }();
+    const bool use_cand = cand_env && fanout <= 32;
     const int64_t runs = std::max<int64_t>(1, ceil_div(max_parents, run));
     // parents above this degree go to the 8-warp CTA kernel (lower thresholds
     // for the small hops were measured slower: the CTA kernel runs after it)
@@ -450,10 +628,17 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     const unsigned cap_blocks = (unsigned)kNumSMs * 8;
     if (blocks > cap_blocks) blocks = cap_blocks;               // runs are claimed dynamically
     if (max_ctas > 0 && blocks > (unsigned)max_ctas) blocks = (unsigned)max_ctas;
-    sample_fused_kernel<<<blocks, kWarpsPerBlock * 32, 0, st>>>(
-        indptr, indices, parents, num_parents_dev, fanout, table, draw_base, ss, w.deg_prefix, w.k_prefix, w.heavy,
-        w.heavy_count, out_ids, out_parent_idx, num_out_dev, bm, (int32_t)run, heavy_deg);
-    BGL_TRY(launch_status("sample_fused_kernel"));
+    if (use_cand) {
+        sample_cand_kernel<<<blocks, kWarpsPerBlock * 32, 0, st>>>(
+            indptr, indices, parents, num_parents_dev, fanout, table, draw_base, ss, w.deg_prefix, w.k_prefix,
+            w.heavy, w.heavy_count, out_ids, out_parent_idx, num_out_dev, bm, (int32_t)run, heavy_deg);
+        BGL_TRY(launch_status("sample_cand_kernel"));
+    } else {
+        sample_fused_kernel<<<blocks, kWarpsPerBlock * 32, 0, st>>>(
+            indptr, indices, parents, num_parents_dev, fanout, table, draw_base, ss, w.deg_prefix, w.k_prefix,
+            w.heavy, w.heavy_count, out_ids, out_parent_idx, num_out_dev, bm, (int32_t)run, heavy_deg);
+        BGL_TRY(launch_status("sample_fused_kernel"));
+    }
     if (max_parents == 0) return BGL_OK;
     int kcap = 32;
     if (fanout > 32) {

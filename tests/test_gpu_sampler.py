@@ -124,7 +124,7 @@ def test_edge_cases(bgl):
     assert len(fr[0]) == 0 and len(fr[1]) == 0 and d.tolist() == [2]
 
 
-@pytest.mark.parametrize("fanouts", [(15, 10, 5), (25, 10), (40,), (3, 3, 3, 3)])
+@pytest.mark.parametrize("fanouts", [(15, 10, 5), (25, 10), (40,), (3, 3, 3, 3), (32, 2), (1, 1, 1)])
 def test_random_power_law_matches_oracle(bgl, fanouts):
     from paper_2112_08541_b200.graph import generate_power_law_device
     dg = generate_power_law_device(30000, 24, seed=5, train_fraction=0.1, num_labels=8)
@@ -136,6 +136,42 @@ def test_random_power_law_matches_oracle(bgl, fanouts):
         cfg = bgl.SamplingConfig(fanouts=fanouts, seed=11)
         fr, d = bgl.sample_batch(dg, seeds, cfg, batch_seed=bseed)
         fr_o, _, d_o, _ = so.sample_batch(hg.row_offsets, hg.col_indices, seeds, fanouts, 11, bseed)
+        for a, b in zip(fr, fr_o):
+            assert np.array_equal(a, b)
+        assert np.array_equal(d, d_o)
+
+
+@pytest.mark.parametrize("fanouts", [(5, 5), (32,), (12, 3)])
+def test_hubs_zero_degree_and_duplicates_match_oracle(bgl, fanouts):
+    """Parents the flat-stream kernel must route elsewhere or skip: hubs with
+    deg > 2048 (CTA kernel) sitting between light parents of the same run,
+    isolated (deg 0) parents, parents repeated in a hop, deg == fanout."""
+    rng = np.random.default_rng(3)
+    n = 12000
+    adj = [set() for _ in range(n)]
+    for h in (5, 6, 900):                       # three hubs, two adjacent IDs
+        for v in rng.choice(n, size=3000 + h, replace=False):
+            if v != h:
+                adj[h].add(int(v)); adj[int(v)].add(h)
+    for v in range(20, n - 1):                  # chain + random extra edges; 0..19 isolated
+        if v % 7:
+            adj[v].add(v + 1); adj[v + 1].add(v)
+        u = int(rng.integers(20, n))
+        if u != v:
+            adj[v].add(u); adj[u].add(v)
+    for v in range(20):
+        for u in list(adj[v]):
+            adj[u].discard(v)
+        adj[v] = set()
+    off = np.zeros(n + 1, np.int64)
+    off[1:] = np.cumsum([len(a) for a in adj])
+    col = np.concatenate([np.array(sorted(a), np.int64) for a in adj])
+    g = G(off, col)
+    seeds = np.concatenate([np.array([5, 6, 900, 0, 3, 5, 5, 6]), rng.integers(0, n, 500)])
+    for bseed in (1, 2):
+        cfg = bgl.SamplingConfig(fanouts=fanouts, seed=4)
+        fr, d = bgl.sample_batch(g, seeds, cfg, batch_seed=bseed)
+        fr_o, _, d_o, _ = so.sample_batch(off, col, seeds, fanouts, 4, bseed)
         for a, b in zip(fr, fr_o):
             assert np.array_equal(a, b)
         assert np.array_equal(d, d_o)
