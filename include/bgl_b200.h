@@ -54,8 +54,10 @@ int bgl_host_unregister(void* host_ptr);
  * drawn by `Generator.random` in gnnio/sampler.py:61-62,90.
  * states: uint64[nb][4] = (state_hi, state_lo, inc_hi, inc_lo) taken from
  *         numpy's bit_generator.state (the host keeps SeedSequence).
- * tables: uint64[nb][65][4]; row 0 = the state, row 1+k = (A_hi, A_lo, C_hi,
- *         C_lo) of the affine map advancing the LCG by 2^k steps. */
+ * tables: uint64[nb][BGL_PCG_TABLE_ROWS][4]; row 0 = the state, row
+ *         1 + 15*i + (j-1) = (A_hi, A_lo, C_hi, C_lo) of the affine map
+ *         advancing the LCG by j * 16^i steps (i < 16, 1 <= j <= 15). */
+#define BGL_PCG_TABLE_ROWS 241
 int bgl_pcg64_tables(const uint64_t* states, int64_t nb, uint64_t* tables, void* stream);
 /* 53-bit integers m of draws [first, first+n) of the stream of `table`
  * (Generator.random() == m * 2^-53). Parity/diagnostics only. */
@@ -297,7 +299,7 @@ int bgl_ipc_close(void* dev_ptr);
  * Step staging for the CUDA-graph-captured pipeline (no reference
  * counterpart: the reference loops batches in Python, sampler.py:136).
  * i = *batch_counter % num_batches; seeds_out = order[i*b, min((i+1)*b,
- * total)), *seed_count_out = its length, table_out = tables[i] (65x4),
+ * total)), *seed_count_out = its length, table_out = tables[i] (BGL_PCG_TABLE_ROWS x 4),
  * *batch_index_out = i (may be NULL); then *batch_counter += 1.
  * fed_count_dev != NULL (host-fed mode): `order` holds only this batch's
  * seeds (copied from the host), *fed_count_dev of them. */

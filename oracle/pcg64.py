@@ -63,14 +63,31 @@ def draw_u53(state: int, inc: int, index: int) -> int:
     return output(s) >> 11
 
 
+def affine_map(inc: int, delta: int) -> tuple[int, int]:
+    """(A, C) with s -> A*s + C advancing `delta` steps."""
+    acc_mult, acc_plus = 1, 0
+    cur_mult, cur_plus = MULT, inc
+    while delta > 0:
+        if delta & 1:
+            acc_mult = (acc_mult * cur_mult) & MASK128
+            acc_plus = (acc_plus * cur_mult + cur_plus) & MASK128
+        cur_plus = ((cur_mult + 1) * cur_plus) & MASK128
+        cur_mult = (cur_mult * cur_mult) & MASK128
+        delta >>= 1
+    return acc_mult, acc_plus
+
+
+TABLE_ROWS = 1 + 16 * 15
+
+
 def jump_table(state: int, inc: int) -> np.ndarray:
-    """[65, 4] uint64 rows. Row 0 = (state_hi, state_lo, inc_hi, inc_lo);
-    row 1+k = (A_hi, A_lo, C_hi, C_lo) with s -> A*s + C advancing 2**k steps.
-    Same layout the CUDA kernel `bgl_pcg64_tables` produces."""
+    """[241, 4] uint64 rows. Row 0 = (state_hi, state_lo, inc_hi, inc_lo);
+    row 1 + 15*i + (j-1) = (A_hi, A_lo, C_hi, C_lo) with s -> A*s + C
+    advancing j * 16**i steps. Same layout the CUDA kernel `bgl_pcg64_tables`
+    produces (a jump is one map per nonzero hex digit)."""
     rows = [(state >> 64, state & MASK64, inc >> 64, inc & MASK64)]
-    a, c = MULT, inc
-    for _ in range(64):
-        rows.append((a >> 64, a & MASK64, c >> 64, c & MASK64))
-        c = ((a + 1) * c) & MASK128
-        a = (a * a) & MASK128
+    for i in range(16):
+        for j in range(1, 16):
+            a, c = affine_map(inc, j * 16 ** i)
+            rows.append((a >> 64, a & MASK64, c >> 64, c & MASK64))
     return np.array(rows, dtype=np.uint64)

@@ -14,6 +14,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libbgl_b200.so")
 
+PCG_TABLE_ROWS = 241   # BGL_PCG_TABLE_ROWS (include/bgl_b200.h)
 BGL_OK, BGL_EINVAL, BGL_ECUDA, BGL_ENOMEM, BGL_EUNSUPPORTED = 0, 1, 2, 3, 4
 
 c_i32, c_i64, c_u64, c_sz, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_size_t, ctypes.c_void_p

@@ -13,28 +13,39 @@ void set_error(const char* fmt, ...) {
     va_end(ap);
 }
 
-// One thread per batch: row 0 = stream state; rows 1..64 = 2^k-step maps.
+__device__ __forceinline__ void compose(U128 A2, U128 C2, U128* A1, U128* C1) {   // (A1,C1) <- (A2,C2) o (A1,C1)
+    *C1 = add128(mul128(A2, *C1), C2);
+    *A1 = mul128(A2, *A1);
+}
+
+// One thread per (batch, hex digit position i): row 0 = stream state; rows
+// 1 + 15 i + (j-1) = the map advancing j * 16^i steps.
 __global__ void pcg64_tables_kernel(const uint64_t* __restrict__ states, int64_t nb,
                                     uint64_t* __restrict__ tables) {
-    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t b = gid >> 4;
+    const int i = (int)(gid & 15);
     if (b >= nb) return;
     const uint64_t* s = states + 4 * b;
-    uint64_t* t = tables + 65 * 4 * b;
-    t[0] = s[0];
-    t[1] = s[1];
-    t[2] = s[2];
-    t[3] = s[3];
+    uint64_t* t = tables + (int64_t)kPcgTableRows * 4 * b;
+    if (i == 0) {
+        t[0] = s[0];
+        t[1] = s[1];
+        t[2] = s[2];
+        t[3] = s[3];
+    }
+    // one step: s -> A s + inc; 16^i steps by squaring 4i times
     U128 A{2549297995355413924ull, 4865540595714422341ull};
     U128 C{s[2], s[3]};
-    const U128 one{0, 1};
-    for (int k = 0; k < 64; ++k) {
-        uint64_t* r = t + 4 * (1 + k);
-        r[0] = A.hi;
-        r[1] = A.lo;
-        r[2] = C.hi;
-        r[3] = C.lo;
-        C = mul128(add128(A, one), C);
-        A = mul128(A, A);
+    for (int sq = 0; sq < 4 * i; ++sq) compose(A, C, &A, &C);
+    U128 Aj = A, Cj = C;
+    for (int j = 1; j <= 15; ++j) {
+        uint64_t* r = t + 4 * (1 + 15 * i + (j - 1));
+        r[0] = Aj.hi;
+        r[1] = Aj.lo;
+        r[2] = Cj.hi;
+        r[3] = Cj.lo;
+        compose(A, C, &Aj, &Cj);
     }
 }
 
@@ -74,7 +85,7 @@ int bgl_pcg64_tables(const uint64_t* states, int64_t nb, uint64_t* tables, void*
     BGL_CHECK_ARG(nb >= 0, "bgl_pcg64_tables: nb < 0");
     if (nb == 0) return BGL_OK;
     BGL_CHECK_ARG(states && tables, "bgl_pcg64_tables: null pointer");
-    pcg64_tables_kernel<<<(unsigned)ceil_div(nb, 128), 128, 0, as_stream(stream)>>>(states, nb, tables);
+    pcg64_tables_kernel<<<(unsigned)ceil_div(nb * 16, 128), 128, 0, as_stream(stream)>>>(states, nb, tables);
     return launch_status("pcg64_tables_kernel");
 }
 

@@ -38,20 +38,34 @@ __host__ __device__ __forceinline__ uint64_t xsl_rr(U128 s) {
     return (x >> rot) | (x << ((64u - rot) & 63u));
 }
 
-// table layout: uint64 [65][4]; row 0 = (state_hi, state_lo, inc_hi, inc_lo);
-// row 1+k = (A_hi, A_lo, C_hi, C_lo) advancing 2^k steps.
+// table layout: uint64 [kPcgTableRows][4]; row 0 = (state_hi, state_lo,
+// inc_hi, inc_lo); row 1 + 15*i + (j-1) = (A_hi, A_lo, C_hi, C_lo) of the map
+// advancing j * 16^i steps (i = 0..15, j = 1..15): a jump of delta steps is
+// one affine map per nonzero hex digit of delta.
+constexpr int kPcgTableRows = 1 + 16 * 15;
+
 struct PcgTable {
     const uint64_t* t;
+    __device__ __forceinline__ const uint64_t* row(int i, int j) const { return t + 4 * (1 + 15 * i + (j - 1)); }
     __device__ __forceinline__ U128 state() const { return U128{__ldg(t + 0), __ldg(t + 1)}; }
-    __device__ __forceinline__ U128 A(int k) const { return U128{__ldg(t + 4 * (1 + k) + 0), __ldg(t + 4 * (1 + k) + 1)}; }
-    __device__ __forceinline__ U128 C(int k) const { return U128{__ldg(t + 4 * (1 + k) + 2), __ldg(t + 4 * (1 + k) + 3)}; }
+    // map advancing 2^k steps (k < 64)
+    __device__ __forceinline__ U128 A(int k) const {
+        const uint64_t* r = row(k >> 2, 1 << (k & 3));
+        return U128{__ldg(r + 0), __ldg(r + 1)};
+    }
+    __device__ __forceinline__ U128 C(int k) const {
+        const uint64_t* r = row(k >> 2, 1 << (k & 3));
+        return U128{__ldg(r + 2), __ldg(r + 3)};
+    }
     // State after `delta` steps from the stream start.
     __device__ __forceinline__ U128 at(uint64_t delta) const {
         U128 s = state();
         while (delta) {
-            int k = __ffsll((long long)delta) - 1;
-            s = affine(A(k), C(k), s);
-            delta &= delta - 1;
+            const int i = (__ffsll((long long)delta) - 1) >> 2;
+            const int j = (int)((delta >> (4 * i)) & 15u);
+            const uint64_t* r = row(i, j);
+            s = affine(U128{__ldg(r + 0), __ldg(r + 1)}, U128{__ldg(r + 2), __ldg(r + 3)}, s);
+            delta &= ~(15ull << (4 * i));
         }
         return s;
     }

@@ -4,6 +4,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "pcg64.cuh"
 
 namespace bgl {
 
@@ -17,7 +18,7 @@ __global__ void stage_batch_kernel(const int32_t* __restrict__ order, int64_t to
     const int64_t lo = fed_count ? 0 : i * b;
     const int64_t hi = fed_count ? *fed_count : (lo + b < total ? lo + b : total);
     for (int64_t k = threadIdx.x; k < hi - lo; k += blockDim.x) seeds_out[k] = order[lo + k];
-    for (int k = threadIdx.x; k < 65 * 4; k += blockDim.x) table_out[k] = tables[i * 65 * 4 + k];
+    for (int k = threadIdx.x; k < kPcgTableRows * 4; k += blockDim.x) table_out[k] = tables[i * kPcgTableRows * 4 + k];
     __syncthreads();
     if (threadIdx.x == 0) {
         *seed_count = hi - lo;

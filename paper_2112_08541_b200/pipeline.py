@@ -70,7 +70,7 @@ class MiniBatchPipeline:
         self.miss_count = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in range(NB)]
         self.compact_misses = True
         self.tables = pcg_tables(pcg_states(seed, range(self.num_batches)))
-        self.table_stage = [torch.empty((65, 4), dtype=torch.int64, device="cuda") for _ in range(NS)]
+        self.table_stage = [torch.empty((_lib.PCG_TABLE_ROWS, 4), dtype=torch.int64, device="cuda") for _ in range(NS)]
         self.batch_counter = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.batch_index = torch.zeros(NS, dtype=torch.int64, device="cuda")
         self.counters = torch.zeros(8, dtype=torch.int64, device="cuda")

@@ -83,10 +83,10 @@ def pcg_states(seed: int, batch_seeds) -> np.ndarray:
 
 
 def pcg_tables(states: np.ndarray, stream=None) -> torch.Tensor:
-    """Device jump tables uint64 [nb, 65, 4] (bgl_pcg64_tables)."""
+    """Device jump tables uint64 [nb, 241, 4] (bgl_pcg64_tables)."""
     nb = states.shape[0]
     dev_states = torch.from_numpy(states.view(np.int64).copy()).cuda()
-    tables = torch.empty((nb, 65, 4), dtype=torch.int64, device="cuda")
+    tables = torch.empty((nb, _lib.PCG_TABLE_ROWS, 4), dtype=torch.int64, device="cuda")
     _lib.call("bgl_pcg64_tables", _lib.ptr(dev_states), nb, _lib.ptr(tables), _lib.stream_ptr(stream))
     return tables
 
@@ -156,7 +156,7 @@ class BatchSampler:
 
     def run(self, table: torch.Tensor | int, stream=None, hooks=None) -> None:
         """Sample all hops and build the distinct set for the seeds already in
-        segment 0. `table` is the batch's PCG64 jump table (65x4 uint64)."""
+        segment 0. `table` is the batch's PCG64 jump table (241x4 uint64)."""
         lib = _lib.load()
         st = _lib.stream_ptr(stream)
         tptr = table if isinstance(table, int) else table.data_ptr()

@@ -69,14 +69,18 @@ def test_pcg64_restatement_matches_numpy():
     for i in (0, 1, 2, 5, 999, 1999):
         assert pcg64.draw_u53(st, inc, i) * 2.0 ** -53 == ref[i]
     table = pcg64.jump_table(st, inc)
-    assert table.shape == (65, 4)
-    # composing 2^k jumps equals advance()
+    assert table.shape == (pcg64.TABLE_ROWS, 4)
+    # composing one map per nonzero hex digit equals advance()
+    delta = 0x3B0A07
     s = st
-    for k in (0, 3, 10):
-        a = (int(table[1 + k, 0]) << 64) | int(table[1 + k, 1])
-        c = (int(table[1 + k, 2]) << 64) | int(table[1 + k, 3])
-        s = (a * s + c) & pcg64.MASK128
-    assert s == pcg64.advance(st, inc, 1 + 8 + 1024)
+    for i in range(6):
+        j = (delta >> (4 * i)) & 15
+        if j:
+            r = 1 + 15 * i + (j - 1)
+            a = (int(table[r, 0]) << 64) | int(table[r, 1])
+            c = (int(table[r, 2]) << 64) | int(table[r, 3])
+            s = (a * s + c) & pcg64.MASK128
+    assert s == pcg64.advance(st, inc, delta)
 
 
 def _cache_cases(npz):
