@@ -106,14 +106,31 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- inputs
 
-def build_inputs(cfg, features_where: str):
+def make_graph(cfg, kind: str):
+    """kind "exact": gnnio.graph.generate_power_law(n, avg_degree, seed=1,
+    train, labels) itself, rebuilt bit-identically by the native generator
+    (tests/golden/graphgen.npz); "continuum": the GPU continuum-limit model of
+    the same generator (papers100M scale, where the sequential process alone
+    would take minutes)."""
+    from paper_2112_08541_b200.graph import generate_power_law_device, generate_power_law_exact_device
+    gen = generate_power_law_exact_device if kind == "exact" else generate_power_law_device
+    return gen(cfg["n"], cfg["avg_degree"], seed=GRAPH_SEED, train_fraction=cfg["train"], num_labels=cfg["labels"])
+
+
+def graph_data(cfg, kind: str) -> str:
+    if kind == "exact":
+        return (f"synthetic: gnnio.graph.generate_power_law({cfg['n']}, {cfg['avg_degree']}, seed={GRAPH_SEED}, "
+                f"train_fraction={cfg['train']}, num_labels={cfg['labels']}) rebuilt bit-exactly by the native "
+                f"generator; hashed fp32 features")
+    return "synthetic (GPU continuum-limit power-law generator, seed 1; hashed fp32 features)"
+
+
+def build_inputs(cfg, features_where: str, graph_kind: str = "exact"):
     import torch
     from paper_2112_08541_b200.features import synthetic_features
-    from paper_2112_08541_b200.graph import generate_power_law_device
     from paper_2112_08541_b200.ordering import proximity_schedule_device
     t0 = time.time()
-    dg = generate_power_law_device(cfg["n"], cfg["avg_degree"], seed=GRAPH_SEED, train_fraction=cfg["train"],
-                                   num_labels=cfg["labels"])
+    dg = make_graph(cfg, graph_kind)
     torch.cuda.synchronize()
     t1 = time.time()
     feats = synthetic_features(cfg["n"], cfg["dim"], seed=GRAPH_SEED, device_resident=(features_where == "hbm"))
@@ -193,7 +210,7 @@ def run_bgl(args, cfg):
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    dg, feats, order, setup = build_inputs(cfg, args.features)
+    dg, feats, order, setup = build_inputs(cfg, args.features, args.graph)
     b = cfg["b"]
     cap = int(cfg["cache_frac"] * cfg["n"]) // world
     rb = cfg["dim"] * 4
@@ -343,8 +360,8 @@ def run_bgl(args, cfg):
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32 ids / u53 PCG64 keys / fp32 rows moved",
-        "data": "synthetic (GPU power-law generator, seed 1; hashed fp32 features)",
-        "config": {"workload": cfg["workload"], "num_nodes": cfg["n"], "csr_entries": dg.num_edges,
+        "data": graph_data(cfg, args.graph),
+        "config": {"workload": cfg["workload"], "graph": args.graph, "num_nodes": cfg["n"], "csr_entries": dg.num_edges,
                    "max_degree": dg.max_degree, "feature_dim": cfg["dim"], "fanouts": list(cfg["fanouts"]),
                    "batch": b, "cache_rows_per_gpu": cap, "features": args.features,
                    "parallelism": f"replicas{world}" if world > 1 else "single",
@@ -398,7 +415,7 @@ def run_sharded(args, cfg):
     rank, local_rank, world = dist_env()
     torch.cuda.set_device(local_rank)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    dg, feats, order, setup = build_inputs(cfg, args.features)
+    dg, feats, order, setup = build_inputs(cfg, args.features, args.graph)
     b, rb, dim = cfg["b"], cfg["dim"] * 4, cfg["dim"]
     cap = int(cfg["cache_frac"] * cfg["n"]) // world
     nb_total = (order.numel() + b - 1) // b
@@ -470,8 +487,8 @@ def run_sharded(args, cfg):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int32 ids / u53 PCG64 keys / fp32 rows moved",
-        "data": "synthetic (GPU power-law generator, seed 1; hashed fp32 features)",
-        "config": {"workload": cfg["workload"], "num_nodes": cfg["n"], "csr_entries": dg.num_edges,
+        "data": graph_data(cfg, args.graph),
+        "config": {"workload": cfg["workload"], "graph": args.graph, "num_nodes": cfg["n"], "csr_entries": dg.num_edges,
                    "feature_dim": cfg["dim"], "fanouts": list(cfg["fanouts"]), "batch": b,
                    "cache_rows_per_gpu": cap, "features": args.features,
                    "parallelism": f"dp{world} + node-ID-sharded FIFO cache (home = v % {world}); IDs by NCCL "
@@ -499,10 +516,8 @@ def run_reference(args, cfg):
     import torch
     torch.cuda.set_device(local_rank)
     from oracle import ordering_oracle as oo
-    from paper_2112_08541_b200.graph import generate_power_law_device
     # identical inputs: the same generated graph, copied to the host
-    dg = generate_power_law_device(cfg["n"], cfg["avg_degree"], seed=GRAPH_SEED, train_fraction=cfg["train"],
-                                   num_labels=cfg["labels"])
+    dg = make_graph(cfg, args.graph)
     hg = dg.to_host()
     del dg
     torch.cuda.empty_cache()
@@ -524,8 +539,9 @@ def run_reference(args, cfg):
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 * r["seconds"] / r["batches"], 2), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64 ids / fp64 priorities / fp32 rows moved",
-        "data": "synthetic (same generated graph + hashed features, on the host)", "impl": "reference",
-        "config": {"workload": cfg["workload"], "num_nodes": cfg["n"], "csr_entries": int(hg.num_edges),
+        "data": graph_data(cfg, args.graph) + " (same graph and features, on the host)", "impl": "reference",
+        "config": {"workload": cfg["workload"], "graph": args.graph, "num_nodes": cfg["n"],
+                   "csr_entries": int(hg.num_edges),
                    "fanouts": list(cfg["fanouts"]), "batch": cfg["b"]},
         "feature_gbs": round(r["feature_bytes"] / r["seconds"] / 1e9, 3),
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "port",
@@ -545,6 +561,8 @@ def main():
     ap.add_argument("--impl", choices=["bgl", "reference"], default="bgl")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--features", choices=["host", "hbm"], default="host")
+    ap.add_argument("--graph", choices=["exact", "continuum"], default=None,
+                    help="exact: the reference generator's own graph (default for c1/c2); continuum: GPU model (c3)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="use the multi-GPU sharded engine even at N=1")
     ap.add_argument("--exchange", choices=["push", "nccl"], default="push",
@@ -553,6 +571,8 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
     cfg = CONFIGS[args.config]
+    if args.graph is None:
+        args.graph = "continuum" if args.config == "c3" else "exact"
     if args.impl == "reference":
         run_reference(args, cfg)
     elif dist_env()[2] > 1 or args.sharded:

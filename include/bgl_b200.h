@@ -229,6 +229,20 @@ int bgl_gather_list(const int32_t* pos, const int64_t* count_dev, int64_t max_n,
 int bgl_synthetic_features(int64_t first_node, int64_t num_nodes, int32_t dim, uint64_t seed,
                            float* out, void* stream);
 
+/* ---------------------------------------------------------------- graph generator
+ * Bit-exact native gnnio.graph.generate_power_law (graph.py:218-297), host
+ * code: pcg_state = (state_hi, state_lo, inc_hi, inc_lo, has_uint32,
+ * uinteger) of np.random.default_rng(seed).bit_generator.state, m =
+ * max(1, round(avg_degree / 2)), num_train = floor(train_fraction * n).
+ * edges_out: int32 [max_edges][2] host buffer (>= bgl_power_law_edge_bound)
+ * receives the edges in generation order (self-loops and duplicates
+ * included, as the reference's list); train_mask_out: uint8 [n]. The CSR is
+ * csr_from_edges of the list (graph.py:88-107). */
+int64_t bgl_power_law_edge_bound(int64_t n, int64_t m, int32_t num_labels);
+int bgl_power_law_generate(int64_t n, int64_t m, int32_t num_labels, double cross_fraction, int64_t num_train,
+                           const uint64_t* pcg_state, int32_t* edges_out, int64_t max_edges,
+                           int64_t* num_edges_out, uint8_t* train_mask_out);
+
 /* ---------------------------------------------------------------- ordering
  * Level-synchronous BFS of gnnio.ordering.generate_bfs_sequences
  * (ordering.py:57-116) and the closed-form round-robin of form_batches over

@@ -17,7 +17,8 @@ from .cachesim import (  # noqa: F401
     simulate,
     warm_static,
 )
-from .graph import DeviceGraph, Graph, generate_power_law_device  # noqa: F401
+from .graph import (DeviceGraph, Graph, generate_power_law, generate_power_law_device,  # noqa: F401
+                    generate_power_law_exact_device, power_law_edges)
 from .ordering import (  # noqa: F401
     BatchSchedule,
     ShufflingErrorReport,

@@ -1,5 +1,6 @@
 """CSR graph container (mirror of gnnio.graph.Graph, graph.py:20-75), its
-device-resident copy, and a GPU synthetic generator for the large configs.
+device-resident copy, the reference's power-law generator (bit-exact, native,
+graph.py:218-297) and a GPU continuum-limit generator for the large configs.
 
 The hot-path kernels consume `DeviceGraph`: int64 row offsets and int32
 column indices in HBM (papers100M shape: 0.9 GB + 12.9 GB, resident in the
@@ -114,9 +115,92 @@ def device_graph(g) -> DeviceGraph:
 
 # ----------------------------------------------------------------------------- generator
 
+def _check_generator_args(n, avg_degree, train_fraction, num_labels):
+    # graph.py:239-248 (same messages)
+    if n < 2:
+        raise ValueError("n must be >= 2")
+    if avg_degree < 1:
+        raise ValueError("avg_degree must be >= 1")
+    if avg_degree >= n:
+        raise ValueError("avg_degree must be < n")
+    if not 0 < train_fraction <= 1:
+        raise ValueError("train_fraction must be in (0, 1]")
+    if num_labels < 1 or num_labels > n:
+        raise ValueError("num_labels must be in [1, n]")
+
+
+def power_law_edges(n: int, avg_degree: int, seed: int, train_fraction: float = 0.1, num_labels: int = 1,
+                    cross_fraction: float = 0.05):
+    """The reference generator's raw output, bit-exact: (edges int32 [E, 2] in
+    generation order, train_mask bool [n], labels int64 [n]). The sequential
+    preferential-attachment process runs natively (bgl_power_law_generate);
+    numpy supplies only the SeedSequence hash of `seed` (graph.py:250)."""
+    from . import _lib
+    _check_generator_args(n, avg_degree, train_fraction, num_labels)
+    lib = _lib.load(require_cuda=False)
+    m = max(1, int(round(avg_degree / 2)))                  # graph.py:251
+    st = np.random.default_rng(seed).bit_generator.state    # graph.py:250
+    s, inc = st["state"]["state"], st["state"]["inc"]
+    mask = (1 << 64) - 1
+    ps = np.array([s >> 64, s & mask, inc >> 64, inc & mask, st["has_uint32"], st["uinteger"]], dtype=np.uint64)
+    bound = int(lib.bgl_power_law_edge_bound(n, m, num_labels))
+    edges = np.empty((bound, 2), dtype=np.int32)
+    ne = _lib.c_i64()
+    train = np.empty(n, dtype=np.uint8)
+    _lib.check(lib.bgl_power_law_generate(n, m, num_labels, float(cross_fraction), int(math.floor(train_fraction * n)),
+                                          ps.ctypes.data, edges.ctypes.data, bound, _lib.ctypes.byref(ne),
+                                          train.ctypes.data))
+    bounds = [i * n // num_labels for i in range(num_labels + 1)]
+    labels = np.repeat(np.arange(num_labels, dtype=np.int64), np.diff(bounds))
+    return edges[: ne.value], train.astype(bool), labels
+
+
+def csr_from_edges_device(edges: np.ndarray, n: int, dev=None) -> tuple[torch.Tensor, torch.Tensor]:
+    """Sorted, deduplicated, symmetric CSR without self-loops on the device
+    (csr_from_edges, graph.py:88-107): (indptr int64 [n+1], indices int32)."""
+    dev = torch.device("cuda", torch.cuda.current_device()) if dev is None else torch.device(dev)
+    e = torch.from_numpy(np.ascontiguousarray(edges)).to(dev)
+    src, dst = e[:, 0].to(torch.int64), e[:, 1].to(torch.int64)
+    del e
+    keep = src != dst
+    src, dst = src[keep], dst[keep]
+    key = torch.unique(torch.cat([src * n + dst, dst * n + src]))
+    del src, dst, keep
+    row = key // n
+    col = (key - row * n).to(torch.int32)
+    del key
+    indptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    indptr[1:] = torch.cumsum(torch.bincount(row, minlength=n), 0)
+    return indptr, col
+
+
+def generate_power_law_exact_device(n: int, avg_degree: int, seed: int, train_fraction: float = 0.1,
+                                    num_labels: int = 1, cross_fraction: float = 0.05, device=None) -> DeviceGraph:
+    """gnnio.graph.generate_power_law(...) (graph.py:218-297), bit-identical,
+    built straight into HBM: native edge process + device CSR."""
+    edges, train, labels = power_law_edges(n, avg_degree, seed, train_fraction, num_labels, cross_fraction)
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    indptr, col = csr_from_edges_device(edges, n, dev)
+    del edges
+    return DeviceGraph(indptr, col, n, train_mask=torch.from_numpy(train).to(dev),
+                       labels=torch.from_numpy(labels).to(dev))
+
+
+def generate_power_law(n: int, avg_degree: int, seed: int, train_fraction: float = 0.1, num_labels: int = 1,
+                       cross_fraction: float = 0.05) -> Graph:
+    """Drop-in for gnnio.graph.generate_power_law (graph.py:218-297): the same
+    host `Graph`, bit-identical (tests/golden/graphgen.npz), from the native
+    generator with the CSR built on the device."""
+    dg = generate_power_law_exact_device(n, avg_degree, seed, train_fraction, num_labels, cross_fraction)
+    return dg.to_host()
+
+
 def generate_power_law_device(n: int, avg_degree: int, seed: int, train_fraction: float = 0.1,
                               num_labels: int = 1, cross_fraction: float = 0.05,
                               device=None) -> DeviceGraph:
+    """Same graph MODEL as generate_power_law, generated entirely on the GPU in
+    its continuum limit (power_law_csr) -- NOT bit-exact; for shapes where the
+    sequential exact process is too long (papers100M: 1.55B edges)."""
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     indptr, col, train_mask, comm = power_law_csr(n, avg_degree, seed, train_fraction, num_labels,
                                                   cross_fraction, dev)

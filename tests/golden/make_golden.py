@@ -341,12 +341,36 @@ def make_shuffle(gs):
     np.savez_compressed(os.path.join(HERE, "shuffle.npz"), **out)
 
 
+GRAPHGEN_SPECS = [  # (n, avg_degree, seed, train_fraction, num_labels, cross_fraction)
+    (300, 6, 1, 0.1, 1, 0.05),
+    (2000, 10, 2, 0.2, 3, 0.05),
+    (12000, 9, 4, 0.05, 5, 0.05),      # choice(): tail shuffle branch (n > 10000, size > n // 50)
+    (3000, 51, 5, 0.08, 4, 0.05),      # m = 26 (products' edges per node): set resizes 8 -> 32 -> 128
+    (5000, 7, 9, 1.0, 2, 0.0),         # every node trains, no cross edges
+    (15000, 4, 3, 0.3, 16, 0.2),
+]
+
+
+def make_graphgen():
+    """gnnio.graph.generate_power_law outputs (graph.py:218-297) for the
+    native generator (bgl_power_law_generate)."""
+    out = {"specs": np.array([[n, d, s, nl] for n, d, s, _, nl, _ in GRAPHGEN_SPECS], dtype=np.int64),
+           "fracs": np.array([[tf, cf] for _, _, _, tf, _, cf in GRAPHGEN_SPECS], dtype=np.float64)}
+    for i, (n, d, seed, tf, nl, cf) in enumerate(GRAPHGEN_SPECS):
+        g = generate_power_law(n, d, seed, train_fraction=tf, num_labels=nl, cross_fraction=cf)
+        out[f"off_{i}"] = g.row_offsets.astype(np.int64)
+        out[f"col_{i}"] = g.col_indices.astype(np.int32)
+        out[f"train_{i}"] = np.packbits(g.train_mask)
+        out[f"labels_{i}"] = g.labels.astype(np.int16)
+    np.savez_compressed(os.path.join(HERE, "graphgen.npz"), **out)
+
+
 if __name__ == "__main__":
+    parts = sys.argv[1:] or ["sampler", "cache", "ordering", "static", "shuffle", "graphgen"]
     gs = graphs()
-    make_sampler(gs)
-    make_cache()
-    make_ordering(gs)
-    make_static(gs)
-    make_shuffle(gs)
-    for f in ("sampler.npz", "cache.npz", "ordering.npz", "static.npz", "shuffle.npz"):
+    makers = {"sampler": lambda: make_sampler(gs), "cache": make_cache, "ordering": lambda: make_ordering(gs),
+              "static": lambda: make_static(gs), "shuffle": lambda: make_shuffle(gs), "graphgen": make_graphgen}
+    for part in parts:
+        makers[part]()
+        f = part + ".npz"
         print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -89,3 +89,31 @@ def test_trace_and_schedule_roundtrip(tmp_path):
     back = load_schedule(tmp_path / "s.txt")
     assert back.policy == "proximity-S2" and back.batch_size == 2
     assert [b.tolist() for b in back.batches] == [[3, 1], [2]]
+
+
+def test_native_power_law_generator_is_bit_exact(golden):
+    """bgl_power_law_generate (host code behind the C ABI, no GPU) emits the
+    reference generator's edge list: its CSR, train mask and labels equal
+    gnnio.graph.generate_power_law's on every golden case (graph.py:218-297)."""
+    from oracle import graph_oracle as go
+    from paper_2112_08541_b200.graph import power_law_edges
+    npz = golden("graphgen")
+    for i, ((n, d, seed, nl), (tf, cf)) in enumerate(zip(npz["specs"], npz["fracs"])):
+        n, d, seed, nl = int(n), int(d), int(seed), int(nl)
+        edges, train, labels = power_law_edges(n, d, seed, float(tf), nl, float(cf))
+        off, col = go.csr_from_edges(edges.astype(np.int64), n)
+        assert np.array_equal(off, npz[f"off_{i}"]) and np.array_equal(col, npz[f"col_{i}"]), (n, d, seed)
+        assert np.array_equal(train, np.unpackbits(npz[f"train_{i}"])[:n].astype(bool))
+        assert np.array_equal(labels, npz[f"labels_{i}"].astype(np.int64))
+
+
+def test_power_law_generator_argument_errors():
+    from paper_2112_08541_b200.graph import power_law_edges
+    for args, msg in [((1, 1, 0), "n must be"), ((10, 0, 0), "avg_degree must be >= 1"),
+                      ((10, 10, 0), "avg_degree must be < n")]:
+        with pytest.raises(ValueError, match=msg):
+            power_law_edges(*args)
+    with pytest.raises(ValueError, match="train_fraction"):
+        power_law_edges(10, 2, 0, train_fraction=0.0)
+    with pytest.raises(ValueError, match="num_labels"):
+        power_law_edges(10, 2, 0, num_labels=11)

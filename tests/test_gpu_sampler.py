@@ -175,3 +175,13 @@ def test_hubs_zero_degree_and_duplicates_match_oracle(bgl, fanouts):
         for a, b in zip(fr, fr_o):
             assert np.array_equal(a, b)
         assert np.array_equal(d, d_o)
+
+
+def test_exact_generator_device_csr_matches_reference(golden, bgl):
+    """generate_power_law (native edges + device CSR) == gnnio's graphs."""
+    npz = golden("graphgen")
+    for i, ((n, d, seed, nl), (tf, cf)) in enumerate(zip(npz["specs"], npz["fracs"])):
+        g = bgl.generate_power_law(int(n), int(d), int(seed), float(tf), int(nl), float(cf))
+        assert np.array_equal(g.row_offsets, npz[f"off_{i}"]) and np.array_equal(g.col_indices, npz[f"col_{i}"])
+        assert np.array_equal(g.train_mask, np.unpackbits(npz[f"train_{i}"])[:int(n)].astype(bool))
+        assert np.array_equal(g.labels, npz[f"labels_{i}"].astype(np.int64))

@@ -209,3 +209,25 @@ def test_static_oracle_matches_reference(golden):
         c, cd = co.static_run(batches, dev, host, d)
         assert np.array_equal(c, cnt)
         assert all(np.array_equal(a, b) for a, b in zip(cd, codes))
+
+
+def _graphgen_cases(npz):
+    for i, ((n, d, seed, nl), (tf, cf)) in enumerate(zip(npz["specs"], npz["fracs"])):
+        train = np.unpackbits(npz[f"train_{i}"])[:n].astype(bool)
+        yield (int(n), int(d), int(seed), float(tf), int(nl), float(cf)), npz[f"off_{i}"], npz[f"col_{i}"], train, \
+            npz[f"labels_{i}"].astype(np.int64)
+
+
+def test_graph_generator_restatement_matches_reference(golden):
+    """oracle/graph_oracle.py (numpy PCG64/Lemire/choice + CPython set order)
+    reproduces gnnio.graph.generate_power_law exactly (graph.py:218-297)."""
+    from oracle import graph_oracle as go
+    npz = golden("graphgen")
+    for (n, d, seed, tf, nl, cf), off, col, train, labels in _graphgen_cases(npz):
+        if n > 5000:
+            continue                      # the pure-Python restatement is slow; native covers all cases
+        e, lab, tr = go.power_law_edges(n, d, seed, tf, nl, cf)
+        o, c = go.csr_from_edges(e, n)
+        assert np.array_equal(o, off) and np.array_equal(c, col), (n, d, seed)
+        assert np.array_equal(lab, labels)
+        assert np.array_equal(tr, np.flatnonzero(train))
