@@ -42,7 +42,8 @@ from .graph import DeviceGraph
 from .sampler import BatchSampler, pcg_states, pcg_tables
 
 NS, NB = 4, 3          # sampler buffers, row/plan buffers
-PHASES = 12            # lcm(NS, NB)
+NF = 2                 # host-fed seed buffers
+PHASES = 12            # lcm(NS, NB, NF)
 
 
 class MiniBatchPipeline:
@@ -74,8 +75,14 @@ class MiniBatchPipeline:
         self.batch_counter = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.batch_index = torch.zeros(NS, dtype=torch.int64, device="cuda")
         self.counters = torch.zeros(8, dtype=torch.int64, device="cuda")
-        self.fed_seeds = torch.empty(self.b, dtype=torch.int32, device="cuda")
-        self.fed_count = torch.zeros(1, dtype=torch.int64, device="cuda")
+        # host-fed seeds: NF device buffers [count (int64) | seeds (int32)], each
+        # filled by ONE H2D copy from a pinned staging buffer on a side stream,
+        # so the copy for batch i overlaps the step in flight (feed())
+        self.fed_dev = [torch.zeros(2 + self.b, dtype=torch.int32, device="cuda") for _ in range(NF)]
+        self.fed_host = [torch.zeros(2 + self.b, dtype=torch.int32, pin_memory=True) for _ in range(NF)]
+        self.copy_stream = torch.cuda.Stream()
+        self.fed_ready = [torch.cuda.Event() for _ in range(NF)]   # H2D copy of the buffer done
+        self.fed_free = [torch.cuda.Event() for _ in range(NF)]    # its batch has been staged
         # host-fed results: distinct IDs + {n, counters} of each batch stored
         # into pinned host memory by zero-copy writes (no host sync per step)
         self.host_ids = [torch.empty(self.max_uniq, dtype=torch.int32, pin_memory=True) for _ in range(NB)]
@@ -95,11 +102,12 @@ class MiniBatchPipeline:
     def _sample(self, batch: int, stream=None, fed: bool = False, hooks=None) -> None:
         slot = batch % NS
         s = self.samplers[slot]
-        order = self.fed_seeds if fed else self.order
-        _lib.call("bgl_stage_batch", order.data_ptr(), self.order.numel(), self.b, self.num_batches,
+        fbuf = self.fed_dev[batch % NF].data_ptr()
+        order = fbuf + 8 if fed else self.order.data_ptr()
+        _lib.call("bgl_stage_batch", order, self.order.numel(), self.b, self.num_batches,
                   self.tables.data_ptr(), self.batch_counter.data_ptr(), s.nodes.data_ptr(), s.counts.data_ptr(),
                   self.table_stage[slot].data_ptr(), self.batch_index.data_ptr() + 8 * slot,
-                  self.fed_count.data_ptr() if fed else None, _lib.stream_ptr(stream))
+                  fbuf if fed else None, _lib.stream_ptr(stream))
         s.run(self.table_stage[slot], stream=stream, hooks=hooks)
 
     def _li(self, batch: int, stream=None) -> None:
@@ -130,15 +138,48 @@ class MiniBatchPipeline:
                       self.counters.data_ptr(), self._host_ids_dev[j], self._host_meta_dev[j],
                       _lib.stream_ptr(stream))
 
+    def feed(self, batch: int, seeds) -> int:
+        """Host-fed mode: queue batch `batch`'s seeds (host int sequence or
+        tensor). They are staged in pinned memory and copied H2D (count +
+        seeds, one copy) on a side stream, overlapping the step in flight; the
+        step that samples `batch` waits for the copy. Returns the H2D bytes."""
+        j = batch % NF
+        seeds = torch.as_tensor(seeds)
+        n = int(seeds.numel())
+        if n == 0:
+            raise ValueError("seeds must be nonempty")
+        if n > self.b:
+            raise ValueError("batch larger than the pipeline was sized for")
+        self.fed_ready[j].synchronize()          # staging j's previous copy has finished
+        h = self.fed_host[j]
+        h[:2].view(torch.int64).fill_(n)
+        h[2:2 + n].copy_(seeds.to(torch.int32))
+        with torch.cuda.stream(self.copy_stream):
+            self.copy_stream.wait_event(self.fed_free[j])   # its previous batch was staged
+            self.fed_dev[j][:2 + n].copy_(h[:2 + n], non_blocking=True)
+            self.fed_ready[j].record(self.copy_stream)
+        return (2 + n) * 4
+
+    def _fed_sample_guard(self, batch: int, before: bool) -> None:
+        j = batch % NF
+        if before:
+            torch.cuda.current_stream().wait_event(self.fed_ready[j])
+        else:
+            self.fed_free[j].record(torch.cuda.current_stream())
+
     def prime(self, fed: bool = False, feed=None) -> None:
         """Prologue (untimed): sample k..k+2, LI(k), miss(k), LI(k+1).
-        In host-fed mode `feed(i)` must load batch i's seeds."""
+        In host-fed mode `feed(i)` must queue batch i's seeds (self.feed)."""
         if self.primed:
             return
         for i in range(self.k, self.k + self.lookahead):
             if fed and feed is not None:
                 feed(i)
+            if fed:
+                self._fed_sample_guard(i, True)
             self._sample(i, fed=fed)
+            if fed:
+                self._fed_sample_guard(i, False)
         self._li(self.k)
         self._miss(self.k)
         self._li(self.k + 1)
@@ -163,7 +204,11 @@ class MiniBatchPipeline:
 
     def step_eager(self, fed: bool = False) -> None:
         self.prime(fed)
+        if fed:
+            self._fed_sample_guard(self.k + 3, True)
         self._overlapped(self.k, fed)
+        if fed:
+            self._fed_sample_guard(self.k + 3, False)
         self.k += 1
 
     def step_serial(self, events) -> None:
@@ -206,7 +251,11 @@ class MiniBatchPipeline:
         if g is None or not self.primed:
             self.step_eager(fed)
             return
+        if fed:
+            self._fed_sample_guard(self.k + 3, True)
         g.replay()
+        if fed:
+            self._fed_sample_guard(self.k + 3, False)
         self.k += 1
 
     # -- results of the last completed batch (k - 1) -----------------------------

@@ -57,9 +57,7 @@ def test_pipeline_matches_oracle(use_graph, where):
     pipe.reset()
 
     def feed(i):
-        sb = torch.from_numpy(ref_batches[i].astype(np.int32))
-        pipe.fed_seeds[: len(sb)].copy_(sb)
-        pipe.fed_count.fill_(len(sb))
+        pipe.feed(i, ref_batches[i])
 
     pipe.prime(fed=True, feed=feed)
     for i in range(4):
