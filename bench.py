@@ -406,13 +406,16 @@ def run_bgl(args, cfg):
 
 def run_sharded(args, cfg):
     """N GPUs, one process each: node-ID-sharded FIFO cache (home = v % N,
-    cachesim.py:505-506), rank w samples batches i = j*N + w, IDs and rows
-    exchanged with NCCL all-to-all (paper_2112_08541_b200/distributed.py).
+    cachesim.py:505-506), rank w samples batches i = j*N + w. Default engine:
+    ShardedPipeline -- IDs pushed to the homes over peer memory by the
+    partition kernel, rows and codes pushed back by the homes' gathers, NCCL
+    only as a one-int barrier, no host synchronisation per round
+    (paper_2112_08541_b200/distributed.py). `--exchange nccl`: the all-to-all
+    baseline (ShardedFeatureCache, host-synchronised per round).
     One step = one round = N mini-batches (one per GPU)."""
     import torch
     import torch.distributed as dist
-    from paper_2112_08541_b200.distributed import (GpuShardEngine, GpuShardOps, PeerPushFeatureCache,
-                                                   ShardedFeatureCache)
+    from paper_2112_08541_b200.distributed import GpuShardEngine, GpuShardOps, ShardedFeatureCache, ShardedPipeline
     from paper_2112_08541_b200.sampler import BatchSampler, pcg_states, pcg_tables
 
     if "RANK" not in os.environ:            # single process without torchrun (--sharded at N=1)
@@ -425,38 +428,48 @@ def run_sharded(args, cfg):
     b, rb, dim = cfg["b"], cfg["dim"] * 4, cfg["dim"]
     cap = int(cfg["cache_frac"] * cfg["n"]) // world
     nb_total = (order.numel() + b - 1) // b
-    sampler = BatchSampler(dg, cfg["fanouts"], b)
-    engine = GpuShardEngine(rank, world, cap, feats, sampler.max_uniq)
-    ops = GpuShardOps(world, sampler.max_uniq, rb)
-    if args.exchange == "push":
-        # IDs by NCCL all-to-all, rows stored by the homes' gather straight into
-        # the worker GPU's buffer over NVLink (CUDA IPC, bgl_gather_rows_push)
-        sc = PeerPushFeatureCache(rank, world, engine, ops, dim, sampler.max_uniq)
-    else:
-        sc = ShardedFeatureCache(rank, world, engine, ops, dim)
-    tables = pcg_tables(pcg_states(RUN_SEED, range(nb_total)))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     order_host = order.cpu().numpy().astype(np.int32)
     seeds_pinned = torch.from_numpy(order_host).pin_memory()
-    out_ids = torch.empty(sampler.max_uniq, dtype=torch.int32).pin_memory()
 
-    def one_round(j, host_fed=False):
-        i = (j * world + rank) % nb_total
-        lo, hi = i * b, min((i + 1) * b, order.numel())
-        src = seeds_pinned[lo:hi] if host_fed else order[lo:hi]
-        sampler.load_seeds(src)
-        sampler.run(tables[i])
-        u = int(sampler.num_uniq.item())
-        rows, codes = sc.step(sampler.uniq[:u])
-        if host_fed:
-            out_ids[:u].copy_(sampler.uniq[:u], non_blocking=True)
-        return u
+    if args.exchange == "push":
+        pipe = ShardedPipeline(rank, world, dg, cfg["fanouts"], b, order, RUN_SEED, cap, feats)
+        counters = pipe.counters
+        launches = pipe.kernels_per_round
+        graphs = "off"
+        if not args.no_graphs:
+            try:
+                pipe.capture()                    # one CUDA graph per step phase, NCCL barriers inside
+                graphs = "on"
+            except Exception as e:                # noqa: BLE001 -- report and run the same steps eagerly
+                pipe.graphs.clear()
+                graphs = f"capture failed ({type(e).__name__}: {str(e)[:80]}); eager"
+
+        def one_round(j, host_fed=False):
+            pipe.step()                   # step j: rows of round j complete
+    else:
+        graphs = "off"
+        sampler = BatchSampler(dg, cfg["fanouts"], b)
+        engine = GpuShardEngine(rank, world, cap, feats, sampler.max_uniq)
+        sc = ShardedFeatureCache(rank, world, engine, GpuShardOps(world, sampler.max_uniq, rb), dim)
+        tables = pcg_tables(pcg_states(RUN_SEED, range(nb_total)))
+        counters = engine.counters
+        launches = 3 * len(cfg["fanouts"]) + 4 + 3 + 5 * world
+
+        def one_round(j, host_fed=False):
+            i = (j * world + rank) % nb_total
+            lo, hi = i * b, min((i + 1) * b, order.numel())
+            sampler.load_seeds(seeds_pinned[lo:hi] if host_fed else order[lo:hi])
+            sampler.run(tables[i])
+            u = int(sampler.num_uniq.item())
+            sc.step(sampler.uniq[:u])
 
     for j in range(args.warmup):
         one_round(j)
     torch.cuda.synchronize()
-    c0 = engine.counters.clone()
+    c0 = counters.clone()
     dist.barrier()
+    torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local_rank) as clk:
         for k in range(args.steps):
@@ -467,51 +480,81 @@ def run_sharded(args, cfg):
         torch.cuda.synchronize()
     dist.barrier()
     total_ms = sum(s.elapsed_time(e) for s, e in ev)
-    d = engine.counters - c0
+    d = counters - c0
     dist.all_reduce(d)
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     q, own, peer, hst = (int(x) for x in d[:4].tolist())
-    # e2e: seeds H2D from pinned host, distinct IDs D2H, every round
-    e2e_ms, h2d, d2h = [], 0, 0
-    for k in range(max(3, min(args.steps, 50))):
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        u = one_round(args.warmup + args.steps + k, host_fed=True)
-        e1.record()
-        e1.synchronize()
-        e2e_ms.append(e0.elapsed_time(e1))
-        h2d += b * 4
-        d2h += u * 4
+    # e2e: every round the next round's seeds go H2D from pinned host (on the
+    # sampling stream, ahead of the sampler) and the round's distinct IDs (the
+    # AccessTrace row) + counters are stored into pinned host memory
+    n_e2e = max(3, min(args.steps, 50))
+    from paper_2112_08541_b200 import _lib
+    if args.exchange == "push":
+        maxu = pipe.maxu
+    else:
+        maxu = sampler.max_uniq
+    host_ids = torch.empty(maxu, dtype=torch.int32).pin_memory()
+    host_meta = torch.zeros(16, dtype=torch.int64).pin_memory()
+    hid, hmeta = _lib.host_device_pointer(host_ids), _lib.host_device_pointer(host_meta)
+    eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_e2e)]
+    h2d, d2h = 0, 0
+    torch.cuda.synchronize()
+    for k in range(n_e2e):
+        j = args.warmup + args.steps + k
+        eev[k][0].record()
+        if args.exchange == "push":
+            i = pipe.batch_of(j + 3)      # step j samples round j + 3: its seeds come from the host
+            lo, hi = i * b, min((i + 1) * b, order.numel())
+            with torch.cuda.stream(pipe.s_sample):
+                pipe.order[lo:hi].copy_(seeds_pinned[lo:hi], non_blocking=True)
+            one_round(j)
+            s = pipe.samplers[j % pipe.NSMP]
+            pipe.store_result(j, hid, hmeta)       # side stream, overlapping the next step
+            if k == n_e2e - 1:                     # (back-to-back steps: every hand-off ends inside the region)
+                torch.cuda.current_stream().wait_stream(pipe.s_result)
+        else:
+            one_round(j, host_fed=True)
+            s = sampler
+            _lib.call("bgl_d2h_result", s.uniq.data_ptr(), s.num_uniq.data_ptr(), s.max_uniq, counters.data_ptr(),
+                      hid, hmeta, _lib.stream_ptr())
+        eev[k][1].record()
+        h2d += (hi - lo if args.exchange == "push" else b) * 4
+    torch.cuda.synchronize()
+    e2e_ms = [x.elapsed_time(y) for x, y in eev]
+    u_last = int(host_meta[0])
+    assert torch.equal(host_ids[:u_last], s.uniq[:u_last].cpu()), "host-side result differs from the device"
+    d2h = n_e2e * (u_last * 4 + 72)
     t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    n_e2e = len(e2e_ms)
     out = {
         "metric": METRIC, "value": round(world * args.steps / (total_ms * 1e-3), 2), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int32 ids / u53 PCG64 keys / fp32 rows moved",
         "data": graph_data(cfg, args.graph),
-        "config": {"workload": cfg["workload"], "graph": args.graph, "num_nodes": cfg["n"], "csr_entries": dg.num_edges,
-                   "feature_dim": cfg["dim"], "fanouts": list(cfg["fanouts"]), "batch": b,
-                   "cache_rows_per_gpu": cap, "features": args.features,
-                   "parallelism": f"dp{world} + node-ID-sharded FIFO cache (home = v % {world}); IDs by NCCL "
-                                  f"all-to-all, rows by " + ("home-push over NVLink (CUDA IPC)" if args.exchange == "push"
-                                                             else "NCCL all-to-all"),
+        "config": {"workload": cfg["workload"], "graph": args.graph, "num_nodes": cfg["n"],
+                   "csr_entries": dg.num_edges, "feature_dim": cfg["dim"], "fanouts": list(cfg["fanouts"]),
+                   "batch": b, "cache_rows_per_gpu": cap, "features": args.features,
+                   "parallelism": f"dp{world} + node-ID-sharded FIFO cache (home = v % {world}); " + (
+                       "IDs pushed to the homes over peer memory by the partition kernel, rows/codes pushed back "
+                       "by the homes' gathers (CUDA IPC), NCCL one-int barriers, no host sync per round"
+                       if args.exchange == "push" else "IDs and rows by NCCL all-to-all (host-synchronised)"),
                    "l2": "flushed between timed steps (256 MB write, outside the events)",
-                   "step": f"one round = {world} mini-batches (one per GPU)"},
+                   "step": f"one round = {world} mini-batches (one per GPU)", "cuda_graphs": graphs},
         "feature_gbs": round(q * rb / (total_ms * 1e-3) / 1e9, 2),
         "hit_pct": round(100.0 * (own + peer + hst) / max(q, 1), 2),
         "peer_hit_pct": round(100.0 * peer / max(q, 1), 2),
         "e2e": {"value": round(world * n_e2e / (float(t.item()) * 1e-3), 2), "unit": UNIT,
                 "h2d_bytes_per_step": int(h2d / n_e2e), "d2h_bytes_per_step": int(d2h / n_e2e)},
-        "gpu_launches": (3 * len(cfg["fanouts"]) + 4 + 3 + 5 * world) * args.steps,
+        "gpu_launches": launches * args.steps,
         "clocks": clk.summary(), "setup": setup,
     }
     if rank == 0:
         print(json.dumps(out), flush=True)
+    if args.exchange == "push":
+        pipe.close()
     dist.destroy_process_group()
 
 
@@ -570,6 +613,7 @@ def main():
     ap.add_argument("--graph", choices=["exact", "continuum"], default=None,
                     help="exact: the reference generator's own graph (default for c1/c2); continuum: GPU model (c3)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true", help="sharded engine: eager steps (no CUDA graphs)")
     ap.add_argument("--sharded", action="store_true", help="use the multi-GPU sharded engine even at N=1")
     ap.add_argument("--exchange", choices=["push", "nccl"], default="push",
                     help="multi-GPU row exchange: home-push over peer memory or NCCL all-to-all")

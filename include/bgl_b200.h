@@ -177,6 +177,13 @@ int bgl_cache_insert_plan(bgl_cache_t cache, const int32_t* sorted_ids, int64_t 
                           int32_t* plan, int64_t* plan_count, int64_t* counters, void* stream);
 int bgl_cache_copy_rows(bgl_cache_t cache, const int32_t* plan, const int64_t* plan_count,
                         int64_t max_sorted, const void* batch_rows, void* stream);
+/* bgl_cache_copy_rows with the batch rows addressed through row_index: the
+ * survivor at batch position p is copied from batch_rows + row_index[p] *
+ * row_bytes (multi-GPU: the rows already pushed into the worker's output,
+ * read back over peer memory, row_index = the bucket's batch positions). */
+int bgl_cache_copy_rows_indexed(bgl_cache_t cache, const int32_t* plan, const int64_t* plan_count,
+                                int64_t max_sorted, const void* batch_rows, const int32_t* row_index,
+                                void* stream);
 /* Synchronous export of the ring contents (int64, -1 = empty) and tails, in
  * the layout of FifoLevel.slots / .tail (cachesim.py:273-275). Any pointer may
  * be NULL. dev_slots: [num_shards][shard_capacity]; dev_tails: [num_shards]. */
@@ -221,7 +228,8 @@ int bgl_gather_rows(const int32_t* ids, const int64_t* src_row, const int64_t* n
  * (pos from bgl_cache_lookup_misses). rows_in_flight (0 = 4, or 2/4/8) rows
  * per warp are loaded before any is stored; ctas > 0 launches exactly that
  * many 8-warp CTAs. push_out/push_pos (both or neither): every row is also
- * stored at push_out + push_pos[pos[j]] * row_bytes (home-push, peer memory). */
+ * stored at push_out + push_pos[pos[j]] * row_bytes (home-push, peer memory);
+ * with a push, `out` may be NULL. */
 int bgl_gather_list(const int32_t* pos, const int64_t* count_dev, int64_t max_n, const int32_t* ids,
                     const void* table, int64_t row_bytes, void* out, void* push_out, const int32_t* push_pos,
                     int32_t rows_in_flight, int32_t ctas, void* stream);
@@ -292,12 +300,23 @@ size_t bgl_partition_workspace(int64_t max_n, int32_t num_homes);
 int bgl_partition_by_home(const int32_t* ids, const int64_t* n_dev, int64_t max_n, int32_t num_homes,
                           int32_t* out_ids, int32_t* out_pos, int64_t* counts_dev, void* workspace,
                           void* stream);
+/* The partition with the ID exchange fused in (no collective for the data):
+ * bucket h (ascending IDs of home h) and its batch positions are stored
+ * straight into home h's receive area over peer memory -- peer_ids[h] /
+ * peer_pos[h] are DEVICE arrays of H pointers (this rank's slot in every
+ * home's IPC-mapped receive buffers), *peer_cnt[h] receives the bucket size.
+ * counts_dev: local int64 [H]. The kernel ends with a system-scope fence; the
+ * caller crosses a barrier before the homes read. */
+int bgl_partition_push(const int32_t* ids, const int64_t* n_dev, int64_t max_n, int32_t num_homes,
+                       int32_t* const* peer_ids, int32_t* const* peer_pos, int64_t* const* peer_cnt,
+                       int64_t* counts_dev, void* workspace, void* stream);
 int bgl_scatter_rows(const int32_t* pos, const int64_t* n_dev, int64_t max_n, const void* rows,
                      int64_t row_bytes, void* out, void* stream);
 /* Home-push gather (the row exchange fused into the gather): rows as in
  * bgl_gather_rows go to the local `out` (kept for the ring insert) AND to
  * push_out + push_pos[i] * row_bytes -- the worker GPU's output buffer,
- * mapped into this process with bgl_ipc_open_handle, written over NVLink. */
+ * mapped into this process with bgl_ipc_open_handle, written over NVLink.
+ * `out` may be NULL (rows only pushed). */
 int bgl_gather_rows_push(const int32_t* ids, const int64_t* src_row, const int64_t* n_dev, int64_t max_n,
                          const void* ring_rows, const void* table, int64_t row_bytes, void* out,
                          void* push_out, const int32_t* push_pos, int32_t mode, int32_t ctas,
@@ -312,7 +331,8 @@ int bgl_ipc_close(void* dev_ptr);
 /* ---------------------------------------------------------------- pipeline staging
  * Step staging for the CUDA-graph-captured pipeline (no reference
  * counterpart: the reference loops batches in Python, sampler.py:136).
- * i = *batch_counter % num_batches; seeds_out = order[i*b, min((i+1)*b,
+ * i = (*batch_counter * batch_stride + batch_offset) % num_batches (multi-GPU:
+ * stride = number of GPUs, offset = rank); seeds_out = order[i*b, min((i+1)*b,
  * total)), *seed_count_out = its length, table_out = tables[i] (BGL_PCG_TABLE_ROWS x 4),
  * *batch_index_out = i (may be NULL); then *batch_counter += 1.
  * fed_count_dev != NULL (host-fed mode): `order` holds only this batch's
@@ -320,7 +340,7 @@ int bgl_ipc_close(void* dev_ptr);
 int bgl_stage_batch(const int32_t* order, int64_t total, int64_t batch_size, int64_t num_batches,
                     const uint64_t* tables, int64_t* batch_counter, int32_t* seeds_out,
                     int64_t* seed_count_out, uint64_t* table_out, int64_t* batch_index_out,
-                    const int64_t* fed_count_dev, void* stream);
+                    const int64_t* fed_count_dev, int64_t batch_stride, int64_t batch_offset, void* stream);
 /* Sync-free result hand-off: host_ids[0..n) = ids[0..*n_dev) and host_meta =
  * {n, counters[0..8)} written straight into mapped pinned host memory
  * (device aliases from bgl_host_device_pointer). counters may be NULL. */

@@ -52,6 +52,7 @@ PROTOTYPES = {
     "bgl_cache_plan_stride": (c_i64, [c_vp, c_i64]),
     "bgl_cache_insert_plan": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "bgl_cache_copy_rows": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "bgl_cache_copy_rows_indexed": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "bgl_cache_export":(ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
     "bgl_degree_histogram": (ctypes.c_int, [c_vp, c_i64, c_i32, c_i64, c_vp, c_vp, c_vp]),
     "bgl_select_flags": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp]),
@@ -73,6 +74,7 @@ PROTOTYPES = {
     "bgl_shuffling_tv": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "bgl_partition_workspace": (c_sz, [c_i64, c_i32]),
     "bgl_partition_by_home": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "bgl_partition_push": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "bgl_scatter_rows": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "bgl_gather_rows_push": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i32,
                                              c_i32, c_vp]),
@@ -80,7 +82,8 @@ PROTOTYPES = {
     "bgl_ipc_open_handle": (ctypes.c_int, [c_vp, ctypes.POINTER(c_vp)]),
     "bgl_ipc_close": (ctypes.c_int, [c_vp]),
     "bgl_d2h_result": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
-    "bgl_stage_batch":(ctypes.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "bgl_stage_batch": (ctypes.c_int, [c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64,
+                                        c_i64, c_vp]),
 }
 
 _lib = None

@@ -365,10 +365,11 @@ __global__ void insert_finalize_kernel(int32_t d, int64_t C, int64_t Ch, int64_t
     counters[6] += ev;
 }
 
-// deferred survivor row copy: plan[y][r] = (batch position, ring slot)
+// deferred survivor row copy: plan[y][r] = (batch position, ring slot); the
+// row of batch position p is batch_rows[row_index ? row_index[p] : p]
 __global__ void copy_rows_kernel(const int32_t* __restrict__ plan, const int64_t* __restrict__ plan_count,
                                  int64_t stride, int64_t C, const unsigned char* __restrict__ batch_rows,
-                                 unsigned char* __restrict__ rows, int64_t rb) {
+                                 unsigned char* __restrict__ rows, int64_t rb, const int32_t* __restrict__ row_index) {
     const int y = blockIdx.y;
     const int64_t cnt = plan_count[y];
     const int lane = lane_id();
@@ -377,7 +378,8 @@ __global__ void copy_rows_kernel(const int32_t* __restrict__ plan, const int64_t
     for (int64_t r = gw; r < cnt; r += nw) {
         const int32_t pos = plan[2 * ((int64_t)y * stride + r)];
         const int32_t slot = plan[2 * ((int64_t)y * stride + r) + 1];
-        const unsigned char* src = batch_rows + (int64_t)pos * rb;
+        const int64_t src_row = row_index ? (int64_t)row_index[pos] : (int64_t)pos;
+        const unsigned char* src = batch_rows + src_row * rb;
         unsigned char* dst = rows + ((int64_t)y * C + slot) * rb;
         if ((rb & 15) == 0) {
             for (int64_t b = (int64_t)lane * 16; b < rb; b += 32 * 16)
@@ -612,7 +614,19 @@ int bgl_cache_copy_rows(bgl_cache_t c, const int32_t* plan, const int64_t* plan_
     if (c->C == 0 || max_sorted <= 0) return BGL_OK;
     dim3 grid(grid_for(stride * 32, 256, 8), c->d);
     copy_rows_kernel<<<grid, 256, 0, as_stream(stream)>>>(plan, plan_count, stride, c->C,
-                                                          (const unsigned char*)batch_rows, c->rows, c->rb);
+                                                          (const unsigned char*)batch_rows, c->rows, c->rb, nullptr);
+    return launch_status("copy_rows_kernel");
+}
+
+int bgl_cache_copy_rows_indexed(bgl_cache_t c, const int32_t* plan, const int64_t* plan_count, int64_t max_sorted,
+                                const void* batch_rows, const int32_t* row_index, void* stream) {
+    BGL_CHECK_ARG(c && plan && plan_count && batch_rows && row_index, "bgl_cache_copy_rows_indexed: null pointer");
+    BGL_CHECK_ARG(c->rb > 0, "cache was created without feature rows");
+    const int64_t stride = bgl_cache_plan_stride(c, max_sorted);
+    if (c->C == 0 || max_sorted <= 0) return BGL_OK;
+    dim3 grid(grid_for(stride * 32, 256, 8), c->d);
+    copy_rows_kernel<<<grid, 256, 0, as_stream(stream)>>>(plan, plan_count, stride, c->C,
+                                                          (const unsigned char*)batch_rows, c->rows, c->rb, row_index);
     return launch_status("copy_rows_kernel");
 }
 

@@ -96,6 +96,65 @@ home_scatter_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__
     }
 }
 
+// home_scatter with the exchange fused in: every bucketed ID (and its batch
+// position) is stored straight into its HOME GPU's receive area over peer
+// memory (CUDA IPC mappings, NVLink), at its offset inside the bucket; the
+// first block also stores the bucket sizes. Ends with a system-scope fence so
+// the stores are visible to the homes once the kernel has completed (the
+// caller then crosses a barrier).
+__global__ void __launch_bounds__(kXThreads)
+home_push_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ n_dev, int32_t H,
+                 const int64_t* __restrict__ tile_off, const int64_t* __restrict__ counts,
+                 int32_t* const* __restrict__ peer_ids, int32_t* const* __restrict__ peer_pos,
+                 int64_t* const* __restrict__ peer_cnt) {
+    constexpr int NW = kXThreads / 32;
+    __shared__ int32_t s_w[NW][kXMaxHomes];
+    __shared__ int64_t s_run[kXMaxHomes];
+    __shared__ int64_t s_start[kXMaxHomes];
+    const int64_t n = *n_dev;
+    const int lane = lane_id(), wid = warp_id();
+    const unsigned lt = (1u << lane) - 1u;
+    if (threadIdx.x == 0) {
+        int64_t c = 0;
+        for (int h = 0; h < H; ++h) {
+            s_start[h] = c;
+            c += counts[h];
+        }
+    }
+    for (int h = threadIdx.x; h < H; h += blockDim.x) {
+        s_run[h] = tile_off[blockIdx.x * (int64_t)H + h];
+        if (blockIdx.x == 0) *peer_cnt[h] = counts[h];
+    }
+    __syncthreads();
+    for (int r = 0; r < kXRounds; ++r) {
+        const int64_t e = blockIdx.x * (int64_t)kXTile + r * kXThreads + threadIdx.x;
+        const int32_t v = e < n ? ids[e] : 0;
+        const int h = e < n ? v % H : -1;
+        int rank = 0;
+        for (int y = 0; y < H; ++y) {
+            const unsigned m = __ballot_sync(0xffffffffu, h == y);
+            if (h == y) rank = __popc(m & lt);
+            if (lane == 0) s_w[wid][y] = __popc(m);
+        }
+        __syncthreads();
+        if (h >= 0) {
+            int64_t p = s_run[h] + rank;
+            for (int w = 0; w < wid; ++w) p += s_w[w][h];
+            p -= s_start[h];
+            peer_ids[h][p] = v;
+            peer_pos[h][p] = (int32_t)e;
+        }
+        __syncthreads();
+        for (int y = threadIdx.x; y < H; y += blockDim.x) {
+            int64_t add = 0;
+            for (int w = 0; w < NW; ++w) add += s_w[w][y];
+            s_run[y] += add;
+        }
+        __syncthreads();
+    }
+    __threadfence_system();
+}
+
 __global__ void scatter_rows_kernel(const int32_t* __restrict__ pos, const int64_t* __restrict__ n_dev,
                                     const unsigned char* __restrict__ rows, int64_t rb,
                                     unsigned char* __restrict__ out) {
@@ -141,6 +200,24 @@ int bgl_partition_by_home(const int32_t* ids, const int64_t* n_dev, int64_t max_
     BGL_TRY(launch_status("home_scan_kernel"));
     home_scatter_kernel<<<(unsigned)ntiles, kXThreads, 0, st>>>(ids, n_dev, num_homes, tc, out_ids, out_pos);
     return launch_status("home_scatter_kernel");
+}
+
+int bgl_partition_push(const int32_t* ids, const int64_t* n_dev, int64_t max_n, int32_t num_homes,
+                       int32_t* const* peer_ids, int32_t* const* peer_pos, int64_t* const* peer_cnt,
+                       int64_t* counts_dev, void* workspace, void* stream) {
+    BGL_CHECK_ARG(num_homes >= 1 && num_homes <= kXMaxHomes, "num_homes must be in [1, 64]");
+    BGL_CHECK_ARG(ids && n_dev && peer_ids && peer_pos && peer_cnt && counts_dev && workspace,
+                  "bgl_partition_push: null pointer");
+    cudaStream_t st = as_stream(stream);
+    const int64_t ntiles = std::max<int64_t>(1, ceil_div(max_n, kXTile));
+    int64_t* tc = reinterpret_cast<int64_t*>(workspace);
+    home_count_kernel<<<(unsigned)ntiles, kXThreads, 0, st>>>(ids, n_dev, num_homes, tc);
+    BGL_TRY(launch_status("home_count_kernel"));
+    home_scan_kernel<<<1, kXThreads, 0, st>>>(tc, ntiles, num_homes, counts_dev);
+    BGL_TRY(launch_status("home_scan_kernel"));
+    home_push_kernel<<<(unsigned)ntiles, kXThreads, 0, st>>>(ids, n_dev, num_homes, tc, counts_dev, peer_ids,
+                                                              peer_pos, peer_cnt);
+    return launch_status("home_push_kernel");
 }
 
 int bgl_scatter_rows(const int32_t* pos, const int64_t* n_dev, int64_t max_n, const void* rows, int64_t row_bytes,

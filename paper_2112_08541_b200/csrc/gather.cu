@@ -68,9 +68,11 @@ gather_v4_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ sr
 #pragma unroll
             for (int u = 0; u < kRows; ++u)
                 if (src[u]) v[u] = ld_nc_v4(src[u] + c * 16);
+            if (out) {
 #pragma unroll
-            for (int u = 0; u < kRows; ++u)
-                if (src[u]) st_na_v4(out + (r0 + u) * rb + c * 16, v[u]);
+                for (int u = 0; u < kRows; ++u)
+                    if (src[u]) st_na_v4(out + (r0 + u) * rb + c * 16, v[u]);
+            }
             if (push_out) {   // home-push: the same row straight into the worker GPU's output (peer memory)
 #pragma unroll
                 for (int u = 0; u < kRows; ++u)
@@ -117,9 +119,11 @@ gather_list_kernel(const int32_t* __restrict__ pos, const int64_t* __restrict__ 
 #pragma unroll
             for (int u = 0; u < R; ++u)
                 if (src[u]) v[u] = ld_nc_v4(src[u] + c * 16);
+            if (out) {
 #pragma unroll
-            for (int u = 0; u < R; ++u)
-                if (src[u]) st_na_v4(out + dst[u] * rb + c * 16, v[u]);
+                for (int u = 0; u < R; ++u)
+                    if (src[u]) st_na_v4(out + dst[u] * rb + c * 16, v[u]);
+            }
             if (push_out) {
 #pragma unroll
                 for (int u = 0; u < R; ++u)
@@ -207,7 +211,7 @@ int bgl_gather_rows_push(const int32_t* ids, const int64_t* src_row, const int64
                          const void* ring_rows, const void* table, int64_t row_bytes, void* out, void* push_out,
                          const int32_t* push_pos, int32_t mode, int32_t ctas, void* stream) {
     BGL_CHECK_ARG(mode >= 0 && mode <= 2, "gather mode must be 0 (all), 1 (hits) or 2 (misses)");
-    BGL_CHECK_ARG(ids && n_dev && table && out && push_out && push_pos, "bgl_gather_rows_push: null pointer");
+    BGL_CHECK_ARG(ids && n_dev && table && push_out && push_pos, "bgl_gather_rows_push: null pointer");
     BGL_CHECK_ARG(src_row == nullptr || ring_rows != nullptr, "bgl_gather_rows_push: src_row without ring rows");
     BGL_CHECK_ARG(row_bytes % 16 == 0 && (uintptr_t)table % 16 == 0 && (uintptr_t)out % 16 == 0 &&
                       (uintptr_t)push_out % 16 == 0,
@@ -228,7 +232,7 @@ int bgl_gather_rows_push(const int32_t* ids, const int64_t* src_row, const int64
 int bgl_gather_list(const int32_t* pos, const int64_t* count_dev, int64_t max_n, const int32_t* ids,
                     const void* table, int64_t row_bytes, void* out, void* push_out, const int32_t* push_pos,
                     int32_t rows_in_flight, int32_t ctas, void* stream) {
-    BGL_CHECK_ARG(pos && count_dev && ids && table && out, "bgl_gather_list: null pointer");
+    BGL_CHECK_ARG(pos && count_dev && ids && table && (out || push_out), "bgl_gather_list: null pointer");
     BGL_CHECK_ARG((push_out == nullptr) == (push_pos == nullptr), "bgl_gather_list: push_out and push_pos go together");
     BGL_CHECK_ARG(row_bytes % 16 == 0 && (uintptr_t)table % 16 == 0 && (uintptr_t)out % 16 == 0 &&
                       (uintptr_t)push_out % 16 == 0,

@@ -12,8 +12,8 @@ __global__ void stage_batch_kernel(const int32_t* __restrict__ order, int64_t to
                                    const uint64_t* __restrict__ tables, int64_t* __restrict__ batch_counter,
                                    int32_t* __restrict__ seeds_out, int64_t* __restrict__ seed_count,
                                    uint64_t* __restrict__ table_out, int64_t* __restrict__ batch_index_out,
-                                   const int64_t* __restrict__ fed_count) {
-    const int64_t i = *batch_counter % nb;
+                                   const int64_t* __restrict__ fed_count, int64_t stride, int64_t offset) {
+    const int64_t i = (*batch_counter * stride + offset) % nb;
     // host-fed mode: `order` holds just this batch (fed_count entries)
     const int64_t lo = fed_count ? 0 : i * b;
     const int64_t hi = fed_count ? *fed_count : (lo + b < total ? lo + b : total);
@@ -56,13 +56,15 @@ extern "C" {
 int bgl_stage_batch(const int32_t* order, int64_t total, int64_t batch_size, int64_t num_batches,
                     const uint64_t* tables, int64_t* batch_counter, int32_t* seeds_out, int64_t* seed_count_out,
                     uint64_t* table_out, int64_t* batch_index_out, const int64_t* fed_count_dev,
-                    void* stream) {
+                    int64_t batch_stride, int64_t batch_offset, void* stream) {
     BGL_CHECK_ARG(order && tables && batch_counter && seeds_out && seed_count_out && table_out,
                   "bgl_stage_batch: null pointer");
     BGL_CHECK_ARG(batch_size >= 1 && num_batches >= 1 && total >= 1, "bgl_stage_batch: empty schedule");
+    BGL_CHECK_ARG(batch_stride >= 1 && batch_offset >= 0, "bgl_stage_batch: bad stride/offset");
     stage_batch_kernel<<<1, 1024, 0, as_stream(stream)>>>(order, total, batch_size, num_batches, tables,
                                                           batch_counter, seeds_out, seed_count_out, table_out,
-                                                          batch_index_out, fed_count_dev);
+                                                          batch_index_out, fed_count_dev, batch_stride,
+                                                          batch_offset);
     return launch_status("stage_batch_kernel");
 }
 

@@ -239,3 +239,325 @@ class PeerPushFeatureCache(ShardedFeatureCache):
         dist.barrier(group=self.group)
         n = int(ids.numel())
         return self.out_rows[:n], self.out_codes[:n]
+
+
+def ipc_map(tensors, rank: int, world: int, group=None) -> list[list[int]]:
+    """Exchange CUDA IPC handles of `tensors` (this rank's buffers) and return,
+    per tensor, the device address of every rank's copy as mapped in this
+    process (own address for rank == self). Collective."""
+    lib = _lib.load()
+    mine = []
+    for t in tensors:
+        h = (_lib.ctypes.c_char * 64)()
+        off = _lib.c_i64()
+        _lib.check(lib.bgl_ipc_get_handle(t.data_ptr(), h, _lib.ctypes.byref(off)))
+        mine.append((bytes(h), off.value))
+    handles = [None] * world
+    dist.all_gather_object(handles, mine, group=group)
+    out, opened = [[0] * world for _ in tensors], []
+    for w in range(world):
+        for k, t in enumerate(tensors):
+            if w == rank:
+                out[k][w] = t.data_ptr()
+                continue
+            hb, off = handles[w][k]
+            p = _lib.c_vp()
+            _lib.check(lib.bgl_ipc_open_handle(_lib.ctypes.create_string_buffer(hb, 64), _lib.ctypes.byref(p)))
+            out[k][w] = p.value + off
+            opened.append(p.value)
+    return out, opened
+
+
+class ShardedPipeline:
+    """Pipelined, host-sync-free rounds of the node-ID-sharded cache; one
+    process per GPU (rank = home shard `rank` of `world`, cachesim.py:505-506).
+
+    Round j, rank w = worker of batch i = j*world + w (cachesim.py:495). Its
+    stages:
+      S(j)   sample the batch (side stream)
+      X(j)   bgl_partition_push: bucket h of the sorted distinct IDs
+             (ascending = the insert order, cachesim.py:527-528) and the IDs'
+             batch positions stored straight into home h's receive area over
+             peer memory; then a barrier (NCCL all-reduce of one int -- the
+             only collective on the data path)
+      LI(j)  at every home, per bucket w in worker order (= global batch
+             order, so each shard's FIFO state machine sees the reference's
+             batch sequence): lookup vs the pre-bucket state + index insert,
+             outcome codes pushed into worker w's buffer
+      M(j)   per bucket: misses' rows over the host link (compacted list),
+             stored straight into worker w's output (peer memory)
+      B(j)   per bucket: ring hits pushed likewise, then the survivors' rows
+             into their ring slots (after the hits were read)
+      Z(j)   barrier: every home's pushes of round j landed
+    Step k enqueues S(k+3), X(k+2), LI(k+2) || M(k+1) || B(k), Z(k): the host
+    link streams misses of round k+1 while round k+2's bookkeeping and round
+    k's ring traffic run beside it (the single-GPU pipeline.py schedule,
+    with buckets inside each stage). Dependencies point backwards only; the
+    LI chain is strictly ordered, so every output equals the reference's.
+    Buffers: receive areas, bucket state and outputs by round % 3 (X(k+3)
+    is issued after Z(k), the last reader of set k % 3), samplers by round %
+    4. The homes keep no row staging: rows are written once, into the
+    worker's output; B(j) copies the survivors into the ring from there (a
+    peer read of the miss bytes over NVLink). No host synchronisation:
+    counts stay on the device and every launch is sized for the worst case.
+    Rows of round j are complete after step j (Z(j)) in out_rows[j % 3] and
+    stay valid until step j + 2 begins. `barrier` defaults to an NCCL
+    all-reduce on the current stream; tests that put several processes on
+    one GPU pass a host barrier.
+    """
+
+    NR, NSMP = 3, 4        # round sets (receive/bucket state/outputs), samplers
+
+    def __init__(self, rank: int, world: int, dg, fanouts, batch_size: int, order: torch.Tensor, seed: int,
+                 shard_capacity: int, features: torch.Tensor, num_batches: int | None = None, group=None,
+                 barrier=None):
+        from .sampler import BatchSampler, pcg_states, pcg_tables
+        self.rank, self.world, self.group = rank, world, group
+        self.b = int(batch_size)
+        self.order = order.to(device="cuda", dtype=torch.int32).contiguous()
+        total = int(self.order.numel())
+        self.num_batches = int(num_batches or (total + self.b - 1) // self.b)
+        self.samplers = [BatchSampler(dg, fanouts, self.b) for _ in range(self.NSMP)]
+        maxu = self.maxu = self.samplers[0].max_uniq
+        self.dim = features.shape[1]
+        self.engine = FeatureCacheEngine(CacheConfig(device_capacity=shard_capacity, host_capacity=0, num_devices=1,
+                                                     feature_bytes_per_node=self.dim * features.element_size()),
+                                         features, maxu, shard=(rank, world))
+        self.rb = self.engine.row_bytes
+        self.tables = pcg_tables(pcg_states(seed, range(self.num_batches)))
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.batch_counter = torch.zeros(1, dtype=torch.int64, device=dev)    # rounds staged so far
+        self.table_stage = [torch.empty((_lib.PCG_TABLE_ROWS, 4), dtype=torch.int64, device=dev)
+                            for _ in range(self.NSMP)]
+        W, R = world, self.NR
+        # receive areas (written by the workers over peer memory), per round set
+        self.recv_ids = torch.zeros((R, W, maxu), dtype=torch.int32, device=dev)
+        self.recv_pos = torch.zeros((R, W, maxu), dtype=torch.int32, device=dev)
+        self.recv_cnt = torch.zeros((R, W), dtype=torch.int64, device=dev)
+        # this rank's outputs as a worker (written by the homes), per round set
+        self.out_rows = torch.zeros((R, maxu, self.dim), dtype=features.dtype, device=dev)
+        self.out_codes = torch.zeros((R, maxu), dtype=torch.uint8, device=dev)
+        # home-side per-(round set, bucket) state
+        self.codes = torch.empty((R, W, maxu), dtype=torch.uint8, device=dev)
+        self.src_row = torch.empty((R, W, maxu), dtype=torch.int64, device=dev)
+        self.miss_pos = torch.empty((R, W, maxu), dtype=torch.int32, device=dev)
+        self.miss_cnt = torch.zeros((R, W), dtype=torch.int64, device=dev)
+        self.plans = [[self.engine.plan_buffers() for _ in range(W)] for _ in range(R)]
+        self.counters = torch.zeros(8, dtype=torch.int64, device=dev)
+        self.part_counts = torch.zeros(W, dtype=torch.int64, device=dev)
+        lib = _lib.load()
+        self.part_ws = torch.empty(int(lib.bgl_partition_workspace(maxu, W)), dtype=torch.uint8, device=dev)
+        ptrs, self._opened = ipc_map([self.recv_ids, self.recv_pos, self.recv_cnt, self.out_rows, self.out_codes],
+                                     rank, world, group)
+        rid, rpos, rcnt, orow, ocode = ptrs
+        # this rank's slot in every home's receive area, per round set: [R][W] addresses
+        slot = [[(r * W + rank) for _ in range(W)] for r in range(R)]
+        self.peer_ids = torch.tensor([[rid[h] + slot[r][h] * maxu * 4 for h in range(W)] for r in range(R)],
+                                     dtype=torch.int64, device=dev)
+        self.peer_pos = torch.tensor([[rpos[h] + slot[r][h] * maxu * 4 for h in range(W)] for r in range(R)],
+                                     dtype=torch.int64, device=dev)
+        self.peer_cnt = torch.tensor([[rcnt[h] + slot[r][h] * 8 for h in range(W)] for r in range(R)],
+                                     dtype=torch.int64, device=dev)
+        self.worker_rows, self.worker_codes = orow, ocode     # per worker w: base of its [R] output sets
+        self.token = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.barrier = barrier if barrier is not None else (lambda: dist.all_reduce(self.token, group=group))
+        self.s_sample, self.s_li, self.s_miss, self.s_back = (torch.cuda.Stream() for _ in range(4))
+        self.s_result = torch.cuda.Stream()
+        self.sampled = [torch.cuda.Event() for _ in range(self.NSMP)]
+        self.parted = [torch.cuda.Event() for _ in range(self.NSMP)]
+        self.reported = [torch.cuda.Event() for _ in range(self.NSMP)]   # result hand-off read the sampler
+        self.xdone = [torch.cuda.Event() for _ in range(R)]
+        self.li_done = [[torch.cuda.Event() for _ in range(W)] for _ in range(R)]
+        self.miss_done = [[torch.cuda.Event() for _ in range(W)] for _ in range(R)]
+        self.k = 0
+        self.primed = False
+        self._in_graph = False
+        self.graphs: dict = {}
+        # per round: hops (memset-free kernels: fused + heavy) + dedup (mark, emit, reset) + stage copy;
+        # partition (count, scan, push); per bucket: lookup, insert(2), codes push, miss gather, hit gather, copy
+        self.kernels_per_round = (2 * len(fanouts) + 3) + 3 + W * 7
+
+    def close(self) -> None:
+        lib = _lib.load()
+        for p in self._opened:
+            lib.bgl_ipc_close(p)
+        self._opened = []
+
+    def batch_of(self, j: int) -> int:
+        return (j * self.world + self.rank) % self.num_batches
+
+    # -- stages ------------------------------------------------------------------
+    def _S(self, j: int) -> None:
+        """Sample round j (batch (j*world + rank) % num_batches, chosen on the
+        device by bgl_stage_batch from a counter, so captured steps replay
+        every round of the epoch)."""
+        slot = j % self.NSMP
+        s = self.samplers[slot]
+        with torch.cuda.stream(self.s_sample):
+            if not self._in_graph:                                    # (a replayed step follows the whole
+                self.s_sample.wait_event(self.parted[slot])           # previous step: implicit there)
+                self.s_sample.wait_event(self.reported[slot])
+            _lib.call("bgl_stage_batch", self.order.data_ptr(), self.order.numel(), self.b, self.num_batches,
+                      self.tables.data_ptr(), self.batch_counter.data_ptr(), s.nodes.data_ptr(), s.counts.data_ptr(),
+                      self.table_stage[slot].data_ptr(), None, None, self.world, self.rank,
+                      _lib.stream_ptr(self.s_sample))
+            s.run(self.table_stage[slot], stream=self.s_sample)
+            self.sampled[slot].record(self.s_sample)
+
+    def _X(self, j: int) -> None:
+        main = torch.cuda.current_stream()
+        s = self.samplers[j % self.NSMP]
+        r = j % self.NR
+        if not self._in_graph:
+            main.wait_event(self.sampled[j % self.NSMP])
+        _lib.call("bgl_partition_push", s.uniq.data_ptr(), s.num_uniq.data_ptr(), s.max_uniq, self.world,
+                  self.peer_ids[r].data_ptr(), self.peer_pos[r].data_ptr(), self.peer_cnt[r].data_ptr(),
+                  self.part_counts.data_ptr(), self.part_ws.data_ptr(), _lib.stream_ptr(main))
+        self.parted[j % self.NSMP].record(main)
+        self.barrier()                                              # round j's IDs at every home
+        self.xdone[r].record(main)
+
+    def _LI(self, j: int) -> None:
+        r, maxu, h = j % self.NR, self.maxu, self.engine.dev.handle
+        lib = _lib.load()
+        with torch.cuda.stream(self.s_li):
+            st = _lib.stream_ptr(self.s_li)
+            self.s_li.wait_event(self.xdone[r])
+            for w in range(self.world):
+                ids, pos, cnt = self.recv_ids[r, w], self.recv_pos[r, w], self.recv_cnt[r, w:w + 1]
+                plan, pcount = self.plans[r][w]
+                _lib.check(lib.bgl_cache_lookup_misses(h, ids.data_ptr(), cnt.data_ptr(), maxu, w,
+                                                       self.codes[r, w].data_ptr(), self.src_row[r, w].data_ptr(),
+                                                       self.counters.data_ptr(), self.miss_pos[r, w].data_ptr(),
+                                                       self.miss_cnt[r, w:w + 1].data_ptr(), st))
+                _lib.check(lib.bgl_cache_insert_plan(h, ids.data_ptr(), maxu, plan.data_ptr(), pcount.data_ptr(),
+                                                     self.counters.data_ptr(), st))
+                _lib.check(lib.bgl_scatter_rows(pos.data_ptr(), cnt.data_ptr(), maxu, self.codes[r, w].data_ptr(), 1,
+                                                self.worker_codes[w] + r * maxu, st))
+                self.li_done[r][w].record(self.s_li)
+
+    def _M(self, j: int) -> None:
+        r, maxu, rb, eng = j % self.NR, self.maxu, self.rb, self.engine
+        ctas = 0 if eng.features.is_cuda else eng.miss_ctas
+        lib = _lib.load()
+        with torch.cuda.stream(self.s_miss):
+            st = _lib.stream_ptr(self.s_miss)
+            for w in range(self.world):
+                if not self._in_graph:
+                    self.s_miss.wait_event(self.li_done[r][w])
+                # rows go only to worker w's output (peer memory); B(j) reads the survivors back from there
+                _lib.check(lib.bgl_gather_list(self.miss_pos[r, w].data_ptr(), self.miss_cnt[r, w:w + 1].data_ptr(),
+                                               maxu, self.recv_ids[r, w].data_ptr(), eng.table, rb, None,
+                                               self.worker_rows[w] + r * maxu * rb, self.recv_pos[r, w].data_ptr(),
+                                               eng.miss_rows_in_flight, ctas, st))
+                self.miss_done[r][w].record(self.s_miss)
+
+    def _B(self, j: int) -> None:
+        r, maxu, rb, eng = j % self.NR, self.maxu, self.rb, self.engine
+        h, ring = eng.dev.handle, eng.dev.rows_ptr() or None
+        lib = _lib.load()
+        with torch.cuda.stream(self.s_back):
+            st = _lib.stream_ptr(self.s_back)
+            for w in range(self.world):
+                plan, pcount = self.plans[r][w]
+                cnt = self.recv_cnt[r, w:w + 1]
+                out_w = self.worker_rows[w] + r * maxu * rb
+                if not self._in_graph:
+                    self.s_back.wait_event(self.miss_done[r][w])
+                _lib.check(lib.bgl_gather_rows_push(self.recv_ids[r, w].data_ptr(), self.src_row[r, w].data_ptr(),
+                                                    cnt.data_ptr(), maxu, ring, eng.table, rb, None, out_w,
+                                                    self.recv_pos[r, w].data_ptr(), 1, 0, st))
+                if ring:   # survivors' rows into their ring slots, read back from worker w's output
+                    _lib.check(lib.bgl_cache_copy_rows_indexed(h, plan.data_ptr(), pcount.data_ptr(), maxu, out_w,
+                                                               self.recv_pos[r, w].data_ptr(), st))
+
+    def prime(self) -> None:
+        """Prologue: S(0..2), X(0), LI(0), M(0), X(1), LI(1)."""
+        if self.primed:
+            return
+        for j in range(3):
+            self._S(j)
+        self._X(0)
+        self._LI(0)
+        self._M(0)
+        self._X(1)
+        self._LI(1)
+        self.primed = True
+
+    PHASES = 12            # lcm(NR, NSMP): one captured graph per step phase
+
+    def _step_body(self, k: int) -> None:
+        main = torch.cuda.current_stream()
+        for x in (self.s_sample, self.s_li, self.s_miss, self.s_back):   # fork (graph capture needs it)
+            x.wait_stream(main)
+        self._S(k + 3)
+        self._X(k + 2)
+        self._LI(k + 2)
+        self._M(k + 1)
+        self._B(k)
+        for x in (self.s_sample, self.s_li, self.s_miss, self.s_back):   # the step ends when all its work has
+            main.wait_stream(x)
+        self.barrier()                                              # every home's pushes of round k landed
+
+    def capture(self) -> None:
+        """Capture the step of every phase k % 12 in a CUDA graph (with the
+        barriers: NCCL collectives are capturable). Cross-step event waits are
+        dropped inside the graphs -- replay order already puts each step
+        after the whole previous one."""
+        self.prime()
+        torch.cuda.synchronize()
+        saved = self.batch_counter.clone()
+        self._in_graph = True
+        try:
+            for phase in range(self.PHASES):
+                g = torch.cuda.CUDAGraph()
+                cs = torch.cuda.Stream()
+                cs.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(cs):
+                    with torch.cuda.graph(g, stream=cs):
+                        self._step_body(phase)
+                torch.cuda.current_stream().wait_stream(cs)
+                self.graphs[phase] = g
+        finally:
+            self._in_graph = False
+        torch.cuda.synchronize()
+        self.batch_counter.copy_(saved)        # capture does not execute; keep the counter exact
+
+    def step(self) -> None:
+        """Enqueue step k: S(k+3), X(k+2), LI(k+2) || M(k+1) || B(k), Z(k).
+        No host synchronisation; round k's rows are complete afterwards."""
+        self.prime()
+        k = self.k
+        g = self.graphs.get(k % self.PHASES)
+        if g is None:
+            self._step_body(k)
+        else:
+            main = torch.cuda.current_stream()
+            main.wait_stream(self.s_result)     # result hand-offs outside the graphs (store_result)
+            main.wait_stream(self.s_sample)     # e.g. host seeds copied on the sampling stream
+            g.replay()
+        self.k += 1
+
+    def store_result(self, j: int, host_ids_dev: int, host_meta_dev: int) -> None:
+        """After step j: hand round j's distinct IDs (the AccessTrace row) and
+        the cache counters to mapped pinned host memory (bgl_d2h_result) on a
+        side stream -- no host synchronisation, off the next step's path."""
+        s = self.samplers[j % self.NSMP]
+        self.s_result.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.s_result):
+            _lib.call("bgl_d2h_result", s.uniq.data_ptr(), s.num_uniq.data_ptr(), s.max_uniq,
+                      self.counters.data_ptr(), host_ids_dev, host_meta_dev, _lib.stream_ptr(self.s_result))
+            self.reported[j % self.NSMP].record(self.s_result)
+
+    # -- results of a completed round j (host views; synchronising) ----------------
+    def distinct(self, j: int) -> torch.Tensor:
+        s = self.samplers[j % self.NSMP]
+        return s.uniq[: int(s.num_uniq.item())]
+
+    def rows(self, j: int) -> torch.Tensor:
+        n = int(self.samplers[j % self.NSMP].num_uniq.item())
+        return self.out_rows[j % self.NR][:n]
+
+    def outcome_codes(self, j: int) -> torch.Tensor:
+        n = int(self.samplers[j % self.NSMP].num_uniq.item())
+        return self.out_codes[j % self.NR][:n]

@@ -107,7 +107,7 @@ class MiniBatchPipeline:
         _lib.call("bgl_stage_batch", order, self.order.numel(), self.b, self.num_batches,
                   self.tables.data_ptr(), self.batch_counter.data_ptr(), s.nodes.data_ptr(), s.counts.data_ptr(),
                   self.table_stage[slot].data_ptr(), self.batch_index.data_ptr() + 8 * slot,
-                  fbuf if fed else None, _lib.stream_ptr(stream))
+                  fbuf if fed else None, 1, 0, _lib.stream_ptr(stream))
         s.run(self.table_stage[slot], stream=stream, hooks=hooks)
 
     def _li(self, batch: int, stream=None) -> None:

@@ -1,0 +1,149 @@
+"""GPU test of the pipelined, host-sync-free sharded round (ShardedPipeline):
+two processes share one GPU (CUDA IPC works between processes of one device),
+each is home shard `rank` and worker of every other batch. IDs reach the homes
+through bgl_partition_push (peer stores), rows and codes come back through the
+homes' pushes; a host barrier stands in for the NCCL one (NCCL cannot put two
+ranks on one GPU). Every round's distinct set, per-node outcome codes and rows
+must equal the reference: the oracle sampler + the reference's 2-device FIFO
+simulation (cachesim.py:461-549) + F[ids]."""
+
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import cache_oracle as co
+from oracle import features_oracle as fo
+from oracle import sampler_oracle as so
+
+pytestmark = pytest.mark.gpu
+WORLD = 2
+N, DEG, FAN, B, SEED, DIM = 20000, 10, (10, 5), 256, 6, 32
+
+
+def _graph():
+    from paper_2112_08541_b200.graph import generate_power_law_exact_device
+    return generate_power_law_exact_device(N, DEG, seed=3, train_fraction=0.2, num_labels=4)
+
+
+def _order():
+    dg_train = np.arange(N)[np.random.default_rng(1).permutation(N)][: 12 * B]
+    return dg_train.astype(np.int32)
+
+
+def _worker(rank, port, cap, where, rounds, path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    from paper_2112_08541_b200.distributed import ShardedPipeline
+    from paper_2112_08541_b200.features import synthetic_features
+
+    def host_barrier():
+        torch.cuda.synchronize()
+        dist.barrier()
+
+    dg = _graph()
+    feats = synthetic_features(N, DIM, seed=8, device_resident=(where == "hbm"))
+    order = torch.from_numpy(_order()).cuda()
+    pipe = ShardedPipeline(rank, WORLD, dg, FAN, B, order, SEED, cap, feats, num_batches=rounds * WORLD,
+                           barrier=host_barrier)
+    out = {}
+    for j in range(rounds):
+        pipe.step()
+        torch.cuda.synchronize()
+        i = pipe.batch_of(j)
+        out[f"ids{i}"] = pipe.distinct(j).cpu().numpy()
+        out[f"rows{i}"] = pipe.rows(j).cpu().numpy()
+        out[f"codes{i}"] = pipe.outcome_codes(j).cpu().numpy()
+        host_barrier()            # nobody starts round j+2 (overwriting parity j) before all have read j
+    out["counters"] = pipe.counters.cpu().numpy()
+    np.savez(path + f".{rank}.npz", **out)
+    dist.barrier()
+    pipe.close()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("where,cap", [("host", 700), ("hbm", 300)])
+def test_sharded_pipeline_matches_reference(where, cap):
+    rounds = 6
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "res")
+        mp.spawn(_worker, args=(_free_port(), cap, where, rounds, path), nprocs=WORLD, join=True)
+        res = {}
+        for r in range(WORLD):
+            res.update({k + (f"_r{r}" if k == "counters" else ""): v for k, v in np.load(path + f".{r}.npz").items()})
+    # reference: same graph on the host, oracle sampler, 2-device FIFO simulation
+    from paper_2112_08541_b200.graph import power_law_edges
+    from oracle import graph_oracle as go
+    edges, _, _ = power_law_edges(N, DEG, 3, 0.2, 4)
+    off, col = go.csr_from_edges(edges.astype(np.int64), N)
+    order = _order()
+    nb = rounds * WORLD
+    distinct = [so.sample_batch(off, col, order[i * B:(i + 1) * B].astype(np.int64), FAN, SEED, i)[2]
+                for i in range(nb)]
+    # the pipeline's lookups run two rounds ahead (LI(k+2) in step k): rounds
+    # 0..rounds+1, batch indices wrapping over the epoch
+    seq = [distinct[i % nb] for i in range((rounds + 2) * WORLD)]
+    ref_cnt, ref_codes = co.FifoEngine(cap, 0, WORLD).run(seq)
+    for i in range(nb):
+        assert np.array_equal(res[f"ids{i}"], distinct[i]), i
+        assert np.array_equal(res[f"codes{i}"], ref_codes[i]), i
+        assert np.array_equal(res[f"rows{i}"], fo.synthetic_features(distinct[i], DIM, seed=8)), i
+    tot = res["counters_r0"] + res["counters_r1"]
+    assert tot[:7].tolist() == np.asarray(ref_cnt).sum(axis=0)[:7].tolist()
+
+
+def test_sharded_pipeline_graphs_single_rank_nccl():
+    """World size 1 over NCCL: the captured step (12 phases, NCCL barrier
+    inside) replays the same rounds as the eager steps, and both equal the
+    reference's 1-device FIFO simulation + F[ids]."""
+    import torch.distributed as dist
+    from paper_2112_08541_b200.distributed import ShardedPipeline
+    from paper_2112_08541_b200.features import synthetic_features
+    from paper_2112_08541_b200.graph import power_law_edges
+    from oracle import graph_oracle as go
+    if dist.is_initialized():
+        pytest.skip("process group already initialised")
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        dg = _graph()
+        feats = synthetic_features(N, DIM, seed=8)
+        order = torch.from_numpy(_order()).cuda()
+        nb, cap = 12, 500
+        pipe = ShardedPipeline(0, 1, dg, FAN, B, order, SEED, cap, feats, num_batches=nb)
+        got = {}
+        for j in range(30):
+            if j == 3:
+                pipe.capture()
+            pipe.step()
+            torch.cuda.synchronize()
+            got[j] = (pipe.distinct(j).cpu().numpy(), pipe.outcome_codes(j).cpu().numpy(),
+                      pipe.rows(j).cpu().numpy())
+        pipe.close()
+    finally:
+        dist.destroy_process_group()
+    edges, _, _ = power_law_edges(N, DEG, 3, 0.2, 4)
+    off, col = go.csr_from_edges(edges.astype(np.int64), N)
+    order_h = _order()
+    distinct = [so.sample_batch(off, col, order_h[i * B:(i + 1) * B].astype(np.int64), FAN, SEED, i)[2]
+                for i in range(nb)]
+    _, ref_codes = co.FifoEngine(cap, 0, 1).run([distinct[j % nb] for j in range(30)])
+    for j in range(30):
+        ids, codes, rows = got[j]
+        assert np.array_equal(ids, distinct[j % nb]), j
+        assert np.array_equal(codes, ref_codes[j]), j
+        assert np.array_equal(rows, fo.synthetic_features(ids, DIM, seed=8)), j
