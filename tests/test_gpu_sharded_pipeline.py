@@ -147,3 +147,37 @@ def test_sharded_pipeline_graphs_single_rank_nccl():
         assert np.array_equal(ids, distinct[j % nb]), j
         assert np.array_equal(codes, ref_codes[j]), j
         assert np.array_equal(rows, fo.synthetic_features(ids, DIM, seed=8)), j
+
+
+def _shm_worker(rank, port, path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    from paper_2112_08541_b200.features import shared_synthetic_features, table_pointer
+    from paper_2112_08541_b200 import _lib
+    n, dim = 50000, 24
+    t = shared_synthetic_features(n, dim, 5, f"bgl_test_{port}", rank, WORLD, dist.barrier, chunk_rows=7000)
+    ids = torch.from_numpy(np.random.default_rng(rank).integers(0, n, 3000).astype(np.int32)).cuda()
+    pos = torch.arange(3000, dtype=torch.int32, device="cuda")
+    cnt = torch.tensor([3000], dtype=torch.int64, device="cuda")
+    out = torch.empty((3000, dim), dtype=torch.float32, device="cuda")
+    _lib.call("bgl_gather_list", pos.data_ptr(), cnt.data_ptr(), 3000, ids.data_ptr(), table_pointer(t), dim * 4,
+              out.data_ptr(), None, None, 2, 16, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    np.savez(path + f".{rank}.npz", ids=ids.cpu().numpy(), rows=out.cpu().numpy(), host=t[::997].numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_shared_feature_store_across_processes():
+    """The /dev/shm feature store filled cooperatively by two processes and
+    registered by both: zero-copy gathers read F[ids] in each process."""
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "shm")
+        port = _free_port()
+        mp.spawn(_shm_worker, args=(port, path), nprocs=WORLD, join=True)
+        for r in range(WORLD):
+            z = np.load(path + f".{r}.npz")
+            assert np.array_equal(z["rows"], fo.synthetic_features(z["ids"], 24, seed=5))
+            assert np.array_equal(z["host"], fo.synthetic_features(np.arange(0, 50000, 997), 24, seed=5))
+        assert not os.path.exists(f"/dev/shm/bgl_test_{port}")
