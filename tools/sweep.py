@@ -60,15 +60,18 @@ if __name__ == "__main__":
     ap.add_argument("--caps", default="0.01,0.02,0.05,0.1,0.2")
     ap.add_argument("--steps", type=int, default=150)
     ap.add_argument("--warmup", type=int, default=40)
+    ap.add_argument("--orderings", default="proximity,random")
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
-    DG, FEATS, prox, setup = bench.build_inputs(cfg, "host")
+    DG, FEATS, prox, setup = bench.build_inputs(cfg, "host", "continuum" if a.config in ("c3", "c5") else "exact")
     rnd_batches = random_shuffle_schedule(DG, cfg["b"], seed=bench.RUN_SEED).batches
     rnd = torch.from_numpy(np.concatenate(rnd_batches).astype(np.int32)).cuda()
     out = {"config": a.config, "workload": cfg["workload"], "csr_entries": DG.num_edges, "setup": setup, "rows": []}
     for frac in [float(x) for x in a.caps.split(",")]:
         cap = int(frac * cfg["n"])
         for name, order in (("proximity", prox), ("random", rnd)):
+            if name not in a.orderings.split(","):
+                continue
             r = run(cfg, order, cap, a.steps, a.warmup)
             r.update(ordering=name, cache_frac=frac, cache_rows=cap)
             out["rows"].append(r)
