@@ -118,7 +118,7 @@ class FeatureCacheEngine:
         self.counters = torch.zeros(8, dtype=torch.int64, device="cuda")
         # host-link miss gather: 74 CTAs x 8 warps saturate the link while
         # leaving half the SMs' load/store pipes to the overlapped sampler
-        # (tools/gather_bench.cu, tools/overlap_probe*.py)
+        # (tools/gather_bench.cu, tools/overlap_probe.py)
         self.miss_ctas = int(os.environ.get("BGL_MISS_CTAS", 74))
         self.miss_rows_in_flight = int(os.environ.get("BGL_MISS_ROWS", 2))
 

@@ -1,4 +1,5 @@
-"""Time the two branches of a pipelined step alone and together (diagnostic)."""
+"""Pipelined step time vs the host-link floor (sum of miss-gather times) over the
+same batches from the same cold cache (diagnostic)."""
 import os
 import sys
 
@@ -10,48 +11,44 @@ import bench  # noqa: E402
 from paper_2112_08541_b200.cachesim import CacheConfig  # noqa: E402
 from paper_2112_08541_b200.pipeline import MiniBatchPipeline  # noqa: E402
 
-feat = sys.argv[1] if len(sys.argv) > 1 else "host"
-cfg = bench.CONFIGS["c2"]
-dg, feats, order, _ = bench.build_inputs(cfg, feat)
-ctas = [int(x) for x in sys.argv[2:]] or [0]
-for c in ctas:
-    pipe = MiniBatchPipeline(dg, cfg["fanouts"], cfg["b"], order, 1,
-                             CacheConfig(device_capacity=240000, feature_bytes_per_node=400), feats, sampler_ctas=c)
-    pipe.capture()
-    for _ in range(30):
-        pipe.step()
+cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
+N = 120
+dg, feats, order, _ = bench.build_inputs(cfg, "host")
+pipe = MiniBatchPipeline(dg, cfg["fanouts"], cfg["b"], order, 1,
+                         CacheConfig(device_capacity=int(0.1 * cfg["n"]), feature_bytes_per_node=cfg["dim"] * 4), feats)
+pipe.capture()
+E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+# serial pass: per-stage times for steps 0..N-1
+pipe.reset()
+pipe.prime()
+tot = [0.0] * 6
+for _ in range(N):
+    ev = [E() for _ in range(7)]
+    pipe.step_serial(ev)
     torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for _ in range(100):
-        pipe.step()
-    e.record()
-    torch.cuda.synchronize()
-    print(feat, "sampler_ctas", c, "graph step ms", s.elapsed_time(e) / 100, flush=True)
-    del pipe
-sys.exit(0)
-
-
-def timed(fn, n=50):
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for _ in range(n):
-        fn()
-    e.record()
-    torch.cuda.synchronize()
-    return s.elapsed_time(e) / n
-
-
-print("graph step      ", timed(pipe.step))
-print("eager overlapped", timed(pipe.step_eager))
-par = pipe.k % 2
-print("sample only     ", timed(lambda: pipe._sample(1 - par)))
-print("cache only      ", timed(lambda: pipe._cache(par)))
-g = torch.cuda.CUDAGraph()
-cs = torch.cuda.Stream()
-cs.wait_stream(torch.cuda.current_stream())
-with torch.cuda.stream(cs):
-    with torch.cuda.graph(g, stream=cs):
-        pipe._cache(par, stream=cs)
-torch.cuda.current_stream().wait_stream(cs)
-print("cache graph     ", timed(g.replay))
+    for i in range(6):
+        tot[i] += ev[i].elapsed_time(ev[i + 1])
+print("serial stage totals ms (sample, dedup, LI, miss, hit, copy):", [round(t, 2) for t in tot])
+# pipelined pass over the same batches
+pipe.reset()
+pipe.prime()
+s, e = E(), E()
+s.record()
+for _ in range(N):
+    pipe.step()
+e.record()
+torch.cuda.synchronize()
+print("pipelined total ms", round(s.elapsed_time(e), 2), "per step", round(s.elapsed_time(e) / N, 4),
+      "miss floor per step", round(tot[3] / N, 4))
+# miss gathers alone, back to back, same batches (cache state replayed by LI)
+pipe.reset()
+pipe.prime()
+s.record()
+for k in range(N):
+    pipe._li(k + 2)
+    pipe._miss(k + 1)
+    pipe._back(k)
+    pipe._sample(k + 3)
+e.record()
+torch.cuda.synchronize()
+print("eager serial total ms", round(s.elapsed_time(e), 2))
