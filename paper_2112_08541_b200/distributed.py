@@ -373,9 +373,10 @@ class ShardedPipeline:
         self.primed = False
         self._in_graph = False
         self.graphs: dict = {}
-        # per round: hops (memset-free kernels: fused + heavy) + dedup (mark, emit, reset) + stage copy;
-        # partition (count, scan, push); per bucket: lookup, insert(2), codes push, miss gather, hit gather, copy
-        self.kernels_per_round = (2 * len(fanouts) + 3) + 3 + W * 7
+        # per round (our kernels; the two NCCL barrier kernels not counted): stage + hops (sample + heavy)
+        # + dedup (mark, emit, reset); partition (count, scan, push); per bucket: lookup, insert (2),
+        # codes push, miss gather, hit gather, row copy
+        self.kernels_per_round = (1 + 2 * len(fanouts) + 3) + 3 + W * 7
 
     def close(self) -> None:
         lib = _lib.load()

@@ -94,9 +94,9 @@ class MiniBatchPipeline:
         self.k = 0                # batches completed (rows ready)
         self.primed = False
         s = self.samplers[0]
-        # stage + H x (scan, warp, heavy) + dedup (mark seeds, emit, reset) + lookup + insert(2)
-        # + miss gather + hit gather + row copy
-        self.kernels_per_step = 1 + 3 * s.H + 3 + 1 + 2 + 1 + 1 + 1
+        # stage + H x (sample, heavy) + dedup (mark seeds, emit, reset) + lookup + insert(2)
+        # + miss gather + hit gather + row copy (= the ncu launch list of a step); host-fed: + d2h_result
+        self.kernels_per_step = 1 + 2 * s.H + 3 + 1 + 2 + 1 + 1 + 1
 
     # -- stages ------------------------------------------------------------------
     def _sample(self, batch: int, stream=None, fed: bool = False, hooks=None) -> None:
