@@ -12,9 +12,12 @@ One mini-batch of BGL's data path:
             then the survivors' rows into their new slots (bgl_cache_copy_rows)
 
 Software pipeline (the paper overlaps sampling with feature retrieval,
-PAPER.md:536-576). Step k runs four concurrent branches
+PAPER.md:536-576). Step k runs five concurrent branches
 
-    back(k)  ||  miss(k+1)  ||  LI(k+2)  ||  sample(k+3)
+    back(k)  ||  miss(k+1)  ||  LI(k+2)  ||  b(k+3)  ||  a(k+4)
+
+(a = staging + hops 0..H-2, b = the last hop + dedup: the latency-bound
+small hops of one batch fill the GPU beside the large last hop of another)
 
 so the host link streams misses back to back while the cache bookkeeping of
 the next batch, the ring-row work of the previous one and the sampling of
@@ -27,8 +30,9 @@ fixed by that batch's own back() before any batch can hit the new occupant.
 Sampling is cache-independent (rng keyed by the batch index,
 sampler.py:138). The cache state machine therefore sees batches strictly in
 order and every output equals the reference's. Buffers: samplers by batch %
-4, rows / codes / src rows / insert plans by batch % 3; the step is captured
-once per phase (k % 12) in a CUDA graph and replayed.
+5, rows / codes / src rows / insert plans by batch % 3, host-fed seeds by
+batch % 2; the step is captured once per phase (k % 30) in a CUDA graph and
+replayed.
 """
 
 from __future__ import annotations
@@ -41,13 +45,13 @@ from .features import FeatureCacheEngine
 from .graph import DeviceGraph
 from .sampler import BatchSampler, pcg_states, pcg_tables
 
-NS, NB = 4, 3          # sampler buffers, row/plan buffers
+NS, NB = 5, 3          # sampler buffers, row/plan buffers
 NF = 2                 # host-fed seed buffers
-PHASES = 12            # lcm(NS, NB, NF)
+PHASES = 30            # lcm(NS, NB, NF)
 
 
 class MiniBatchPipeline:
-    lookahead = 3      # batch k+3 is sampled during step k
+    lookahead = 4      # batch k+4 is staged (and its first hops sampled) during step k
 
     def __init__(self, dg: DeviceGraph, fanouts, batch_size: int, order: torch.Tensor, seed: int,
                  cache_cfg: CacheConfig, features: torch.Tensor, num_batches: int | None = None,
@@ -89,7 +93,7 @@ class MiniBatchPipeline:
         self.host_meta = [torch.zeros(16, dtype=torch.int64, pin_memory=True) for _ in range(NB)]
         self._host_ids_dev = [_lib.host_device_pointer(t) for t in self.host_ids]
         self._host_meta_dev = [_lib.host_device_pointer(t) for t in self.host_meta]
-        self.streams = [torch.cuda.Stream() for _ in range(4)]     # back, miss, LI, sample
+        self.streams = [torch.cuda.Stream() for _ in range(5)]     # back, miss, LI, sample b, sample a
         self.graphs: dict = {}
         self.k = 0                # batches completed (rows ready)
         self.primed = False
@@ -99,16 +103,25 @@ class MiniBatchPipeline:
         self.kernels_per_step = 1 + 2 * s.H + 3 + 1 + 2 + 1 + 1 + 1
 
     # -- stages ------------------------------------------------------------------
-    def _sample(self, batch: int, stream=None, fed: bool = False, hooks=None) -> None:
+    def _sample(self, batch: int, stream=None, fed: bool = False, hooks=None, part: str = "all") -> None:
+        """part "a": stage the batch + hops 0..H-2; "b": the last hop + dedup;
+        "all": both. The pipeline runs a(k+4) beside b(k+3): the small first
+        hops of one batch fill the GPU beside the big last hop of another."""
         slot = batch % NS
         s = self.samplers[slot]
-        fbuf = self.fed_dev[batch % NF].data_ptr()
-        order = fbuf + 8 if fed else self.order.data_ptr()
-        _lib.call("bgl_stage_batch", order, self.order.numel(), self.b, self.num_batches,
-                  self.tables.data_ptr(), self.batch_counter.data_ptr(), s.nodes.data_ptr(), s.counts.data_ptr(),
-                  self.table_stage[slot].data_ptr(), self.batch_index.data_ptr() + 8 * slot,
-                  fbuf if fed else None, 1, 0, _lib.stream_ptr(stream))
-        s.run(self.table_stage[slot], stream=stream, hooks=hooks)
+        if part in ("a", "all"):
+            fbuf = self.fed_dev[batch % NF].data_ptr()
+            order = fbuf + 8 if fed else self.order.data_ptr()
+            _lib.call("bgl_stage_batch", order, self.order.numel(), self.b, self.num_batches,
+                      self.tables.data_ptr(), self.batch_counter.data_ptr(), s.nodes.data_ptr(), s.counts.data_ptr(),
+                      self.table_stage[slot].data_ptr(), self.batch_index.data_ptr() + 8 * slot,
+                      fbuf if fed else None, 1, 0, _lib.stream_ptr(stream))
+        if part == "all":
+            s.run(self.table_stage[slot], stream=stream, hooks=hooks)
+        elif part == "a":
+            s.run(self.table_stage[slot], stream=stream, hooks=hooks, hops=range(0, s.H - 1), dedup=False)
+        else:
+            s.run(self.table_stage[slot], stream=stream, hooks=hooks, hops=range(s.H - 1, s.H))
 
     def _li(self, batch: int, stream=None) -> None:
         s = self.samplers[batch % NS]
@@ -168,7 +181,7 @@ class MiniBatchPipeline:
             self.fed_free[j].record(torch.cuda.current_stream())
 
     def prime(self, fed: bool = False, feed=None) -> None:
-        """Prologue (untimed): sample k..k+2, LI(k), miss(k), LI(k+1).
+        """Prologue (untimed): sample k..k+2, a(k+3), LI(k), miss(k), LI(k+1).
         In host-fed mode `feed(i)` must queue batch i's seeds (self.feed)."""
         if self.primed:
             return
@@ -177,7 +190,7 @@ class MiniBatchPipeline:
                 feed(i)
             if fed:
                 self._fed_sample_guard(i, True)
-            self._sample(i, fed=fed)
+            self._sample(i, fed=fed, part="all" if i < self.k + self.lookahead - 1 else "a")
             if fed:
                 self._fed_sample_guard(i, False)
         self._li(self.k)
@@ -185,10 +198,10 @@ class MiniBatchPipeline:
         self._li(self.k + 1)
         self.primed = True
 
-    # -- one overlapped step: back(k) || miss(k+1) || LI(k+2) || sample(k+3) -------
+    # -- one overlapped step: back(k) || miss(k+1) || LI(k+2) || b(k+3) || a(k+4) ----
     def _overlapped(self, k: int, fed: bool, stream=None) -> None:
         cur = torch.cuda.current_stream() if stream is None else stream
-        sb, sm, sl, ss = self.streams
+        sb, sm, sl, ss, sa = self.streams
         for s in self.streams:
             s.wait_stream(cur)
         with torch.cuda.stream(sm):
@@ -198,17 +211,19 @@ class MiniBatchPipeline:
         with torch.cuda.stream(sb):
             self._back(k, stream=sb, fed=fed)
         with torch.cuda.stream(ss):
-            self._sample(k + 3, stream=ss, fed=fed)
+            self._sample(k + 3, stream=ss, fed=fed, part="b")
+        with torch.cuda.stream(sa):
+            self._sample(k + 4, stream=sa, fed=fed, part="a")
         for s in self.streams:
             cur.wait_stream(s)
 
     def step_eager(self, fed: bool = False) -> None:
         self.prime(fed)
         if fed:
-            self._fed_sample_guard(self.k + 3, True)
+            self._fed_sample_guard(self.k + self.lookahead, True)
         self._overlapped(self.k, fed)
         if fed:
-            self._fed_sample_guard(self.k + 3, False)
+            self._fed_sample_guard(self.k + self.lookahead, False)
         self.k += 1
 
     def step_serial(self, events) -> None:
@@ -219,7 +234,8 @@ class MiniBatchPipeline:
         k = self.k
         s = self.samplers[(k + 3) % NS]
         events[0].record()
-        self._sample(k + 3, hooks=lambda h: events[1].record() if h == s.H - 1 else None)
+        self._sample(k + 4, part="a")     # hops 0..H-2 of batch k+4 + the last hop of k+3 = one batch's hops
+        self._sample(k + 3, part="b", hooks=lambda h: events[1].record() if h == s.H - 1 else None)
         events[2].record()
         self._li(k + 2)
         events[3].record()
@@ -230,7 +246,7 @@ class MiniBatchPipeline:
         self.k += 1
 
     def capture(self, fed: bool = False) -> None:
-        """Capture the overlapped step for every phase k % 12."""
+        """Capture the overlapped step for every phase k % PHASES."""
         self.prime(fed)
         torch.cuda.synchronize()
         saved = self.batch_counter.clone()
@@ -252,10 +268,10 @@ class MiniBatchPipeline:
             self.step_eager(fed)
             return
         if fed:
-            self._fed_sample_guard(self.k + 3, True)
+            self._fed_sample_guard(self.k + self.lookahead, True)
         g.replay()
         if fed:
-            self._fed_sample_guard(self.k + 3, False)
+            self._fed_sample_guard(self.k + self.lookahead, False)
         self.k += 1
 
     # -- results of the last completed batch (k - 1) -----------------------------

@@ -154,16 +154,18 @@ class BatchSampler:
         self.nodes[:b].copy_(seeds, non_blocking=True)
         self.counts[0].fill_(b)
 
-    def run(self, table: torch.Tensor | int, stream=None, hooks=None) -> None:
+    def run(self, table: torch.Tensor | int, stream=None, hooks=None, hops=None, dedup: bool = True) -> None:
         """Sample all hops and build the distinct set for the seeds already in
-        segment 0. `table` is the batch's PCG64 jump table (241x4 uint64)."""
+        segment 0. `table` is the batch's PCG64 jump table (241x4 uint64).
+        `hops` (a range) / `dedup` run a part of it (software pipelining:
+        hops 0..H-2 of one batch beside the last hop of another)."""
         lib = _lib.load()
         st = _lib.stream_ptr(stream)
         tptr = table if isinstance(table, int) else table.data_ptr()
         base = self.nodes.data_ptr()
         cnt = self.counts.data_ptr()
         db = self.draw_base.data_ptr()
-        for h in range(self.H):
+        for h in (range(self.H) if hops is None else hops):
             _lib.check(lib.bgl_sample_hop(
                 self.dg.indptr.data_ptr(), self.dg.indices.data_ptr(),
                 base + self._seg_bytes[h], cnt + 8 * h, self.caps[h], self.eff[h], tptr, db + 8 * h,
@@ -171,6 +173,8 @@ class BatchSampler:
                 self.hop_ws.data_ptr(), self.uws.data_ptr(), self.max_ctas, st))
             if hooks is not None:
                 hooks(h)
+        if not dedup:
+            return
         # hop outputs were marked by the sampler kernels; mark the seeds and emit
         _lib.check(lib.bgl_unique_sorted(
             base, 1, self._c_seg_off, cnt, self._c_seg_max, self.dg.num_nodes,

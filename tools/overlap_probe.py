@@ -48,7 +48,8 @@ for k in range(N):
     pipe._li(k + 2)
     pipe._miss(k + 1)
     pipe._back(k)
-    pipe._sample(k + 3)
+    pipe._sample(k + 3, part="b")
+    pipe._sample(k + 4, part="a")
 e.record()
 torch.cuda.synchronize()
 print("eager serial total ms", round(s.elapsed_time(e), 2))
