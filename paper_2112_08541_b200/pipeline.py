@@ -302,6 +302,8 @@ class MiniBatchPipeline:
         """Cold cache, batch 0 next (graphs stay valid)."""
         torch.cuda.synchronize()
         _lib.call("bgl_cache_reset", self.engine.dev.handle, _lib.stream_ptr())
+        for smp in self.samplers:          # the batch staged by the last a() never ran its dedup
+            smp.clear_marks()
         self.counters.zero_()
         self.batch_counter.zero_()
         self.k = 0

@@ -185,6 +185,12 @@ class BatchSampler:
         _lib.check(lib.bgl_unique_reset(self.uws.data_ptr(), self.dg.num_nodes, self.uniq.data_ptr(),
                                         self.num_uniq.data_ptr(), self.max_uniq, st))
 
+    def clear_marks(self, stream=None) -> None:
+        """Zero the dedup bitmap: a batch whose hops ran without their
+        dedup (a pipeline reset between the two halves, run(dedup=False))
+        leaves its marks behind."""
+        _lib.call("bgl_unique_workspace_init", _lib.ptr(self.uws), self.dg.num_nodes, _lib.stream_ptr(stream))
+
     # host views (synchronising) -------------------------------------------------
     def host_counts(self) -> list[int]:
         return self.counts.cpu().tolist()
