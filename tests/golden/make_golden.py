@@ -365,11 +365,32 @@ def make_graphgen():
     np.savez_compressed(os.path.join(HERE, "graphgen.npz"), **out)
 
 
+def make_c1():
+    """BASELINE.json configs[0], end to end by the reference itself:
+    generate_power_law(100K, 20, seed=1, 0.1, 64) -> proximity_schedule(S=4,
+    b=1024, seed=1) -> simulate_epoch([10, 5], seed=1) -> simulate(FIFO,
+    10,000 device slots, d=1) with per-node outcomes."""
+    g = generate_power_law(100_000, 20, seed=1, train_fraction=0.1, num_labels=64)
+    sched = od.proximity_schedule(g, 4, 1024, seed=1)
+    cfg = sp.SamplingConfig(fanouts=(10, 5), batch_size=1024, seed=1)
+    trace, comm = sp.simulate_epoch(g, random_partition(g, 1), sched, cfg)
+    rep = cs.simulate(trace, cs.CacheConfig(device_capacity=10_000, policy="fifo", feature_bytes_per_node=512),
+                      record_outcomes=True)
+    out = {"csr_entries": np.array([g.num_edges], dtype=np.int64)}
+    put(out, "schedule", sched.batches, np.int32)
+    put(out, "trace", trace.batches, np.int32)
+    out["counters"] = np.array([rep.batch_queries, rep.batch_own_hits, rep.batch_peer_hits, rep.batch_host_hits,
+                                rep.batch_misses, rep.batch_insertions, rep.batch_evictions], dtype=np.int64).T
+    put(out, "codes", [np.array(["DPHM".index(c) for c in o], dtype=np.uint8) for o in rep.outcomes], np.uint8)
+    np.savez_compressed(os.path.join(HERE, "c1.npz"), **out)
+
+
 if __name__ == "__main__":
-    parts = sys.argv[1:] or ["sampler", "cache", "ordering", "static", "shuffle", "graphgen"]
+    parts = sys.argv[1:] or ["sampler", "cache", "ordering", "static", "shuffle", "graphgen", "c1"]
     gs = graphs()
     makers = {"sampler": lambda: make_sampler(gs), "cache": make_cache, "ordering": lambda: make_ordering(gs),
-              "static": lambda: make_static(gs), "shuffle": lambda: make_shuffle(gs), "graphgen": make_graphgen}
+              "static": lambda: make_static(gs), "shuffle": lambda: make_shuffle(gs), "graphgen": make_graphgen,
+              "c1": make_c1}
     for part in parts:
         makers[part]()
         f = part + ".npz"

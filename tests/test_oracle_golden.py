@@ -231,3 +231,28 @@ def test_graph_generator_restatement_matches_reference(golden):
         assert np.array_equal(o, off) and np.array_equal(c, col), (n, d, seed)
         assert np.array_equal(lab, labels)
         assert np.array_equal(tr, np.flatnonzero(train))
+
+
+def test_oracle_reproduces_reference_c1_epoch(golden):
+    """BASELINE.json configs[0] at full size: the reference's own epoch
+    (tests/golden/c1.npz: graph, proximity schedule, trace, FIFO outcomes)
+    reproduced by the oracle restatement on the native generator's graph."""
+    from oracle import cache_oracle as co
+    from oracle import graph_oracle as go
+    from oracle import ordering_oracle as oo
+    from oracle import sampler_oracle as so
+    from paper_2112_08541_b200.graph import power_law_edges
+    npz = golden("c1")
+    n = 100_000
+    edges, train, _ = power_law_edges(n, 20, 1, 0.1, 64)
+    off, col = go.csr_from_edges(edges.astype(np.int64), n)
+    assert len(col) == int(npz["csr_entries"][0])
+    sched = oo.proximity_schedule(off, col, train, 4, 1024, 1)
+    ref_sched = get(npz, "schedule")
+    assert all(np.array_equal(a, b) for a, b in zip(sched, ref_sched))
+    trace = [so.sample_batch(off, col, b, (10, 5), 1, i)[2] for i, b in enumerate(sched)]
+    ref_trace = get(npz, "trace")
+    assert all(np.array_equal(a, b) for a, b in zip(trace, ref_trace))
+    cnt, codes = co.FifoEngine(10_000, 0, 1).run(trace)
+    assert np.array_equal(cnt, npz["counters"])
+    assert all(np.array_equal(a, b) for a, b in zip(codes, get(npz, "codes")))
