@@ -385,12 +385,40 @@ def make_c1():
     np.savez_compressed(os.path.join(HERE, "c1.npz"), **out)
 
 
+def make_c2(nbatches: int = 3):
+    """BASELINE.json configs[1] (the bench workload) by the reference itself,
+    for the first `nbatches` mini-batches: generate_power_law(2.4M, 51,
+    seed=1, 0.08, 47) (~10 min in pure Python) -> proximity_schedule(S=4,
+    b=1024, seed=1) -> sample_batch traces ([15, 10, 5], seed=1, batch_seed=i,
+    as simulate_epoch keys them) -> simulate(FIFO, 240,000 slots) with
+    per-node outcomes. Stores the graph's CSR size + a checksum, the schedule
+    head, the traces, codes and counters."""
+    g = generate_power_law(2_400_000, 51, seed=1, train_fraction=0.08, num_labels=47)
+    sched = od.proximity_schedule(g, 4, 1024, seed=1)
+    cfg = sp.SamplingConfig(fanouts=(15, 10, 5), batch_size=1024, seed=1)
+    trace = sp.AccessTrace(batches=[sp.sample_batch(g, sched.batches[i], cfg, batch_seed=i)[1]
+                                    for i in range(nbatches)])
+    rep = cs.simulate(trace, cs.CacheConfig(device_capacity=240_000, policy="fifo", feature_bytes_per_node=400),
+                      record_outcomes=True)
+    col = g.col_indices.astype(np.int64)
+    out = {"csr_entries": np.array([g.num_edges], dtype=np.int64),
+           "csr_checksum": np.array([int((col * (np.arange(col.size) % 1000003 + 1)).sum() % (1 << 61))],
+                                    dtype=np.int64),
+           "offsets_tail": g.row_offsets[-1000:].astype(np.int64)}
+    put(out, "schedule", sched.batches[:nbatches], np.int32)
+    put(out, "trace", trace.batches, np.int32)
+    out["counters"] = np.array([rep.batch_queries, rep.batch_own_hits, rep.batch_peer_hits, rep.batch_host_hits,
+                                rep.batch_misses, rep.batch_insertions, rep.batch_evictions], dtype=np.int64).T
+    put(out, "codes", [np.array(["DPHM".index(c) for c in o], dtype=np.uint8) for o in rep.outcomes], np.uint8)
+    np.savez_compressed(os.path.join(HERE, "c2.npz"), **out)
+
+
 if __name__ == "__main__":
-    parts = sys.argv[1:] or ["sampler", "cache", "ordering", "static", "shuffle", "graphgen", "c1"]
+    parts = sys.argv[1:] or ["sampler", "cache", "ordering", "static", "shuffle", "graphgen", "c1", "c2"]
     gs = graphs()
     makers = {"sampler": lambda: make_sampler(gs), "cache": make_cache, "ordering": lambda: make_ordering(gs),
               "static": lambda: make_static(gs), "shuffle": lambda: make_shuffle(gs), "graphgen": make_graphgen,
-              "c1": make_c1}
+              "c1": make_c1, "c2": make_c2}
     for part in parts:
         makers[part]()
         f = part + ".npz"
