@@ -307,37 +307,6 @@ sample_fused_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
     }
 }
 
-// Fallback of the threshold-candidate kernel for one light parent (deg <=
-// 2048, k <= 32): the running warp top-k of sample_fused_kernel over all its
-// draws, from the state of its first draw. Rare (L < k candidates), kept out
-// of line so it costs no registers on the main path.
-__device__ __noinline__ void topk_rewalk(U128 s, const U128 A32, const U128 C32, int64_t dg, int ki,
-                                         const int32_t* __restrict__ indices, int64_t offi, int64_t oi, int32_t pidx,
-                                         int32_t* __restrict__ out_ids, int32_t* __restrict__ out_pidx,
-                                         uint32_t* __restrict__ bitmap) {
-    const int lane = lane_id();
-    const uint64_t INF = ~0ull;
-    uint64_t best = INF, kth = INF;
-    const int64_t nc = (dg + 31) >> 5;
-    for (int64_t c = 0; c < nc; ++c) {
-        if (c > 0) s = affine(A32, C32, s);
-        const int64_t t = (c << 5) + lane;
-        const uint64_t cand = t < dg ? make_key(draw_of_state(s), (uint32_t)t, (uint64_t*)nullptr) : INF;
-        if (c == 0) {
-            best = warp_bitonic_sort(cand);
-            kth = shfl(best, ki - 1);
-        } else {
-            fold_chunk(best, kth, cand, ki);
-        }
-    }
-    if (lane < ki) {
-        const int32_t v = indices[offi + key_t(best)];
-        out_ids[oi + lane] = v;
-        out_pidx[oi + lane] = pidx;
-        if (bitmap) mark_bit(bitmap, v);
-    }
-}
-
 // ---------------------------------------------------------------- threshold-candidate sampling
 // Same look-back prologue and lane-aligned per-parent stream walk as
 // sample_fused_kernel, but without a running top-k: a draw is a candidate when
@@ -346,9 +315,9 @@ __device__ __noinline__ void topk_rewalk(U128 s, const U128 A32, const U128 C32,
 // after the parent's last chunk each candidate's rank is counted by broadcast
 // comparisons and the k smallest are written at their rank. Exact: with
 // L >= k candidates every non-candidate has m >= T > every candidate's m, so
-// the k smallest (m, t) overall are the k smallest candidates. L < k or L > 64
-// (rare) re-walks the parent's draws in-warp with the running top-k
-// (topk_rewalk), so the CTA kernel after the hop only sees true heavy parents.
+// the k smallest (m, t) overall are the k smallest candidates. L < k (rare)
+// repeats the parent's pass from its first draw with a doubled threshold;
+// L > 64 (rarer still) sends it to sample_heavy_kernel.
 constexpr int kCandCap = 64;
 
 __device__ __forceinline__ uint64_t cand_threshold(int64_t k, int64_t deg) {
@@ -358,7 +327,7 @@ __device__ __forceinline__ uint64_t cand_threshold(int64_t k, int64_t deg) {
     return (uint64_t)(mu / (double)deg * 9007199254740992.0);
 }
 
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
 sample_cand_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                    const int32_t* __restrict__ parents, const int64_t* __restrict__ num_parents_dev,
                    int32_t fanout, const uint64_t* __restrict__ table, int64_t* __restrict__ draw_base,
@@ -434,22 +403,31 @@ sample_cand_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
                 s = T.at((uint64_t)(D0 + __shfl_sync(FULL, ex_d, i) + lane + 1));
                 have = true;
             }
-            const U128 s_first = s;                       // for the (rare) in-warp re-walk
+            const U128 s_first = s;                       // state of the parent's first draw
             const int nc = (int)((dg + 31) >> 5);
             int L = 0;
             U128 sn;
-            for (int c = 0; c < nc; ++c) {
-                const int t = (c << 5) + lane;
-                const uint64_t m = draw_of_state(s);
-                sn = affine(A32, C32, s);            // next chunk (the last one feeds the hand-off)
-                const bool pass = t < dg && m < tm;
-                const unsigned bm = __ballot_sync(FULL, pass);
-                if (bm) {
-                    const int pos = L + __popc(bm & lt);
-                    if (pass && pos < kCandCap) cand[pos] = (m << 11) | (uint64_t)t;
-                    L += __popc(bm);
+            uint64_t tcur = tm;
+            while (true) {
+                L = 0;
+                s = s_first;
+                for (int c = 0; c < nc; ++c) {
+                    const int t = (c << 5) + lane;
+                    const uint64_t m = draw_of_state(s);
+                    sn = affine(A32, C32, s);            // next chunk (the last one feeds the hand-off)
+                    const bool pass = t < dg && m < tcur;
+                    const unsigned bm = __ballot_sync(FULL, pass);
+                    if (bm) {
+                        const int pos = L + __popc(bm & lt);
+                        if (pass && pos < kCandCap) cand[pos] = (m << 11) | (uint64_t)t;
+                        L += __popc(bm);
+                    }
+                    if (c + 1 < nc) s = sn;
                 }
-                if (c + 1 < nc) s = sn;
+                // rare: fewer than k candidates -> the same pass with a doubled threshold
+                if (L >= ki || tcur >= (1ull << 53)) break;
+                tcur = tcur > (1ull << 52) ? (1ull << 53) : tcur * 2;
+                __syncwarp();
             }
             {   // hand the stream to the next parent: lane l gets draw (dg + l) of this parent's stream
                 const int x = (int)(dg & 31) + lane;                   // offset into chunk nc-1 (if <32) else chunk nc
@@ -465,12 +443,18 @@ sample_cand_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
             __syncwarp();
             const int64_t oi = __shfl_sync(FULL, ex_k, i);
             const int64_t gq = r * run + i;
-            const int64_t offi = __shfl_sync(FULL, off, i);
-            if (L < ki || L > kCandCap) {             // rare: exact running top-k over all its draws, in-warp
-                topk_rewalk(s_first, A32, C32, dg, ki, indices, offi, oi, (int32_t)gq, out_ids, out_pidx, bitmap);
+            if (L > kCandCap) {                       // rarer still (a doubled threshold kept > 64): CTA kernel
+                const int64_t dq = __shfl_sync(FULL, ex_d, i);
+                if (lane == 0) {
+                    const int64_t slot = (int64_t)atomicAdd((unsigned long long*)heavy_count, 1ull);
+                    heavy[slot] = (int32_t)gq;
+                    deg_prefix[gq] = dq;
+                    k_prefix[gq] = oi;
+                }
                 __syncwarp();
                 continue;
             }
+            const int64_t offi = __shfl_sync(FULL, off, i);
             const uint64_t c0 = lane < L ? cand[lane] : ~0ull;
             int r0 = 0;
             if (L <= 32) {
