@@ -250,7 +250,7 @@ def run_bgl(args, cfg):
     rb = cfg["dim"] * 4
     nb_total = (order.numel() + b - 1) // b
     pipe = MiniBatchPipeline(dg, cfg["fanouts"], b, order, RUN_SEED,
-                             CacheConfig(device_capacity=cap, feature_bytes_per_node=rb), feats)
+                             CacheConfig(device_capacity=cap, feature_bytes_per_node=rb), feats, rng=args.rng)
     pipe.step_eager()                       # warm the kernels before capture
     pipe.step_eager()
     torch.cuda.synchronize()
@@ -404,7 +404,7 @@ def run_bgl(args, cfg):
         "data": graph_data(cfg, args.graph),
         "config": {"workload": cfg["workload"], "graph": args.graph, "num_nodes": cfg["n"], "csr_entries": dg.num_edges,
                    "max_degree": dg.max_degree, "feature_dim": cfg["dim"], "fanouts": list(cfg["fanouts"]),
-                   "batch": b, "cache_rows_per_gpu": cap, "features": args.features,
+                   "batch": b, "cache_rows_per_gpu": cap, "features": args.features, "sampler_rng": args.rng,
                    "parallelism": f"replicas{world}" if world > 1 else "single",
                    "l2": "flushed between timed steps (256 MB write, outside the events)",
                    "batches_per_epoch": nb_total},
@@ -651,6 +651,8 @@ def main():
     ap.add_argument("--features", choices=["host", "hbm"], default="host")
     ap.add_argument("--graph", choices=["exact", "continuum"], default=None,
                     help="exact: the reference generator's own graph (default for c1/c2); continuum: GPU model (c3)")
+    ap.add_argument("--rng", choices=["replay", "counter"], default="replay",
+                    help="replay: the reference's numpy stream bit for bit (default); counter: Philox + Floyd")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="sharded engine: eager steps (no CUDA graphs)")
     ap.add_argument("--sharded", action="store_true", help="use the multi-GPU sharded engine even at N=1")

@@ -83,6 +83,21 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices,
                    int32_t* out_ids, int32_t* out_parent_idx, int64_t* num_out_dev,
                    void* workspace, void* mark_bitmap, int32_t max_ctas, void* stream);
 
+/* Counter-RNG mode (not bit-exact with the reference's numpy stream): per
+ * parent a uniform min(fanout, deg)-subset of its neighbours by Floyd's
+ * algorithm over Philox4x32-10 draws keyed by the batch's stream state (row 0
+ * of `table`) and counted by (parent position, hop, block) -- k draws per
+ * parent instead of deg. Same outputs/layout as bgl_sample_hop (grouped by
+ * parent in parent order; within a parent in Floyd's selection order).
+ * fanout <= 32. workspace: bgl_sample_hop_counter_workspace(max_parents). */
+size_t bgl_sample_hop_counter_workspace(int64_t max_parents);
+/* Host-side Philox4x32-10 of the kernel (diagnostics / known-answer tests). */
+void bgl_philox4x32(const uint32_t* ctr, const uint32_t* key, uint32_t* out);
+int bgl_sample_hop_counter(const int64_t* indptr, const int32_t* indices, const int32_t* parents,
+                           const int64_t* num_parents_dev, int64_t max_parents, int32_t fanout,
+                           const uint64_t* table, int32_t hop, int32_t* out_ids, int32_t* out_parent_idx,
+                           int64_t* num_out_dev, void* workspace, void* mark_bitmap, void* stream);
+
 /* Partition accounting of simulate_epoch (sampler.py:139-153).
  * request_load[part_of[p]] += 1 for every parent; local_remote[0] += #parents
  * with part_of[p] == origins[q]; local_remote[1] += the rest. origins NULL:

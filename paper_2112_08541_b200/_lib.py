@@ -32,6 +32,10 @@ PROTOTYPES = {
     "bgl_sample_hop_workspace": (c_sz, [c_i64]),
     "bgl_sample_hop": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                        c_i32, c_vp]),
+    "bgl_sample_hop_counter_workspace": (c_sz, [c_i64]),
+    "bgl_philox4x32": (None, [c_vp, c_vp, c_vp]),
+    "bgl_sample_hop_counter": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp,
+                                               c_vp, c_vp]),
     "bgl_comm_account": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),
     "bgl_take_i32": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "bgl_unique_workspace": (c_sz, [c_i64]),

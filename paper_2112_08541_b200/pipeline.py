@@ -55,7 +55,7 @@ class MiniBatchPipeline:
 
     def __init__(self, dg: DeviceGraph, fanouts, batch_size: int, order: torch.Tensor, seed: int,
                  cache_cfg: CacheConfig, features: torch.Tensor, num_batches: int | None = None,
-                 sampler_ctas: int = 0):
+                 sampler_ctas: int = 0, rng: str = "replay"):
         if cache_cfg.num_devices != 1:
             raise ValueError("single-GPU pipeline: one cache shard (num_devices=1)")
         self.dg = dg
@@ -63,7 +63,7 @@ class MiniBatchPipeline:
         self.order = order.to(device="cuda", dtype=torch.int32).contiguous()
         total = int(self.order.numel())
         self.num_batches = int(num_batches or (total + self.b - 1) // self.b)
-        self.samplers = [BatchSampler(dg, fanouts, self.b, max_ctas=sampler_ctas) for _ in range(NS)]
+        self.samplers = [BatchSampler(dg, fanouts, self.b, max_ctas=sampler_ctas, rng=rng) for _ in range(NS)]
         self.max_uniq = self.samplers[0].max_uniq
         self.engine = FeatureCacheEngine(cache_cfg, features, max_batch=self.max_uniq)
         self.outs = [self.engine.out] + [torch.empty_like(self.engine.out) for _ in range(NB - 1)]

@@ -26,9 +26,14 @@ from .graph import DeviceGraph, device_graph
 
 @dataclass
 class SamplingConfig:
+    """sampler.py:18-29. `rng` (not in the reference): "replay" reproduces
+    gnnio's numpy stream bit for bit (the default, the drop-in); "counter"
+    draws from Philox4x32-10 with Floyd's algorithm -- k draws per parent
+    instead of deg, same distribution (uniform k-subsets), different stream."""
     fanouts: tuple[int, ...] = (15, 10, 5)
     batch_size: int = 1000
     seed: int = 0
+    rng: str = "replay"
 
     def __post_init__(self):
         self.fanouts = tuple(int(f) for f in self.fanouts)
@@ -36,6 +41,8 @@ class SamplingConfig:
             raise ValueError("need at least one hop")
         if any(f < 1 for f in self.fanouts):
             raise ValueError("fanouts must be positive")
+        if self.rng not in ("replay", "counter"):
+            raise ValueError("rng must be 'replay' or 'counter'")
 
 
 @dataclass
@@ -103,8 +110,11 @@ class BatchSampler:
     `counts[h]` (device int64) holds the live length of segment h.
     """
 
-    def __init__(self, g, fanouts, max_batch: int, relabel: bool = False, max_ctas: int = 0):
+    def __init__(self, g, fanouts, max_batch: int, relabel: bool = False, max_ctas: int = 0, rng: str = "replay"):
         self.dg: DeviceGraph = device_graph(g)
+        if rng not in ("replay", "counter"):
+            raise ValueError("rng must be 'replay' or 'counter'")
+        self.rng = rng
         self.max_ctas = int(max_ctas)   # cap on sampler CTAs (0 = whole GPU)
         self.fanouts = tuple(int(f) for f in fanouts)
         self.H = len(self.fanouts)
@@ -128,7 +138,10 @@ class BatchSampler:
         self.counts = torch.zeros(self.H + 1, dtype=torch.int64, device=dev)
         self.draw_base = torch.zeros(self.H + 1, dtype=torch.int64, device=dev)   # [0] stays 0
         lib = _lib.load()
-        self.hop_ws = torch.empty(int(lib.bgl_sample_hop_workspace(max(caps[:-1]))), dtype=torch.uint8, device=dev)
+        ws = (lib.bgl_sample_hop_counter_workspace if rng == "counter" else lib.bgl_sample_hop_workspace)
+        self.hop_ws = torch.empty(int(ws(max(caps[:-1]))), dtype=torch.uint8, device=dev)
+        if rng == "counter" and max(self.eff) > 32:
+            raise ValueError("counter-RNG sampler: fanouts must be <= 32")
         n = self.dg.num_nodes
         self.max_uniq = min(total, n)
         self.uws = torch.empty(int(lib.bgl_unique_workspace(n)), dtype=torch.uint8, device=dev)
@@ -166,6 +179,14 @@ class BatchSampler:
         cnt = self.counts.data_ptr()
         db = self.draw_base.data_ptr()
         for h in (range(self.H) if hops is None else hops):
+            if self.rng == "counter":
+                _lib.check(lib.bgl_sample_hop_counter(
+                    self.dg.indptr.data_ptr(), self.dg.indices.data_ptr(), base + self._seg_bytes[h], cnt + 8 * h,
+                    self.caps[h], self.eff[h], tptr, h, base + self._seg_bytes[h + 1], self.pidx[h].data_ptr(),
+                    cnt + 8 * (h + 1), self.hop_ws.data_ptr(), self.uws.data_ptr(), st))
+                if hooks is not None:
+                    hooks(h)
+                continue
             _lib.check(lib.bgl_sample_hop(
                 self.dg.indptr.data_ptr(), self.dg.indices.data_ptr(),
                 base + self._seg_bytes[h], cnt + 8 * h, self.caps[h], self.eff[h], tptr, db + 8 * h,
@@ -211,13 +232,13 @@ class BatchSampler:
 _SAMPLERS: dict = {}
 
 
-def _sampler_for(g, fanouts, batch: int, relabel=False) -> BatchSampler:
+def _sampler_for(g, fanouts, batch: int, relabel=False, rng: str = "replay") -> BatchSampler:
     dg = device_graph(g)
-    key = (id(dg), tuple(fanouts), relabel)
+    key = (id(dg), tuple(fanouts), relabel, rng)
     s = _SAMPLERS.get(key)
     if s is None or s.dg is not dg or s.caps[0] < batch:
         cap = max(batch, s.caps[0] if s is not None and s.dg is dg else 0)
-        s = BatchSampler(dg, fanouts, cap, relabel=relabel)
+        s = BatchSampler(dg, fanouts, cap, relabel=relabel, rng=rng)
         if len(_SAMPLERS) > 8:
             _SAMPLERS.clear()
         _SAMPLERS[key] = s
@@ -236,7 +257,7 @@ def sample_batch(g, seeds, cfg: SamplingConfig, batch_seed: int = 0):
     seeds = np.asarray(seeds, dtype=np.int64) if not isinstance(seeds, torch.Tensor) else seeds
     if len(seeds) == 0:
         raise ValueError("seeds must be nonempty")
-    s = _sampler_for(g, cfg.fanouts, len(seeds))
+    s = _sampler_for(g, cfg.fanouts, len(seeds), rng=cfg.rng)
     table = pcg_tables(pcg_states(cfg.seed, [batch_seed]))
     s.load_seeds(_to_i32_device(seeds))
     s.run(table[0])
@@ -253,7 +274,7 @@ def sample_batch_relabelled(g, seeds, cfg: SamplingConfig, batch_seed: int = 0):
     (np.unique return_inverse)."""
     if len(seeds) == 0:
         raise ValueError("seeds must be nonempty")
-    s = _sampler_for(g, cfg.fanouts, len(seeds), relabel=True)
+    s = _sampler_for(g, cfg.fanouts, len(seeds), relabel=True, rng=cfg.rng)
     table = pcg_tables(pcg_states(cfg.seed, [batch_seed]))
     s.load_seeds(_to_i32_device(seeds))
     s.run(table[0])
@@ -286,7 +307,7 @@ def simulate_epoch(g, p, schedule, cfg: SamplingConfig):
             if len(b) == 0:
                 raise ValueError("seeds must be nonempty")
         maxb = max(len(b) for b in batches)
-        s = _sampler_for(dg, cfg.fanouts, maxb)
+        s = _sampler_for(dg, cfg.fanouts, maxb, rng=cfg.rng)
         tables = pcg_tables(pcg_states(cfg.seed, range(len(batches))))
         flat = np.concatenate(batches)
         offs = np.concatenate([[0], np.cumsum([len(b) for b in batches])])

@@ -117,3 +117,19 @@ def test_power_law_generator_argument_errors():
         power_law_edges(10, 2, 0, train_fraction=0.0)
     with pytest.raises(ValueError, match="num_labels"):
         power_law_edges(10, 2, 0, num_labels=11)
+
+
+def test_philox_known_answers_and_restatement():
+    """The kernel's Philox4x32-10 (host build of the same function) against
+    Random123's known-answer vectors, and the oracle restatement against it."""
+    from oracle import counter_sampler as cso
+    lib = _lib.load(require_cuda=False)
+    kat = [([0, 0, 0, 0], [0, 0], [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]),
+           ([0xFFFFFFFF] * 4, [0xFFFFFFFF] * 2, [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]),
+           ([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344], [0xA4093822, 0x299F31D0],
+            [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1])]
+    for ctr, key, want in kat:
+        c, k, o = np.array(ctr, np.uint32), np.array(key, np.uint32), np.zeros(4, np.uint32)
+        lib.bgl_philox4x32(c.ctypes.data, k.ctypes.data, o.ctypes.data)
+        assert o.tolist() == want
+        assert cso.philox4x32(ctr, key) == want

@@ -20,12 +20,13 @@ ap.add_argument("--config", default="c2")
 ap.add_argument("--features", default="host")
 ap.add_argument("--steps", type=int, default=6)
 ap.add_argument("--warm", type=int, default=20)
+ap.add_argument("--rng", default="replay")
 a = ap.parse_args()
 cfg = bench.CONFIGS[a.config]
 dg, feats, order, _ = bench.build_inputs(cfg, a.features)
 pipe = MiniBatchPipeline(dg, cfg["fanouts"], cfg["b"], order, bench.RUN_SEED,
                          CacheConfig(device_capacity=int(cfg["cache_frac"] * cfg["n"]),
-                                     feature_bytes_per_node=cfg["dim"] * 4), feats)
+                                     feature_bytes_per_node=cfg["dim"] * 4), feats, rng=a.rng)
 pipe.capture()
 for _ in range(a.warm):          # graph replays: warm cache (ncu does not see these as separate kernels)
     pipe.step()
