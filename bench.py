@@ -350,6 +350,7 @@ def run_bgl(args, cfg):
             # bytes that crossed the host link per miss-gather launch (ncu pcie__read_bytes)
             roof["traffic"] = tr["miss_gather"]["pcie_read_bytes_per_launch"]
             roof["traffic_kind"] = "pcie_read_bytes (ncu, one launch)"
+            roof["traffic_launch_algorithmic_bytes"] = tr["miss_gather"].get("algorithmic_bytes_per_launch")
         else:
             roof["traffic"] = tr["miss_gather"]["dram_bytes_per_launch"] + tr["hit_gather"]["dram_bytes_per_launch"]
             roof["traffic_kind"] = "dram__bytes_read+write (ncu, one launch of each gather; writes that stay in L2 are not counted)"
