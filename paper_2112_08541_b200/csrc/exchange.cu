@@ -175,6 +175,7 @@ __global__ void scatter_rows_kernel(const int32_t* __restrict__ pos, const int64
                 *reinterpret_cast<uint32_t*>(d + b) = *reinterpret_cast<const uint32_t*>(s + b);
         }
     }
+    __threadfence_system();   // `out` may be a peer GPU's buffer (codes pushed to the worker)
 }
 
 }  // namespace bgl

@@ -81,6 +81,7 @@ gather_v4_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ sr
             }
         }
     }
+    if (push_out) __threadfence_system();   // peer stores visible system-wide before the caller's barrier
 }
 
 // Compacted miss list (bgl_cache_lookup_misses): row j of the list is batch
@@ -131,6 +132,7 @@ gather_list_kernel(const int32_t* __restrict__ pos, const int64_t* __restrict__ 
             }
         }
     }
+    if (push_out) __threadfence_system();   // peer stores visible system-wide before the caller's barrier
 }
 
 __global__ void __launch_bounds__(kGThreads)
