@@ -300,7 +300,7 @@ def run_bgl(args, cfg):
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
         cb = pipe.counters.clone()
         flush.zero_()
-        pipe.step_serial(evs)                  # sample(k+3) | LI(k+2) | miss(k+1) | back(k)
+        pipe.step_serial(evs)                  # a(k+4) + b(k+3) | LI(k+2) | miss(k+1) | back(k)
         torch.cuda.synchronize()
         hist.append((pipe.counters - cb).cpu().tolist())
         t = [evs[i].elapsed_time(evs[i + 1]) for i in range(6)]

@@ -84,11 +84,13 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices,
                    void* workspace, void* mark_bitmap, int32_t max_ctas, void* stream);
 
 /* Counter-RNG mode (not bit-exact with the reference's numpy stream): per
- * parent a uniform min(fanout, deg)-subset of its neighbours by Floyd's
- * algorithm over Philox4x32-10 draws keyed by the batch's stream state (row 0
- * of `table`) and counted by (parent position, hop, block) -- k draws per
- * parent instead of deg. Same outputs/layout as bgl_sample_hop (grouped by
- * parent in parent order; within a parent in Floyd's selection order).
+ * parent a uniform min(fanout, deg)-subset of its neighbours from
+ * Philox4x32-10 draws keyed by the batch's stream state (row 0 of `table`) --
+ * k draws per parent instead of deg. hop 0: sub-warp per seed, parallel
+ * rejection rounds (counter (q, hop | round << 8, slot, 0)); later hops: lane
+ * per parent, Floyd's algorithm (counter (q, hop, block, 0)); see
+ * oracle/counter_sampler.py. Same outputs/layout as bgl_sample_hop (grouped
+ * by parent in parent order).
  * fanout <= 32. workspace: bgl_sample_hop_counter_workspace(max_parents). */
 size_t bgl_sample_hop_counter_workspace(int64_t max_parents);
 /* Host-side Philox4x32-10 of the kernel (diagnostics / known-answer tests). */

@@ -15,9 +15,15 @@ k = min(fanout, deg), uniform k-subsets) is checked in tests/test_gpu_counter.py
   * key = hash of the batch stream's PCG64 (state, inc) that numpy's
     SeedSequence gives (seed, batch_seed) -- the device reads it from row 0 of
     the batch's jump table;
-  * per parent q of hop h: counter (q, h, block, 0); k = min(fanout, deg);
-    deg <= k -> all neighbours in adjacency order; else Floyd's algorithm with
-    Lemire bounded draws: for j = deg-k .. deg-1: r = uniform[0, j], r = j if
+  * hop 0 (sub-warp per seed): k = min(fanout, deg); deg <= k -> all
+    neighbours in adjacency order; else m = min(k, deg - k) slots draw
+    uniform[0, deg) in rounds (slot s, round rho: Philox counter (q, h | rho
+    << 8, s, 0), Lemire acceptance over its 4 outputs); a slot keeps its draw
+    unless a slot already kept holds the value or a lower slot drew it in the
+    same round; k <= deg/2 -> the kept values in slot order, else they are the
+    excluded indices and the rest is emitted in adjacency order;
+  * hops >= 1 (lane per parent, sample_hop_floyd): counter (q, h, block, 0);
+    Floyd's algorithm: for j = deg-k .. deg-1: r = uniform[0, j], r = j if
     already chosen.
 """
 
@@ -79,6 +85,44 @@ def sample_hop(row_offsets, col, parents, fanout, key, hop):
         if deg <= k:
             out.extend(int(col[off + t]) for t in range(k))
         else:
+            excl = 2 * k > deg
+            m = deg - k if excl else k
+            kept = [None] * m
+            rho = 0
+            thr = ((1 << 32) - deg) % deg
+            while any(v is None for v in kept):
+                draws = {}
+                for sl in range(m):
+                    if kept[sl] is None:
+                        c = philox4x32([q, hop | (rho << 8), sl, 0], key)
+                        for u in c:
+                            mm = u * deg
+                            if (mm & M32) >= thr:
+                                draws[sl] = mm >> 32
+                                break
+                before = {v for v in kept if v is not None}
+                for sl in sorted(draws):
+                    v = draws[sl]
+                    if v not in before and not any(draws[s2] == v for s2 in draws if s2 < sl):
+                        kept[sl] = v
+                rho += 1
+            if excl:
+                ex = set(kept)
+                out.extend(int(col[off + t]) for t in range(deg) if t not in ex)
+            else:
+                out.extend(int(col[off + v]) for v in kept)
+        pidx.extend([q] * k)
+    return np.array(out, dtype=np.int64), np.array(pidx, dtype=np.int64)
+
+
+def sample_hop_floyd(row_offsets, col, parents, fanout, key, hop):
+    out, pidx = [], []
+    for q, p in enumerate(parents):
+        off, deg = int(row_offsets[p]), int(row_offsets[p + 1] - row_offsets[p])
+        k = min(fanout, deg)
+        if deg <= k:
+            out.extend(int(col[off + t]) for t in range(k))
+        else:
             rs, chosen = _Stream(key, q, hop), []
             for i in range(k):
                 j = deg - k + i
@@ -96,7 +140,8 @@ def sample_batch(row_offsets, col, seeds, fanouts, seed, batch_seed=0):
     parents = np.asarray(seeds, dtype=np.int64)
     frontiers, pidxs = [], []
     for h, f in enumerate(fanouts):
-        ids, pidx = sample_hop(row_offsets, col, parents, f, key, h)
+        hop_fn = sample_hop if h == 0 else sample_hop_floyd
+        ids, pidx = hop_fn(row_offsets, col, parents, f, key, h)
         frontiers.append(ids)
         pidxs.append(pidx)
         parents = ids

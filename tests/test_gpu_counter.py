@@ -30,7 +30,7 @@ def graph():
     return dg, dg.to_host()
 
 
-@pytest.mark.parametrize("fanouts", [(15, 10, 5), (25, 10), (32,), (1, 1, 1), (3, 3, 3, 3)])
+@pytest.mark.parametrize("fanouts", [(15, 10, 5), (25, 10), (32,), (1, 1, 1), (3, 3, 3, 3), (2, 7)])
 def test_counter_sampler_matches_its_restatement(graph, fanouts):
     import paper_2112_08541_b200 as bgl
     dg, hg = graph
@@ -72,17 +72,33 @@ def test_counter_sampler_neighbour_validity(graph):
         parents = ids
 
 
-def test_counter_sampler_subsets_are_uniform():
-    """A parent of degree 20 sampled with fanout 5 by 6000 independent
-    parent positions: every neighbour appears with probability 1/4 and every
-    pair with probability C(18,3)/C(20,5) (chi-square, p > 1e-5)."""
+@pytest.mark.parametrize("hop", [0, 1])
+@pytest.mark.parametrize("deg,f", [(20, 5), (9, 6)])
+def test_counter_sampler_subsets_are_uniform(deg, f, hop):
+    """A hub of degree `deg` sampled with fanout f by 6000 independent parent
+    positions: every neighbour appears with probability f/deg and every pair
+    with probability C(deg-2, f-2)/C(deg, f) (chi-square, p > 1e-5). hop 0
+    runs the sub-warp rejection kernel ((9, 6): the complement branch, 3
+    excluded indices drawn), hop 1 the lane-per-parent Floyd kernel (the hub
+    reached through a degree-1 node)."""
     import paper_2112_08541_b200 as bgl
-    deg, f, reps = 20, 5, 6000
-    off = np.array([0, deg] + [deg + i + 1 for i in range(deg)], dtype=np.int64)
-    col = np.concatenate([np.arange(1, deg + 1), np.zeros(deg, dtype=np.int64)])
+    reps = 6000
+    # nodes: 0 = hub, 1..deg = its leaves, deg+1 = a node whose only neighbour is the hub
+    adj = [list(range(1, deg + 1)) + [deg + 1]] + [[0] for _ in range(deg)] + [[0]]
+    if hop == 0:
+        adj[0] = list(range(1, deg + 1))
+        adj = adj[:deg + 1]
+    off = np.concatenate([[0], np.cumsum([len(a) for a in adj])]).astype(np.int64)
+    col = np.concatenate([np.array(a, dtype=np.int64) for a in adj])
     g = G(off, col)
-    fr, _ = bgl.sample_batch(g, np.zeros(reps, dtype=np.int64), bgl.SamplingConfig(fanouts=(f,), seed=1, rng="counter"))
-    picks = fr[0].reshape(reps, f) - 1
+    if hop == 0:
+        seeds, fans = np.zeros(reps, dtype=np.int64), (f,)
+    else:
+        seeds, fans = np.full(reps, deg + 1, dtype=np.int64), (1, f)
+        deg += 1          # the hub's adjacency also holds the entry node (id deg+1)
+    fr, _ = bgl.sample_batch(g, seeds, bgl.SamplingConfig(fanouts=fans, seed=1, rng="counter"))
+    picks = fr[hop].reshape(reps, f)
+    picks = np.where(picks == deg, 0, picks) if hop else picks - 1   # map neighbour IDs to 0..deg-1
     single = np.bincount(picks.ravel(), minlength=deg)
     assert stats.chisquare(single).pvalue > 1e-5
     pair = np.zeros((deg, deg), dtype=np.int64)
