@@ -473,7 +473,7 @@ def run_sharded(args, cfg):
     seeds_pinned = torch.from_numpy(order_host).pin_memory()
 
     if args.exchange == "push":
-        pipe = ShardedPipeline(rank, world, dg, cfg["fanouts"], b, order, RUN_SEED, cap, feats)
+        pipe = ShardedPipeline(rank, world, dg, cfg["fanouts"], b, order, RUN_SEED, cap, feats, rng=args.rng)
         counters = pipe.counters
         launches = pipe.kernels_per_round
         graphs = "off"
@@ -582,7 +582,8 @@ def run_sharded(args, cfg):
                        "by the homes' gathers (CUDA IPC), NCCL one-int barriers, no host sync per round"
                        if args.exchange == "push" else "IDs and rows by NCCL all-to-all (host-synchronised)"),
                    "l2": "flushed between timed steps (256 MB write, outside the events)",
-                   "step": f"one round = {world} mini-batches (one per GPU)", "cuda_graphs": graphs},
+                   "step": f"one round = {world} mini-batches (one per GPU)", "cuda_graphs": graphs,
+                   "sampler_rng": args.rng},
         "feature_gbs": round(q * rb / (total_ms * 1e-3) / 1e9, 2),
         "hit_pct": round(100.0 * (own + peer + hst) / max(q, 1), 2),
         "peer_hit_pct": round(100.0 * peer / max(q, 1), 2),

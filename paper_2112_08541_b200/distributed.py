@@ -310,14 +310,14 @@ class ShardedPipeline:
 
     def __init__(self, rank: int, world: int, dg, fanouts, batch_size: int, order: torch.Tensor, seed: int,
                  shard_capacity: int, features: torch.Tensor, num_batches: int | None = None, group=None,
-                 barrier=None):
+                 barrier=None, rng: str = "replay"):
         from .sampler import BatchSampler, pcg_states, pcg_tables
         self.rank, self.world, self.group = rank, world, group
         self.b = int(batch_size)
         self.order = order.to(device="cuda", dtype=torch.int32).contiguous()
         total = int(self.order.numel())
         self.num_batches = int(num_batches or (total + self.b - 1) // self.b)
-        self.samplers = [BatchSampler(dg, fanouts, self.b) for _ in range(self.NSMP)]
+        self.samplers = [BatchSampler(dg, fanouts, self.b, rng=rng) for _ in range(self.NSMP)]
         maxu = self.maxu = self.samplers[0].max_uniq
         self.dim = features.shape[1]
         self.engine = FeatureCacheEngine(CacheConfig(device_capacity=shard_capacity, host_capacity=0, num_devices=1,
