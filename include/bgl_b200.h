@@ -250,6 +250,12 @@ int bgl_gather_rows(const int32_t* ids, const int64_t* src_row, const int64_t* n
 int bgl_gather_list(const int32_t* pos, const int64_t* count_dev, int64_t max_n, const int32_t* ids,
                     const void* table, int64_t row_bytes, void* out, void* push_out, const int32_t* push_pos,
                     int32_t rows_in_flight, int32_t ctas, void* stream);
+/* bgl_gather_list for the miss path, span-aware: runs of consecutive node IDs
+ * in the compacted list (consecutive output rows too) are copied with one TMA
+ * bulk copy each (host/HBM -> shared -> out), single rows with 16-B loads.
+ * row_bytes % 16 == 0; ctas > 0 launches exactly that many 8-warp CTAs. */
+int bgl_gather_spans(const int32_t* pos, const int64_t* count_dev, int64_t max_n, const int32_t* ids,
+                     const void* table, int64_t row_bytes, void* out, int32_t ctas, void* stream);
 /* Fill rows of the deterministic synthetic feature table (oracle/features_oracle.py). */
 int bgl_synthetic_features(int64_t first_node, int64_t num_nodes, int32_t dim, uint64_t seed,
                            float* out, void* stream);

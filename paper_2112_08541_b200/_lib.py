@@ -65,6 +65,7 @@ PROTOTYPES = {
     "bgl_cache_warm": (ctypes.c_int, [c_vp, c_vp, p_i64, c_vp, c_i64, c_vp]),
     "bgl_gather_rows":(ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_i32, c_i32, c_vp]),
     "bgl_gather_list": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),
+    "bgl_gather_spans": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_i32, c_vp]),
     "bgl_synthetic_features": (ctypes.c_int, [c_i64, c_i64, c_i32, c_u64, c_vp, c_vp]),
     "bgl_power_law_edge_bound": (c_i64, [c_i64, c_i64, c_i32]),
     "bgl_power_law_generate": (ctypes.c_int, [c_i64, c_i64, c_i32, ctypes.c_double, c_i64, c_vp, c_vp, c_i64, c_vp,

@@ -121,6 +121,8 @@ class FeatureCacheEngine:
         # (tools/gather_bench.cu, tools/overlap_probe.py)
         self.miss_ctas = int(os.environ.get("BGL_MISS_CTAS", 74))
         self.miss_rows_in_flight = int(os.environ.get("BGL_MISS_ROWS", 2))
+        # runs of consecutive IDs as TMA bulk copies (bgl_gather_spans); "0": per-row loads only
+        self.miss_spans = os.environ.get("BGL_MISS_SPANS", "1") != "0"
 
     def retrieve_device(self, ids: torch.Tensor, n_dev: torch.Tensor, max_n: int, worker: int,
                         counters: torch.Tensor | None = None, stream=None, out: torch.Tensor | None = None,
@@ -215,6 +217,10 @@ class FeatureCacheEngine:
         lib = _lib.load()
         st = _lib.stream_ptr(stream)
         ctas = 0 if self.features.is_cuda else self.miss_ctas
+        if miss_pos is not None and self.miss_spans and self.row_bytes % 16 == 0:
+            _lib.check(lib.bgl_gather_spans(miss_pos.data_ptr(), miss_count.data_ptr(), max_n, ids.data_ptr(),
+                                            self.table, self.row_bytes, out.data_ptr(), ctas, st))
+            return
         if miss_pos is not None:     # compacted list: every warp keeps real rows in flight
             _lib.check(lib.bgl_gather_list(miss_pos.data_ptr(), miss_count.data_ptr(), max_n, ids.data_ptr(),
                                            self.table, self.row_bytes, out.data_ptr(), None, None,

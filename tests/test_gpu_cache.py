@@ -218,3 +218,38 @@ def test_compacted_miss_list_and_gather(rows_in_flight, where):
                                         _lib.stream_ptr()))
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("dim", [16, 100, 128])
+@pytest.mark.parametrize("where", ["host", "hbm"])
+def test_span_gather_matches_rows(dim, where):
+    """bgl_gather_spans: runs of consecutive IDs (TMA bulk copies) and single
+    rows (16-B loads) in a compacted miss list; exactly the listed rows are
+    written, each equal to F[id]; runs cross the 16-entry chunks."""
+    from paper_2112_08541_b200 import _lib
+    from paper_2112_08541_b200.features import synthetic_features, table_pointer
+    rng = np.random.default_rng(dim)
+    n = 40000
+    feats = synthetic_features(n, dim, seed=4, device_resident=(where == "hbm"))
+    # a sorted distinct batch made of runs of random lengths
+    starts = np.sort(rng.choice(n - 40, 900, replace=False))
+    batch = np.unique(np.concatenate([np.arange(s, s + rng.integers(1, 30)) for s in starts]))
+    batch = batch[batch < n]
+    miss = np.sort(rng.choice(len(batch), int(0.6 * len(batch)), replace=False)).astype(np.int32)
+    ids = torch.from_numpy(batch.astype(np.int32)).cuda()
+    pos = torch.from_numpy(miss).cuda()
+    cnt = torch.tensor([len(miss)], dtype=torch.int64, device="cuda")
+    out = torch.zeros((len(batch), dim), dtype=torch.float32, device="cuda")
+    _lib.call("bgl_gather_spans", pos.data_ptr(), cnt.data_ptr(), len(batch), ids.data_ptr(), table_pointer(feats),
+              dim * 4, out.data_ptr(), 0 if where == "hbm" else 37, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    ref = fo.synthetic_features(batch, dim, seed=4)
+    assert np.array_equal(o[miss], ref[miss])
+    rest = np.setdiff1d(np.arange(len(batch)), miss)
+    assert not o[rest].any()
+    # empty list
+    cnt.zero_()
+    _lib.call("bgl_gather_spans", pos.data_ptr(), cnt.data_ptr(), len(batch), ids.data_ptr(), table_pointer(feats),
+              dim * 4, out.data_ptr(), 0, _lib.stream_ptr())
+    torch.cuda.synchronize()
