@@ -385,6 +385,26 @@ def make_c1():
     np.savez_compressed(os.path.join(HERE, "c1.npz"), **out)
 
 
+def make_policies(gs):
+    """compare_policies (cachesim.py:378-409) + amortized_update_ops
+    (:366-375) over the device-run policies on a sampled trace of the planted
+    graph, d = 2 devices with a host level."""
+    g = gs["dense"]
+    sched = od.proximity_schedule(g, 2, 128, seed=3)
+    trace, _ = sp.simulate_epoch(g, random_partition(g, 1), sched, sp.SamplingConfig(fanouts=(5, 3), seed=2))
+    rows = cs.compare_policies(g, trace, [40, 150, 600], policies=("static-degree", "fifo"), num_devices=2,
+                               host_capacity=100)
+    amort = cs.amortized_update_ops(cs.simulate(trace, cs.CacheConfig(device_capacity=150, host_capacity=100,
+                                                                       num_devices=2)))
+    out = {"rows": np.array([[["static-degree", "fifo"].index(r["policy"]), r["capacity"], r["device_hits"],
+                              r["host_hits"], r["misses"]] for r in rows], dtype=np.int64),
+           "hit_ratio": np.array([r["hit_ratio"] for r in rows], dtype=np.float64),
+           "amortized": np.array([amort[k] for k in ("lookups_per_batch", "insertions_per_batch",
+                                                     "evictions_per_batch", "metadata_updates_per_batch")])}
+    put(out, "trace", trace.batches, np.int32)
+    np.savez_compressed(os.path.join(HERE, "policies.npz"), **out)
+
+
 def make_c2(nbatches: int = 3):
     """BASELINE.json configs[1] (the bench workload) by the reference itself,
     for the first `nbatches` mini-batches: generate_power_law(2.4M, 51,
@@ -414,11 +434,11 @@ def make_c2(nbatches: int = 3):
 
 
 if __name__ == "__main__":
-    parts = sys.argv[1:] or ["sampler", "cache", "ordering", "static", "shuffle", "graphgen", "c1", "c2"]
+    parts = sys.argv[1:] or ["sampler", "cache", "ordering", "static", "shuffle", "graphgen", "c1", "c2", "policies"]
     gs = graphs()
     makers = {"sampler": lambda: make_sampler(gs), "cache": make_cache, "ordering": lambda: make_ordering(gs),
               "static": lambda: make_static(gs), "shuffle": lambda: make_shuffle(gs), "graphgen": make_graphgen,
-              "c1": make_c1, "c2": make_c2}
+              "c1": make_c1, "c2": make_c2, "policies": lambda: make_policies(gs)}
     for part in parts:
         makers[part]()
         f = part + ".npz"

@@ -253,3 +253,30 @@ def test_span_gather_matches_rows(dim, where):
     _lib.call("bgl_gather_spans", pos.data_ptr(), cnt.data_ptr(), len(batch), ids.data_ptr(), table_pointer(feats),
               dim * 4, out.data_ptr(), 0, _lib.stream_ptr())
     torch.cuda.synchronize()
+
+
+def test_compare_policies_and_amortized_ops_match_reference(golden):
+    """compare_policies over the device-run policies (static-degree, FIFO) and
+    amortized_update_ops equal the reference's on a sampled trace
+    (tests/golden/policies.npz; cachesim.py:366-409)."""
+    from paper_2112_08541_b200 import cachesim as cs
+    from paper_2112_08541_b200.sampler import AccessTrace
+    from conftest import golden_graph
+    npz = golden("policies")
+    g_npz = golden("sampler")
+    off, col, train = golden_graph(g_npz, "dense")
+
+    class Gr:
+        row_offsets, col_indices, num_nodes, train_mask = off, col, len(off) - 1, train
+
+    trace = AccessTrace(batches=[b.astype(np.int64) for b in get(npz, "trace")])
+    rows = cs.compare_policies(Gr(), trace, [40, 150, 600], policies=("static-degree", "fifo"), num_devices=2,
+                               host_capacity=100)
+    got = np.array([[["static-degree", "fifo"].index(r["policy"]), r["capacity"], r["device_hits"], r["host_hits"],
+                     r["misses"]] for r in rows])
+    assert np.array_equal(got, npz["rows"])
+    assert [r["hit_ratio"] for r in rows] == npz["hit_ratio"].tolist()
+    amort = cs.amortized_update_ops(cs.simulate(trace, cs.CacheConfig(device_capacity=150, host_capacity=100,
+                                                                      num_devices=2)))
+    assert [amort[k] for k in ("lookups_per_batch", "insertions_per_batch", "evictions_per_batch",
+                               "metadata_updates_per_batch")] == npz["amortized"].tolist()
