@@ -82,3 +82,29 @@ def test_criterion_7_invariant_sweeps(bgl):
         f1, d1 = bgl.sample_batch(g, seeds, cfg, batch_seed=bs)
         f2, d2 = bgl.sample_batch(g, seeds, cfg, batch_seed=bs)
         assert all(np.array_equal(a, b) for a, b in zip(f1, f2)) and np.array_equal(d1, d2)
+
+
+def test_criterion_6_shuffling_error_gate(bgl):
+    """Shuffling error falls as the number of BFS sequences S grows
+    (Spearman <= -0.8 over S = 1..10, 5 graphs each), select_num_sequences
+    returns the minimal S meeting the threshold, and S = 1 / epsilon = 0 for a
+    single-label graph (ordering.py:157-231)."""
+    from scipy.stats import spearmanr
+    b, s_values, means = 200, list(range(1, 11)), []
+    graphs = [bgl.generate_power_law(20000, 10, seed=seed + 1, train_fraction=0.1, num_labels=32) for seed in range(5)]
+    for S in s_values:
+        means.append(float(np.mean([bgl.shuffling_error(bgl.proximity_schedule(g, S, b, seed=seed), g.labels).epsilon
+                                    for seed, g in enumerate(graphs)])))
+    rho = float(spearmanr(s_values, means).statistic)
+    assert rho <= -0.8
+    g2 = bgl.generate_power_law(5000, 10, seed=3, train_fraction=0.1, num_labels=2)
+    M = 4
+    s_sel, rep = bgl.select_num_sequences(g2, 250, M, 10, seed=0)
+    thr = bgl.shuffling_error_threshold(250, M, int(g2.train_mask.sum()))
+    assert rep.threshold_met and rep.epsilon <= thr
+    for smaller in range(1, s_sel):
+        assert bgl.shuffling_error(bgl.proximity_schedule(g2, smaller, 250, seed=0), g2.labels).epsilon > thr
+    g1 = bgl.generate_power_law(5000, 10, seed=3, train_fraction=0.1, num_labels=1)
+    s_const, rep_const = bgl.select_num_sequences(g1, 250, M, 10, seed=0)
+    assert s_const == 1 and rep_const.epsilon == 0.0
+    print(f"\n[criterion 6] spearman={rho:.2f}, minimal S={s_sel} (eps={rep.epsilon:.4f} <= {thr:.4f})")
