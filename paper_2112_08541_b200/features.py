@@ -186,15 +186,6 @@ class FeatureCacheEngine:
         plan = torch.empty((self.cfg.num_devices, stride, 2), dtype=torch.int32, device="cuda")
         return plan, torch.zeros(self.cfg.num_devices, dtype=torch.int64, device="cuda")
 
-    def front(self, ids, n_dev, max_n, worker, out, codes, src_row, plan, plan_count, counters, stream=None,
-              events=None):
-        """Lookup, insert-after-batch (indices/rings only, rows deferred to
-        back()), then the misses' rows from the feature store into `out`."""
-        self.lookup_insert(ids, n_dev, max_n, worker, codes, src_row, plan, plan_count, counters, stream)
-        if events is not None:
-            events[0].record()
-        self.miss_gather(ids, n_dev, max_n, out, src_row, stream)
-
     def lookup_insert(self, ids, n_dev, max_n, worker, codes, src_row, plan, plan_count, counters, stream=None,
                       miss_pos=None, miss_count=None):
         """miss_pos/miss_count given (single-shard engines): the lookup also
