@@ -361,7 +361,8 @@ class ShardedPipeline:
         self.worker_rows, self.worker_codes = orow, ocode     # per worker w: base of its [R] output sets
         self.token = torch.zeros(1, dtype=torch.int32, device=dev)
         self.barrier = barrier if barrier is not None else (lambda: dist.all_reduce(self.token, group=group))
-        self.s_sample, self.s_li, self.s_miss, self.s_back = (torch.cuda.Stream() for _ in range(4))
+        self.s_sample = torch.cuda.Stream(priority=-1)      # sampling: high priority (pipeline.py)
+        self.s_li, self.s_miss, self.s_back = (torch.cuda.Stream() for _ in range(3))
         self.s_result = torch.cuda.Stream()
         self.sampled = [torch.cuda.Event() for _ in range(self.NSMP)]
         self.parted = [torch.cuda.Event() for _ in range(self.NSMP)]
