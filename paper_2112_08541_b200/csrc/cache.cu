@@ -347,6 +347,46 @@ __global__ void insert_kernel(const int32_t* __restrict__ sorted_ids, int32_t d,
     if (lane == 0 && ev) atomicAdd((unsigned long long*)&counters[6], (unsigned long long)ev);
 }
 
+// The same insert with one THREAD per touched slot: index/ring/plan updates
+// only (no row copy), so a warp per slot would leave 31 lanes idle.
+__global__ void insert_index_kernel(const int32_t* __restrict__ sorted_ids, int32_t d, int64_t C, int64_t Ch,
+                                    int32_t* __restrict__ rings, int32_t* __restrict__ hring,
+                                    int32_t* __restrict__ slot_of, int32_t* __restrict__ hslot_of,
+                                    const int64_t* __restrict__ tails, const int64_t* __restrict__ mcount,
+                                    const int32_t* __restrict__ lists, int64_t list_cap,
+                                    int64_t* __restrict__ counters, int32_t* __restrict__ plan, int64_t plan_stride) {
+    const int y = blockIdx.y;
+    const bool host = (y == d);
+    const int64_t cap = host ? Ch : C;
+    if (cap == 0) return;
+    const int64_t M = mcount[y];
+    const int64_t lim = M < cap ? M : cap;
+    const int64_t t0 = tails[y];
+    int32_t* ring = host ? hring : rings + (int64_t)y * C;
+    int32_t* index = host ? hslot_of : slot_of;
+    const int32_t* list = lists + (int64_t)y * list_cap;
+    int64_t ev = 0;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < lim; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t slot = (t0 + r) % cap;
+        const int64_t j = r + cap * ((M - 1 - r) / cap);   // last miss landing in this slot
+        const int32_t pos = list[j];
+        const int32_t v = sorted_ids[pos];
+        const int32_t old = ring[slot];
+        if (old >= 0) {
+            index[old] = -1;
+            ++ev;
+        }
+        ring[slot] = v;
+        index[v] = (int32_t)slot;
+        if (!host && plan != nullptr) {
+            plan[2 * ((int64_t)y * plan_stride + r)] = pos;
+            plan[2 * ((int64_t)y * plan_stride + r) + 1] = (int32_t)slot;
+        }
+    }
+    const int64_t wev = warp_sum_i64(ev);
+    if (lane_id() == 0 && wev) atomicAdd((unsigned long long*)&counters[6], (unsigned long long)wev);
+}
+
 __global__ void insert_finalize_kernel(int32_t d, int64_t C, int64_t Ch, int64_t* __restrict__ tails,
                                        const int64_t* __restrict__ mcount, int64_t* __restrict__ counters,
                                        int64_t* __restrict__ plan_count) {
@@ -596,11 +636,11 @@ int bgl_cache_insert_plan(bgl_cache_t c, const int32_t* sorted_ids, int64_t max_
     const int64_t stride = bgl_cache_plan_stride(c, max_sorted);
     const int64_t work = std::min<int64_t>(max_sorted, std::max(c->C, c->Ch));
     if (work > 0) {
-        dim3 grid(grid_for(work * 32, 256, 8), c->d + 1);
-        insert_kernel<<<grid, 256, 0, st>>>(sorted_ids, c->d, c->C, c->Ch, c->rings, c->hring, c->slot_of,
-                                            c->hslot_of, c->tails, c->mcount, c->lists, c->list_cap, nullptr,
-                                            c->rows, c->rb, counters, plan, stride);
-        BGL_TRY(launch_status("insert_kernel"));
+        dim3 grid(grid_for(work, 256, 8), c->d + 1);
+        insert_index_kernel<<<grid, 256, 0, st>>>(sorted_ids, c->d, c->C, c->Ch, c->rings, c->hring, c->slot_of,
+                                                  c->hslot_of, c->tails, c->mcount, c->lists, c->list_cap,
+                                                  counters, plan, stride);
+        BGL_TRY(launch_status("insert_index_kernel"));
     }
     insert_finalize_kernel<<<1, 32, 0, st>>>(c->d, c->C, c->Ch, c->tails, c->mcount, counters, plan_count);
     return launch_status("insert_finalize_kernel");
