@@ -325,7 +325,7 @@ def run_bgl(args, cfg):
         achieved = host_bytes / (gather_ms * 1e-3) / 1e9
         roof = {"bound": "host_link", "achieved": round(achieved, 2), "peak": round(peak_host, 2), "unit": "GB/s",
                 "frac": round(achieved / peak_host, 3),
-                "traffic": None, "kernel": "gather_list_kernel (compacted misses, zero-copy host reads)",
+                "traffic": None, "kernel": "gather_span_kernel (compacted misses: TMA spans + 16-B zero-copy host reads)",
                 "algorithmic_bytes_per_launch": int(host_bytes),
                 "peak_source": "max over this run of the pinned host->device cudaMemcpy (256 MB, best of 8; at "
                                "start-up, before the timed region, after the stage breakdown: "
@@ -341,7 +341,7 @@ def run_bgl(args, cfg):
         achieved = alg / (t_g * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 3), "traffic": None,
-                "kernel": "gather_list_kernel (misses) + gather_v4_kernel (hits), one launch each",
+                "kernel": "gather_span_kernel (misses) + gather_v4_kernel (hits), one launch each",
                 "algorithmic_bytes_per_launch": int(alg)}
     prof = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{args.features}.json")
     if os.path.exists(prof):
