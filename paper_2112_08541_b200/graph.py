@@ -155,23 +155,43 @@ def power_law_edges(n: int, avg_degree: int, seed: int, train_fraction: float = 
     return edges[: ne.value], train.astype(bool), labels
 
 
-def csr_from_edges_device(edges: np.ndarray, n: int, dev=None) -> tuple[torch.Tensor, torch.Tensor]:
+def csr_from_edges_device(edges: np.ndarray, n: int, dev=None, max_keys: int = 1 << 29) -> tuple[torch.Tensor, torch.Tensor]:
     """Sorted, deduplicated, symmetric CSR without self-loops on the device
-    (csr_from_edges, graph.py:88-107): (indptr int64 [n+1], indices int32)."""
+    (csr_from_edges, graph.py:88-107): (indptr int64 [n+1], indices int32).
+    Large edge lists (CUB sorts < 2^31 keys; papers100M has 3.1B directed
+    keys) are keyed and deduplicated per source-node range."""
     dev = torch.device("cuda", torch.cuda.current_device()) if dev is None else torch.device(dev)
-    e = torch.from_numpy(np.ascontiguousarray(edges)).to(dev)
-    src, dst = e[:, 0].to(torch.int64), e[:, 1].to(torch.int64)
-    del e
-    keep = src != dst
-    src, dst = src[keep], dst[keep]
-    key = torch.unique(torch.cat([src * n + dst, dst * n + src]))
-    del src, dst, keep
-    row = key // n
-    col = (key - row * n).to(torch.int32)
-    del key
+    E = int(edges.shape[0])
+    limit = max(2, int(max_keys))          # directed keys per pass (both directions of <= limit/2 edges)
+    nchunks = max(1, -(-2 * E // limit))
+    counts = torch.zeros(n, dtype=torch.int64, device=dev)
+    cols = []
+    bounds = [c * n // nchunks for c in range(nchunks + 1)]
+    for c in range(nchunks):
+        lo, hi = bounds[c], bounds[c + 1]
+        parts = []
+        for e0 in range(0, E, limit // 2):    # stream the host edge list through the device
+            e = torch.from_numpy(np.ascontiguousarray(edges[e0:e0 + limit // 2])).to(dev)
+            src, dst = e[:, 0].to(torch.int64), e[:, 1].to(torch.int64)
+            del e
+            keep = src != dst
+            src, dst = src[keep], dst[keep]
+            for a, b in ((src, dst), (dst, src)):
+                m = (a >= lo) & (a < hi)
+                if nchunks == 1:
+                    parts.append(a * n + b)
+                else:
+                    parts.append(a[m] * n + b[m])
+            del src, dst, keep
+        key = torch.unique(torch.cat(parts))
+        del parts
+        row = key // n
+        cols.append((key - row * n).to(torch.int32))
+        counts += torch.bincount(row, minlength=n)
+        del key, row
     indptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-    indptr[1:] = torch.cumsum(torch.bincount(row, minlength=n), 0)
-    return indptr, col
+    indptr[1:] = torch.cumsum(counts, 0)
+    return indptr, torch.cat(cols) if len(cols) > 1 else cols[0]
 
 
 def generate_power_law_exact_device(n: int, avg_degree: int, seed: int, train_fraction: float = 0.1,

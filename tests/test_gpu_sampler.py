@@ -185,3 +185,15 @@ def test_exact_generator_device_csr_matches_reference(golden, bgl):
         assert np.array_equal(g.row_offsets, npz[f"off_{i}"]) and np.array_equal(g.col_indices, npz[f"col_{i}"])
         assert np.array_equal(g.train_mask, np.unpackbits(npz[f"train_{i}"])[:int(n)].astype(bool))
         assert np.array_equal(g.labels, npz[f"labels_{i}"].astype(np.int64))
+
+
+def test_device_csr_chunked_by_source_range():
+    """csr_from_edges_device with tiny passes (the papers100M path: CUB sorts
+    < 2^31 keys) equals the single-pass CSR and numpy's csr_from_edges."""
+    from oracle import graph_oracle as go
+    from paper_2112_08541_b200.graph import csr_from_edges_device, power_law_edges
+    edges, _, _ = power_law_edges(5000, 12, 4, 0.1, 3)
+    off, col = go.csr_from_edges(edges.astype(np.int64), 5000)
+    for mk in (1 << 29, 4096, 1000):
+        ip, ix = csr_from_edges_device(edges, 5000, max_keys=mk)
+        assert np.array_equal(ip.cpu().numpy(), off) and np.array_equal(ix.cpu().numpy(), col), mk
