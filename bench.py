@@ -369,25 +369,31 @@ def run_bgl(args, cfg):
         lo, hi = (i % nbl) * b, min((i % nbl + 1) * b, order_host.size)
         return pipe.feed(i, seeds_pinned[lo:hi])   # staged + one H2D copy on a side stream
 
+    # same batch window as `value`: the same W warm-up steps (untimed, from a
+    # cold cache), then the same K timed steps, each bracketed like `value`
     pipe.reset()
     pipe.prime(fed=True, feed=feed)
+    feed(pipe.lookahead)                           # seeds of the batch sampled in the first step
+    for k in range(args.warmup):
+        pipe.step(fed=True)
+        feed(k + 1 + pipe.lookahead)
     torch.cuda.synchronize()
-    n_e2e = max(3, min(args.steps, 100))
+    n_e2e = args.steps
     ce0 = pipe.counters.clone()
     eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_e2e)]
     h2d = 0
     cur = torch.cuda.current_stream()
-    for k in range(n_e2e):
+    for k in range(args.warmup, args.warmup + n_e2e):
         flush.zero_()
-        eev[k][0].record()
-        if k == 0:
-            h2d += feed(pipe.lookahead)            # seeds of the batch sampled in step 0
-        pipe.step(fed=True)                        # waits for its seeds' copy; stores results into pinned host
+        e = eev[k - args.warmup]
+        e[0].record()
+        cur.wait_event(pipe.fed_ready[(k + pipe.lookahead) % len(pipe.fed_ready)])   # this step's seeds are in
+        pipe.step(fed=True)                        # stores the batch's results into pinned host memory
         # the next step's seeds: copied H2D on the side stream while this step runs,
         # and inside this step's timed region (the end event waits for the copy)
         h2d += feed(k + 1 + pipe.lookahead)
         cur.wait_event(pipe.fed_ready[(k + 1 + pipe.lookahead) % len(pipe.fed_ready)])
-        eev[k][1].record()
+        e[1].record()
     torch.cuda.synchronize()
     e2e_ms = [s.elapsed_time(e) for s, e in eev]
     ids_h, cnt_h = pipe.host_result(pipe.last_slot())
