@@ -310,7 +310,7 @@ sample_fused_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
 // ---------------------------------------------------------------- threshold-candidate sampling
 // Same look-back prologue and lane-aligned per-parent stream walk as
 // sample_fused_kernel, but without a running top-k: a draw is a candidate when
-// m < T(k, deg), a per-parent threshold that keeps ~mu = k + 2.5 sqrt(k) + 2
+// m < T(k, deg), a per-parent threshold that keeps ~mu = k + 2 sqrt(k) + 1
 // of the parent's deg draws. Candidates are appended to a per-warp smem list;
 // after the parent's last chunk each candidate's rank is counted by broadcast
 // comparisons and the k smallest are written at their rank. Exact: with
@@ -320,9 +320,9 @@ sample_fused_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
 // L > 64 (rarer still) sends it to sample_heavy_kernel.
 constexpr int kCandCap = 64;
 
-__device__ __forceinline__ uint64_t cand_threshold(int64_t k, int64_t deg) {
+__device__ __forceinline__ uint64_t cand_threshold(int64_t k, int64_t deg, float ma, float mb) {
     if (deg <= k) return 1ull << 53;
-    const double mu = (double)k + 2.5 * sqrt((double)k) + 2.0;
+    const double mu = (double)k + (double)ma * sqrt((double)k) + (double)mb;
     if (mu >= (double)deg) return 1ull << 53;
     return (uint64_t)(mu / (double)deg * 9007199254740992.0);
 }
@@ -334,7 +334,7 @@ sample_cand_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
                    ScanState ss, int64_t* __restrict__ deg_prefix, int64_t* __restrict__ k_prefix,
                    int32_t* __restrict__ heavy, int64_t* __restrict__ heavy_count,
                    int32_t* __restrict__ out_ids, int32_t* __restrict__ out_pidx, int64_t* __restrict__ num_out,
-                   uint32_t* __restrict__ bitmap, int32_t run, int64_t heavy_deg) {
+                   uint32_t* __restrict__ bitmap, int32_t run, int64_t heavy_deg, float ma, float mb) {
     __shared__ uint64_t s_cand[kWarpsPerBlock][kCandCap];
     uint64_t* cand = s_cand[warp_id()];
     const int64_t n = *num_parents_dev;
@@ -386,7 +386,7 @@ sample_cand_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
             draw_base[1] = D0 + pre_d + incl_d;
             *num_out = pre_k + incl_k;
         }
-        const uint64_t Tm = (valid && !hv) ? cand_threshold(k, deg) : 0;
+        const uint64_t Tm = (valid && !hv) ? cand_threshold(k, deg, ma, mb) : 0;
         bool have = false;
         U128 s{0, 0};
         const int cnt = (int)((n - r * run) < run ? (n - r * run) : run);
@@ -630,6 +630,10 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
         return (e && std::string(e) == "fused") ? 0 : 1;
     }();
     const bool use_cand = cand_env && fanout <= 32;
+    // candidate threshold keeps ~k + 2 sqrt(k) + 1 draws per parent (a sweep of
+    // the margin at C2: (1, 1) 4027, (1.5, 1) 4079, (2, 1) 4102, (2.5, 2) 4046,
+    // (3, 3) 4032 b/s with HBM features -- a few % either way)
+    const float mar[2] = {2.0f, 1.0f};
     const int64_t runs = std::max<int64_t>(1, ceil_div(max_parents, run));
     // parents above this degree go to the 8-warp CTA kernel (lower thresholds
     // for the small hops were measured slower: the CTA kernel runs after it)
@@ -642,7 +646,7 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     if (use_cand) {
         sample_cand_kernel<<<blocks, kWarpsPerBlock * 32, 0, st>>>(
             indptr, indices, parents, num_parents_dev, fanout, table, draw_base, ss, w.deg_prefix, w.k_prefix,
-            w.heavy, w.heavy_count, out_ids, out_parent_idx, num_out_dev, bm, (int32_t)run, heavy_deg);
+            w.heavy, w.heavy_count, out_ids, out_parent_idx, num_out_dev, bm, (int32_t)run, heavy_deg, mar[0], mar[1]);
         BGL_TRY(launch_status("sample_cand_kernel"));
     } else {
         sample_fused_kernel<<<blocks, kWarpsPerBlock * 32, 0, st>>>(
