@@ -428,7 +428,7 @@ def run_bgl(args, cfg):
                        "per-step host sync); checked on the host"},
         "gpu_launches": pipe.kernels_per_step * args.steps,
         "clocks": clk.summary(),
-        "setup": dict(setup, hbm_peak_gb=round(torch.cuda.max_memory_allocated() / 1e9, 2)),
+        "setup": dict(setup, torch_alloc_peak_gb=round(torch.cuda.max_memory_allocated() / 1e9, 2)),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import ordering_oracle  # noqa: F401  (the oracle is the checker/baseline only)
@@ -596,7 +596,7 @@ def run_sharded(args, cfg):
         "e2e": {"value": round(world * n_e2e / (float(t.item()) * 1e-3), 2), "unit": UNIT,
                 "h2d_bytes_per_step": int(h2d / n_e2e), "d2h_bytes_per_step": int(d2h / n_e2e)},
         "gpu_launches": launches * args.steps,
-        "clocks": clk.summary(), "setup": dict(setup, hbm_peak_gb=round(torch.cuda.max_memory_allocated() / 1e9, 2)),
+        "clocks": clk.summary(), "setup": dict(setup, torch_alloc_peak_gb=round(torch.cuda.max_memory_allocated() / 1e9, 2)),
     }
     if rank == 0:
         print(json.dumps(out), flush=True)
