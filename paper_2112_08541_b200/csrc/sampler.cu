@@ -70,10 +70,9 @@ static HopWorkspace carve_hop_ws(void* ws, int64_t max_parents) {
     return w;
 }
 
+// fire-and-forget (RED.OR): no dependent load of the word before the atomic
 __device__ __forceinline__ void mark_bit(uint32_t* bitmap, int32_t v) {
-    uint32_t bit = 1u << (v & 31);
-    uint32_t* w = bitmap + (v >> 5);
-    if (!(ld_volatile(w) & bit)) atomicOr(w, bit);
+    atomicOr(bitmap + (v >> 5), 1u << (v & 31));
 }
 
 // ---------------------------------------------------------------- key types

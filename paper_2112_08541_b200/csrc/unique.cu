@@ -80,9 +80,7 @@ __global__ void mark_kernel(const int32_t* __restrict__ keys, Segs s, uint32_t* 
         int64_t pos;
         if (!seg_locate(s, g, &pos)) continue;
         uint32_t v = (uint32_t)keys[pos];
-        uint32_t bit = 1u << (v & 31);
-        uint32_t* w = bitmap + (v >> 5);
-        if (!(ld_volatile(w) & bit)) atomicOr(w, bit);
+        atomicOr(bitmap + (v >> 5), 1u << (v & 31));   // RED: no dependent load
     }
 }
 
