@@ -47,6 +47,14 @@ CONFIGS = {
                cache_frac=0.10, S=4),
 }
 METRIC = "mini-batches/sec (sample+cache+gather)"
+
+
+def workload_text(cfg, features):
+    """The config's workload line, with the feature store's location as run."""
+    w = cfg["workload"]
+    if features == "hbm":
+        w = w.replace("in pinned host memory", "resident in HBM (misses gathered from HBM)")
+    return w
 UNIT = "mini-batches/s"
 GRAPH_SEED, RUN_SEED = 1, 1
 
@@ -409,7 +417,7 @@ def run_bgl(args, cfg):
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32 ids / u53 PCG64 keys / fp32 rows moved",
         "data": graph_data(cfg, args.graph),
-        "config": {"workload": cfg["workload"], "graph": args.graph, "num_nodes": cfg["n"], "csr_entries": dg.num_edges,
+        "config": {"workload": workload_text(cfg, args.features), "graph": args.graph, "num_nodes": cfg["n"], "csr_entries": dg.num_edges,
                    "max_degree": dg.max_degree, "feature_dim": cfg["dim"], "fanouts": list(cfg["fanouts"]),
                    "batch": b, "cache_rows_per_gpu": cap, "features": args.features, "sampler_rng": args.rng,
                    "parallelism": f"replicas{world}" if world > 1 else "single",
@@ -580,7 +588,7 @@ def run_sharded(args, cfg):
         "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int32 ids / u53 PCG64 keys / fp32 rows moved",
         "data": graph_data(cfg, args.graph),
-        "config": {"workload": cfg["workload"], "graph": args.graph, "num_nodes": cfg["n"],
+        "config": {"workload": workload_text(cfg, args.features), "graph": args.graph, "num_nodes": cfg["n"],
                    "csr_entries": dg.num_edges, "feature_dim": cfg["dim"], "fanouts": list(cfg["fanouts"]),
                    "batch": b, "cache_rows_per_gpu": cap, "features": args.features,
                    "parallelism": f"dp{world} + node-ID-sharded FIFO cache (home = v % {world}); " + (
@@ -636,7 +644,7 @@ def run_reference(args, cfg):
         "warmup": args.warmup, "ms_per_step": round(1e3 * r["seconds"] / r["batches"], 2), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64 ids / fp64 priorities / fp32 rows moved",
         "data": graph_data(cfg, args.graph) + " (same graph and features, on the host)", "impl": "reference",
-        "config": {"workload": cfg["workload"], "graph": args.graph, "num_nodes": cfg["n"],
+        "config": {"workload": workload_text(cfg, args.features), "graph": args.graph, "num_nodes": cfg["n"],
                    "csr_entries": int(hg.num_edges),
                    "fanouts": list(cfg["fanouts"]), "batch": cfg["b"]},
         "feature_gbs": round(r["feature_bytes"] / r["seconds"] / 1e9, 3),

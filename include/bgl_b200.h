@@ -71,6 +71,8 @@ int bgl_pcg64_draws(const uint64_t* table, int64_t first, int64_t n, uint64_t* o
  * grouped by parent in parent order. Writes draw_base[1] = draw_base[0] +
  * sum deg (the chain across hops, sampler.py:110-114) and *num_out_dev.
  * fanout <= 4096 (clamp it to the graph's max degree: k = min(fanout, deg)).
+ * out_ids / out_parent_idx may be NULL (nothing stored: a last hop whose
+ * frontier is only needed as marks in the dedup bitmap).
  * mark_bitmap (may be NULL): the dedup workspace of bgl_unique_sorted; every
  * output is also marked there (fused K2 mark), so the later
  * bgl_unique_sorted call only needs the seed segment. max_ctas > 0 caps the

@@ -298,8 +298,8 @@ sample_fused_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
             const int64_t offi = __shfl_sync(0xffffffffu, off, i);
             if (lane < ki) {
                 const int32_t v = indices[offi + key_t(best)];
-                out_ids[oi + lane] = v;
-                out_pidx[oi + lane] = (int32_t)(r * run + i);
+                if (out_ids) out_ids[oi + lane] = v;
+                if (out_pidx) out_pidx[oi + lane] = (int32_t)(r * run + i);
                 if (bitmap) mark_bit(bitmap, v);
             }
         }
@@ -470,15 +470,15 @@ sample_cand_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
                 }
                 if (lane + 32 < L && r1 < ki) {
                     const int32_t v = indices[offi + (int64_t)(c1 & 2047u)];
-                    out_ids[oi + r1] = v;
-                    out_pidx[oi + r1] = (int32_t)gq;
+                    if (out_ids) out_ids[oi + r1] = v;
+                    if (out_pidx) out_pidx[oi + r1] = (int32_t)gq;
                     if (bitmap) mark_bit(bitmap, v);
                 }
             }
             if (lane < L && r0 < ki) {
                 const int32_t v = indices[offi + (int64_t)(c0 & 2047u)];
-                out_ids[oi + r0] = v;
-                out_pidx[oi + r0] = (int32_t)gq;
+                if (out_ids) out_ids[oi + r0] = v;
+                if (out_pidx) out_pidx[oi + r0] = (int32_t)gq;
                 if (bitmap) mark_bit(bitmap, v);
             }
             __syncwarp();
@@ -556,8 +556,8 @@ sample_heavy_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
                     acc = merge_sorted(acc, WideKey{sm[w * 32 + lane], st2[w * 32 + lane]});
                 if (lane < k) {
                     const int32_t v = indices[off + acc.t];
-                    out_ids[o + lane] = v;
-                    out_pidx[o + lane] = (int32_t)q;
+                    if (out_ids) out_ids[o + lane] = v;
+                    if (out_pidx) out_pidx[o + lane] = (int32_t)q;
                     if (bitmap) mark_bit(bitmap, v);
                 }
             }
@@ -583,8 +583,8 @@ sample_heavy_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
         }
         for (int i = threadIdx.x; i < k; i += blockDim.x) {
             const int32_t v = indices[off + st[i]];
-            out_ids[o + i] = v;
-            out_pidx[o + i] = (int32_t)q;
+            if (out_ids) out_ids[o + i] = v;
+            if (out_pidx) out_pidx[o + i] = (int32_t)q;
             if (bitmap) mark_bit(bitmap, v);
         }
         __syncthreads();

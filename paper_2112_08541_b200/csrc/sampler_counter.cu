@@ -141,8 +141,8 @@ sample_counter_kernel(const int64_t* __restrict__ indptr, const int32_t* __restr
 #pragma unroll 4
             for (int64_t t = 0; t < k; ++t) {
                 const int32_t v = indices[off + t];
-                out_ids[o + t] = v;
-                out_pidx[o + t] = (int32_t)q;
+                if (out_ids) out_ids[o + t] = v;
+                if (out_pidx) out_pidx[o + t] = (int32_t)q;
                 if (bitmap) atomicOr(bitmap + (v >> 5), 1u << (v & 31));   // fire-and-forget (RED)
             }
             continue;
@@ -163,8 +163,8 @@ sample_counter_kernel(const int64_t* __restrict__ indptr, const int32_t* __restr
 #pragma unroll 4
         for (int i = 0; i < (int)k; ++i) {
             const int32_t v = indices[off + chosen[i][lane]];
-            out_ids[o + i] = v;
-            out_pidx[o + i] = (int32_t)q;
+            if (out_ids) out_ids[o + i] = v;
+            if (out_pidx) out_pidx[o + i] = (int32_t)q;
             if (bitmap) atomicOr(bitmap + (v >> 5), 1u << (v & 31));
         }
     }
@@ -282,15 +282,15 @@ sample_counter_group_kernel(const int64_t* __restrict__ indptr, const int32_t* _
         if (all) {
             for (int t = sub; t < (int)k; t += G) {
                 const int32_t vv = indices[off + t];
-                out_ids[o + t] = vv;
-                out_pidx[o + t] = (int32_t)q;
+                if (out_ids) out_ids[o + t] = vv;
+                if (out_pidx) out_pidx[o + t] = (int32_t)q;
                 if (bitmap) atomicOr(bitmap + (vv >> 5), 1u << (vv & 31));
             }
         } else if (!excl) {
             if (slot) {
                 const int32_t vv = indices[off + x];
-                out_ids[o + sub] = vv;
-                out_pidx[o + sub] = (int32_t)q;
+                if (out_ids) out_ids[o + sub] = vv;
+                if (out_pidx) out_pidx[o + sub] = (int32_t)q;
                 if (bitmap) atomicOr(bitmap + (vv >> 5), 1u << (vv & 31));
             }
         } else {
@@ -305,8 +305,8 @@ sample_counter_group_kernel(const int64_t* __restrict__ indptr, const int32_t* _
                 if (emit) {
                     const int pos = base + __popc(em & lt);
                     const int32_t vv = indices[off + t];
-                    out_ids[o + pos] = vv;
-                    out_pidx[o + pos] = (int32_t)q;
+                    if (out_ids) out_ids[o + pos] = vv;
+                    if (out_pidx) out_pidx[o + pos] = (int32_t)q;
                     if (bitmap) atomicOr(bitmap + (vv >> 5), 1u << (vv & 31));
                 }
                 base += __popc(em);

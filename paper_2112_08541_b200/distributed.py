@@ -317,7 +317,7 @@ class ShardedPipeline:
         self.order = order.to(device="cuda", dtype=torch.int32).contiguous()
         total = int(self.order.numel())
         self.num_batches = int(num_batches or (total + self.b - 1) // self.b)
-        self.samplers = [BatchSampler(dg, fanouts, self.b, rng=rng) for _ in range(self.NSMP)]
+        self.samplers = [BatchSampler(dg, fanouts, self.b, rng=rng, frontier_outputs=False) for _ in range(self.NSMP)]
         maxu = self.maxu = self.samplers[0].max_uniq
         self.dim = features.shape[1]
         self.engine = FeatureCacheEngine(CacheConfig(device_capacity=shard_capacity, host_capacity=0, num_devices=1,

@@ -65,7 +65,8 @@ class MiniBatchPipeline:
         self.order = order.to(device="cuda", dtype=torch.int32).contiguous()
         total = int(self.order.numel())
         self.num_batches = int(num_batches or (total + self.b - 1) // self.b)
-        self.samplers = [BatchSampler(dg, fanouts, self.b, max_ctas=sampler_ctas, rng=rng) for _ in range(NS)]
+        self.samplers = [BatchSampler(dg, fanouts, self.b, max_ctas=sampler_ctas, rng=rng, frontier_outputs=False)
+                         for _ in range(NS)]
         self.max_uniq = self.samplers[0].max_uniq
         self.engine = FeatureCacheEngine(cache_cfg, features, max_batch=self.max_uniq)
         self.outs = [self.engine.out] + [torch.empty_like(self.engine.out) for _ in range(NB - 1)]

@@ -110,8 +110,13 @@ class BatchSampler:
     `counts[h]` (device int64) holds the live length of segment h.
     """
 
-    def __init__(self, g, fanouts, max_batch: int, relabel: bool = False, max_ctas: int = 0, rng: str = "replay"):
+    def __init__(self, g, fanouts, max_batch: int, relabel: bool = False, max_ctas: int = 0, rng: str = "replay",
+                 frontier_outputs: bool = True):
+        """frontier_outputs=False (pipelines that only need the distinct
+        set): no parent_idx stores, and the last hop only marks the dedup
+        bitmap (its frontier is never read)."""
         self.dg: DeviceGraph = device_graph(g)
+        self.frontier_outputs = bool(frontier_outputs) or relabel
         if rng not in ("replay", "counter"):
             raise ValueError("rng must be 'replay' or 'counter'")
         self.rng = rng
@@ -179,10 +184,16 @@ class BatchSampler:
         cnt = self.counts.data_ptr()
         db = self.draw_base.data_ptr()
         for h in (range(self.H) if hops is None else hops):
+            out_ids = base + self._seg_bytes[h + 1]
+            out_pidx = self.pidx[h].data_ptr()
+            if not self.frontier_outputs:
+                out_pidx = None
+                if h == self.H - 1:
+                    out_ids = None
             if self.rng == "counter":
                 _lib.check(lib.bgl_sample_hop_counter(
                     self.dg.indptr.data_ptr(), self.dg.indices.data_ptr(), base + self._seg_bytes[h], cnt + 8 * h,
-                    self.caps[h], self.eff[h], tptr, h, base + self._seg_bytes[h + 1], self.pidx[h].data_ptr(),
+                    self.caps[h], self.eff[h], tptr, h, out_ids, out_pidx,
                     cnt + 8 * (h + 1), self.hop_ws.data_ptr(), self.uws.data_ptr(), st))
                 if hooks is not None:
                     hooks(h)
@@ -190,7 +201,7 @@ class BatchSampler:
             _lib.check(lib.bgl_sample_hop(
                 self.dg.indptr.data_ptr(), self.dg.indices.data_ptr(),
                 base + self._seg_bytes[h], cnt + 8 * h, self.caps[h], self.eff[h], tptr, db + 8 * h,
-                base + self._seg_bytes[h + 1], self.pidx[h].data_ptr(), cnt + 8 * (h + 1),
+                out_ids, out_pidx, cnt + 8 * (h + 1),
                 self.hop_ws.data_ptr(), self.uws.data_ptr(), self.max_ctas, st))
             if hooks is not None:
                 hooks(h)
