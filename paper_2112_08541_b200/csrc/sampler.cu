@@ -486,6 +486,241 @@ sample_cand_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
     }
 }
 
+// ---------------------------------------------------------------- segmented threshold walk
+// The draws of a run's parents are consecutive in the batch stream, so the
+// warp walks the run's light draws as ONE sequence (lane l takes walk position
+// W + l, chunk after chunk) instead of parent by parent: no per-parent stream
+// hand-off, no half-empty last chunk per parent. Heavy and degree-0 parents
+// have walk length 0; a lane whose next draw lies past a heavy parent's draws
+// jumps its PCG64 state over them (gap[j] = heavy draws before parent j). A
+// draw of parent j is a candidate when m < T_j (as in sample_cand_kernel);
+// candidates are appended in walk order, so each parent's candidates are one
+// contiguous range of the warp's list and a candidate's rank is counted over
+// its own range only. A parent with fewer than k candidates (or whose range
+// overflowed the list) is redone exactly with a warp top-k over all its draws.
+constexpr int kSegCap = 512;
+
+struct SegWarp {
+    uint64_t cand[kSegCap];
+    uint64_t thr[33];    // [32]: sentinel 0 (lanes past the run's draws never pass)
+    int64_t gap[33];
+    int32_t wst[33];
+    int32_t wend[33];    // [32]: sentinel INT_MAX (ends the parent search)
+    int32_t cst[32];
+    uint8_t cj[kSegCap];
+};
+
+// The lane's parent bound / threshold / walk start stay in registers and are
+// reloaded only when the lane crosses into the next parent.
+__device__ __forceinline__ void seg_take(SegWarp& sw, int w, int& j, int& nb, uint64_t& th, int& ws) {
+    if (w >= nb) {
+        do {
+            ++j;
+            nb = sw.wend[j];
+        } while (w >= nb);
+        th = sw.thr[j];
+        ws = sw.wst[j];
+    }
+}
+
+__device__ __forceinline__ void seg_append(SegWarp& sw, bool pass, uint64_t key, int j, int& L, unsigned lt) {
+    const unsigned bm = __ballot_sync(0xffffffffu, pass);
+    if (pass) {
+        const int pos = L + __popc(bm & lt);
+        if (pos < kSegCap) {
+            sw.cand[pos] = key;
+            sw.cj[pos] = (uint8_t)j;
+        }
+    }
+    L += __popc(bm);
+}
+
+// Walk the run's light draws in chunks of 32; returns the candidate count.
+template <bool kGaps>
+__device__ __forceinline__ int seg_walk(SegWarp& sw, const PcgTable T, U128 A32, U128 C32, int64_t d_run,
+                                        int32_t Wtot, int lane, unsigned lt) {
+    int j = 0;
+    while (lane >= sw.wend[j]) ++j;
+    int nb = sw.wend[j], ws = sw.wst[j];
+    uint64_t th = sw.thr[j];
+    int64_t g = kGaps ? sw.gap[j] : 0;
+    U128 s = T.at((uint64_t)(d_run + lane + g + 1));
+    int L = 0;
+    for (int W = 0; W < Wtot; W += 32) {
+        const int w = W + lane;
+        if (w >= nb) {
+            seg_take(sw, w, j, nb, th, ws);
+            if (kGaps) {
+                const int64_t gj = sw.gap[j];
+                if (gj != g && w < Wtot) {          // heavy parents' draws lie between
+                    s = T.adv(s, (uint64_t)(gj - g));
+                    g = gj;
+                }
+            }
+        }
+        // out >> 11 < T  <=>  out < T << 11 (thr holds T << 11; see the sentinel note)
+        const uint64_t out = xsl_rr_fs(s);
+        seg_append(sw, out < th, (out & ~2047ull) | (uint64_t)(w - ws), j, L, lt);
+        s = affine_mad(A32, C32, s);
+    }
+    return L;
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4)
+sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                  const int32_t* __restrict__ parents, const int64_t* __restrict__ num_parents_dev,
+                  int32_t fanout, const uint64_t* __restrict__ table, int64_t* __restrict__ draw_base,
+                  ScanState ss, int64_t* __restrict__ deg_prefix, int64_t* __restrict__ k_prefix,
+                  int32_t* __restrict__ heavy, int64_t* __restrict__ heavy_count,
+                  int32_t* __restrict__ out_ids, int32_t* __restrict__ out_pidx, int64_t* __restrict__ num_out,
+                  uint32_t* __restrict__ bitmap, int32_t run, int64_t heavy_deg, float ma, float mb) {
+    __shared__ SegWarp s_seg[kWarpsPerBlock];
+    SegWarp& sw = s_seg[warp_id()];
+    const int64_t n = *num_parents_dev;
+    const int64_t nruns = n > 0 ? ceil_div(n, run) : 1;
+    const int lane = lane_id();
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned FULL = 0xffffffffu;
+    const PcgTable T{table};
+    const U128 A32 = T.A(5), C32 = T.C(5);
+    const int64_t D0 = draw_base[0];
+    while (true) {
+        int64_t r = 0;
+        if (lane == 0) r = (int64_t)atomicAdd(ss.ticket, 1u);
+        r = __shfl_sync(FULL, r, 0);
+        if (r >= nruns) break;
+        const int64_t q = r * run + lane;
+        const bool valid = lane < run && q < n;
+        const int32_t p = valid ? parents[q] : 0;
+        const int64_t off = valid ? indptr[p] : 0;
+        const int64_t deg = valid ? indptr[p + 1] - off : 0;
+        const int64_t k = deg < fanout ? deg : fanout;
+        const int64_t incl_d = warp_incl_scan(deg);
+        const int64_t incl_k = warp_incl_scan(k);
+        const int64_t agg_d = __shfl_sync(FULL, incl_d, 31);
+        const int64_t agg_k = __shfl_sync(FULL, incl_k, 31);
+        if (lane == 0) {
+            const uint64_t f = r == 0 ? kFlagInc : kFlagAgg;
+            atomicExch((unsigned long long*)(ss.status + r), (unsigned long long)(f | ((uint64_t)agg_d & kValMask)));
+            atomicExch((unsigned long long*)(ss.status + ss.max_tiles + r),
+                       (unsigned long long)(f | ((uint64_t)agg_k & kValMask)));
+        }
+        const int64_t pre_d = warp_lookback1(ss.status, r, agg_d);
+        const int64_t pre_k = warp_lookback1(ss.status + ss.max_tiles, r, agg_k);
+        const int64_t ex_d = pre_d + incl_d - deg;
+        const int64_t ex_k = pre_k + incl_k - k;
+        const bool hv = valid && (k > 32 || deg > heavy_deg);
+        const unsigned hm = __ballot_sync(FULL, hv);
+        if (hm) {
+            int64_t slot = 0;
+            if (lane == 0) slot = (int64_t)atomicAdd((unsigned long long*)heavy_count, (unsigned long long)__popc(hm));
+            slot = __shfl_sync(FULL, slot, 0);
+            if (hv) {
+                heavy[slot + __popc(hm & lt)] = (int32_t)q;
+                deg_prefix[q] = ex_d;
+                k_prefix[q] = ex_k;
+            }
+        }
+        if (r == nruns - 1 && lane == 31) {
+            draw_base[1] = D0 + pre_d + incl_d;
+            *num_out = pre_k + incl_k;
+        }
+        // walk layout of the run's light parents
+        const bool light = valid && !hv && deg > 0;
+        const int32_t ldeg = light ? (int32_t)deg : 0;
+        const int32_t incl_l = warp_incl_scan(ldeg);
+        const int32_t Wtot = __shfl_sync(FULL, incl_l, 31);
+        sw.wst[lane] = incl_l - ldeg;
+        sw.wend[lane] = incl_l;
+        sw.gap[lane] = (incl_d - deg) - (int64_t)(incl_l - ldeg);
+        {   // T << 11; T = 2^53 ("every draw") -> 2^64 - 1, which drops only an
+            // m = 2^53 - 1 draw: the largest possible, so either k others remain
+            // or the parent takes the exact fallback (fewer than k candidates)
+            const uint64_t tm = light ? cand_threshold(k, deg, ma, mb) : 0;
+            sw.thr[lane] = tm >= (1ull << 53) ? ~0ull : tm << 11;
+        }
+        if (lane == 0) {
+            sw.wend[32] = 0x7fffffff;
+            sw.thr[32] = 0;
+            sw.gap[32] = 0;
+            sw.wst[32] = 0;
+        }
+        __syncwarp();
+        int L = 0;
+        if (Wtot > 0) L = hm ? seg_walk<true>(sw, T, A32, C32, D0 + pre_d, Wtot, lane, lt)
+                             : seg_walk<false>(sw, T, A32, C32, D0 + pre_d, Wtot, lane, lt);
+        __syncwarp();
+        // each parent's candidates are one range of the (parent-ordered) list
+        const int Ls = L < kSegCap ? L : kSegCap;
+        int lo = 0, hi = Ls;                    // first index with cj >= lane
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if ((int)sw.cj[mid] < lane) lo = mid + 1; else hi = mid;
+        }
+        const int c_st = lo;
+        const int c_end = __shfl_down_sync(FULL, c_st, 1);
+        const int c_own = lane < 31 ? c_end - c_st : Ls - c_st;
+        // a range touching the list's end is incomplete when the list overflowed
+        const bool cut = L > kSegCap && c_st + c_own >= Ls;
+        sw.cst[lane] = c_st;
+        const bool fb = light && (c_own < (int)k || cut);
+        __syncwarp();
+        for (int b0 = 0; b0 < Ls; b0 += 32) {
+            const int i = b0 + lane;
+            const bool has = i < Ls;
+            const uint64_t key = has ? sw.cand[i] : ~0ull;
+            const int j = has ? (int)sw.cj[i] : 0;
+            const int kj = __shfl_sync(FULL, (int)k, j);
+            const int64_t offj = __shfl_sync(FULL, off, j);
+            const int64_t oij = __shfl_sync(FULL, ex_k, j);
+            const bool fbj = __shfl_sync(FULL, (int)fb, j) != 0;
+            const int e = __shfl_sync(FULL, c_st + c_own, j);
+            if (has && !fbj) {
+                const int st = sw.cst[j];
+                int rk = 0;
+                for (int x = st; x < e; ++x) rk += sw.cand[x] < key;
+                if (rk < kj) {
+                    const int32_t v = indices[offj + (int64_t)(key & 2047u)];
+                    if (out_ids) out_ids[oij + rk] = v;
+                    if (out_pidx) out_pidx[oij + rk] = (int32_t)(r * run + j);
+                    if (bitmap) mark_bit(bitmap, v);
+                }
+            }
+        }
+        // fallback: exact warp top-k over all of the parent's draws
+        unsigned fm = __ballot_sync(FULL, fb);
+        while (fm) {
+            const int i = __ffs(fm) - 1;
+            fm &= fm - 1;
+            const int64_t dg = __shfl_sync(FULL, deg, i);
+            const int ki = __shfl_sync(FULL, (int)k, i);
+            U128 s = T.at((uint64_t)(D0 + __shfl_sync(FULL, ex_d, i) + lane + 1));
+            uint64_t best = ~0ull, kth = ~0ull;
+            const int nc = (int)((dg + 31) >> 5);
+            for (int c = 0; c < nc; ++c) {
+                if (c > 0) s = affine(A32, C32, s);
+                const int t = (c << 5) + lane;
+                const uint64_t cand = t < dg ? ((draw_of_state(s) << 11) | (uint64_t)t) : ~0ull;
+                if (c == 0) {
+                    best = warp_bitonic_sort(cand);
+                    kth = shfl(best, ki - 1);
+                } else {
+                    fold_chunk(best, kth, cand, ki);
+                }
+            }
+            const int64_t oi = __shfl_sync(FULL, ex_k, i);
+            const int64_t offi = __shfl_sync(FULL, off, i);
+            if (lane < ki) {
+                const int32_t v = indices[offi + key_t(best)];
+                if (out_ids) out_ids[oi + lane] = v;
+                if (out_pidx) out_pidx[oi + lane] = (int32_t)(r * run + i);
+                if (bitmap) mark_bit(bitmap, v);
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // ---------------------------------------------------------------- heavy parents
 constexpr int kHeavyThreads = 256;
 constexpr int kHeavyWarps = kHeavyThreads / 32;
@@ -623,16 +858,24 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     const int64_t want_runs = (int64_t)kNumSMs * 48 * 2;
     int64_t run = ceil_div(std::max<int64_t>(max_parents, 1), want_runs);
     run = std::min<int64_t>(std::max<int64_t>(run, 1), kRun);
-    // threshold-candidate kernel for fanout <= 32 (BGL_SAMPLER=fused: running top-k kernel)
-    static const int cand_env = [] {
+    // fanout <= 32: segmented threshold walk (default), BGL_SAMPLER=cand the
+    // per-parent threshold kernel, =fused the running top-k kernel (A/B)
+    static const int mode_env = [] {
         const char* e = getenv("BGL_SAMPLER");
-        return (e && std::string(e) == "fused") ? 0 : 1;
+        if (e && std::string(e) == "fused") return 0;
+        if (e && std::string(e) == "cand") return 1;
+        return 2;
     }();
-    const bool use_cand = cand_env && fanout <= 32;
+    const int mode = fanout <= 32 ? mode_env : 0;
     // candidate threshold keeps ~k + 2 sqrt(k) + 1 draws per parent (a sweep of
     // the margin at C2: (1, 1) 4027, (1.5, 1) 4079, (2, 1) 4102, (2.5, 2) 4046,
     // (3, 3) 4032 b/s with HBM features -- a few % either way)
     const float mar[2] = {2.0f, 1.0f};
+    if (mode == 2) {   // a run's expected candidates stay well inside the warp's list
+        const double mu = fanout + mar[0] * std::sqrt((double)fanout) + mar[1];
+        const int64_t rmax = std::max<int64_t>(1, (int64_t)(kSegCap / (1.5 * mu)));
+        run = std::min<int64_t>(run, rmax);
+    }
     const int64_t runs = std::max<int64_t>(1, ceil_div(max_parents, run));
     // parents above this degree go to the 8-warp CTA kernel (lower thresholds
     // for the small hops were measured slower: the CTA kernel runs after it)
@@ -642,7 +885,12 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     const unsigned cap_blocks = (unsigned)kNumSMs * 8;
     if (blocks > cap_blocks) blocks = cap_blocks;               // runs are claimed dynamically
     if (max_ctas > 0 && blocks > (unsigned)max_ctas) blocks = (unsigned)max_ctas;
-    if (use_cand) {
+    if (mode == 2) {
+        sample_seg_kernel<<<blocks, kWarpsPerBlock * 32, 0, st>>>(
+            indptr, indices, parents, num_parents_dev, fanout, table, draw_base, ss, w.deg_prefix, w.k_prefix,
+            w.heavy, w.heavy_count, out_ids, out_parent_idx, num_out_dev, bm, (int32_t)run, heavy_deg, mar[0], mar[1]);
+        BGL_TRY(launch_status("sample_seg_kernel"));
+    } else if (mode == 1) {
         sample_cand_kernel<<<blocks, kWarpsPerBlock * 32, 0, st>>>(
             indptr, indices, parents, num_parents_dev, fanout, table, draw_base, ss, w.deg_prefix, w.k_prefix,
             w.heavy, w.heavy_count, out_ids, out_parent_idx, num_out_dev, bm, (int32_t)run, heavy_deg, mar[0], mar[1]);
