@@ -855,7 +855,14 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     uint32_t* bm = reinterpret_cast<uint32_t*>(mark_bitmap);
     // fused scan + sample over runs of `run` parents: short runs when the hop is
     // small (enough warps for hop 1), up to kRun (one per lane) when it is large
-    const int64_t want_runs = (int64_t)kNumSMs * 48 * 2;
+    // ~32 runs per SM (one per resident warp): longer runs amortise the
+    // look-back and the run's PCG64 jump (C2 HBM sweep with sample_seg: 96 ->
+    // 4405, 64 -> 4586, 48 -> 4857, 32 -> 4975, 16 -> 4958, 8 -> 4837 b/s)
+    static const int64_t runs_per_sm = [] {
+        const char* e = getenv("BGL_RUNS_PER_SM");
+        return (int64_t)(e ? atoi(e) : 32);
+    }();
+    const int64_t want_runs = (int64_t)kNumSMs * runs_per_sm;
     int64_t run = ceil_div(std::max<int64_t>(max_parents, 1), want_runs);
     run = std::min<int64_t>(std::max<int64_t>(run, 1), kRun);
     // fanout <= 32: segmented threshold walk (default), BGL_SAMPLER=cand the
