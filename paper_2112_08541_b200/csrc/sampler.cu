@@ -523,11 +523,12 @@ __device__ __forceinline__ void seg_take(SegWarp& sw, int w, int& j, int& nb, ui
     }
 }
 
-__device__ __forceinline__ void seg_append(SegWarp& sw, bool pass, uint64_t key, int j, int& L, unsigned lt) {
+__device__ __forceinline__ void seg_append(SegWarp& sw, bool pass, uint64_t key, int j, int& L, unsigned lt,
+                                           int cap) {
     const unsigned bm = __ballot_sync(0xffffffffu, pass);
     if (pass) {
         const int pos = L + __popc(bm & lt);
-        if (pos < kSegCap) {
+        if (pos < cap) {
             sw.cand[pos] = key;
             sw.cj[pos] = (uint8_t)j;
         }
@@ -538,7 +539,7 @@ __device__ __forceinline__ void seg_append(SegWarp& sw, bool pass, uint64_t key,
 // Walk the run's light draws in chunks of 32; returns the candidate count.
 template <bool kGaps>
 __device__ __forceinline__ int seg_walk(SegWarp& sw, const PcgTable T, U128 A32, U128 C32, int64_t d_run,
-                                        int32_t Wtot, int lane, unsigned lt) {
+                                        int32_t Wtot, int lane, unsigned lt, int cap) {
     int j = 0;
     while (lane >= sw.wend[j]) ++j;
     int nb = sw.wend[j], ws = sw.wst[j];
@@ -560,7 +561,7 @@ __device__ __forceinline__ int seg_walk(SegWarp& sw, const PcgTable T, U128 A32,
         }
         // out >> 11 < T  <=>  out < T << 11 (thr holds T << 11; see the sentinel note)
         const uint64_t out = xsl_rr_fs(s);
-        seg_append(sw, out < th, (out & ~2047ull) | (uint64_t)(w - ws), j, L, lt);
+        seg_append(sw, out < th, (out & ~2047ull) | (uint64_t)(w - ws), j, L, lt, cap);
         s = affine_mad(A32, C32, s);
     }
     return L;
@@ -573,7 +574,7 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
                   ScanState ss, int64_t* __restrict__ deg_prefix, int64_t* __restrict__ k_prefix,
                   int32_t* __restrict__ heavy, int64_t* __restrict__ heavy_count,
                   int32_t* __restrict__ out_ids, int32_t* __restrict__ out_pidx, int64_t* __restrict__ num_out,
-                  uint32_t* __restrict__ bitmap, int32_t run, int64_t heavy_deg, float ma, float mb) {
+                  uint32_t* __restrict__ bitmap, int32_t run, int64_t heavy_deg, float ma, float mb, int cap) {
     __shared__ SegWarp s_seg[kWarpsPerBlock];
     SegWarp& sw = s_seg[warp_id()];
     const int64_t n = *num_parents_dev;
@@ -647,11 +648,11 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
         }
         __syncwarp();
         int L = 0;
-        if (Wtot > 0) L = hm ? seg_walk<true>(sw, T, A32, C32, D0 + pre_d, Wtot, lane, lt)
-                             : seg_walk<false>(sw, T, A32, C32, D0 + pre_d, Wtot, lane, lt);
+        if (Wtot > 0) L = hm ? seg_walk<true>(sw, T, A32, C32, D0 + pre_d, Wtot, lane, lt, cap)
+                             : seg_walk<false>(sw, T, A32, C32, D0 + pre_d, Wtot, lane, lt, cap);
         __syncwarp();
         // each parent's candidates are one range of the (parent-ordered) list
-        const int Ls = L < kSegCap ? L : kSegCap;
+        const int Ls = L < cap ? L : cap;
         int lo = 0, hi = Ls;                    // first index with cj >= lane
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
@@ -661,7 +662,7 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
         const int c_end = __shfl_down_sync(FULL, c_st, 1);
         const int c_own = lane < 31 ? c_end - c_st : Ls - c_st;
         // a range touching the list's end is incomplete when the list overflowed
-        const bool cut = L > kSegCap && c_st + c_own >= Ls;
+        const bool cut = L > cap && c_st + c_own >= Ls;
         sw.cst[lane] = c_st;
         const bool fb = light && (c_own < (int)k || cut);
         __syncwarp();
@@ -878,7 +879,13 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     // the margin at C2: (1, 1) 4027, (1.5, 1) 4079, (2, 1) 4102, (2.5, 2) 4046,
     // (3, 3) 4032 b/s with HBM features -- a few % either way)
     const float mar[2] = {2.0f, 1.0f};
-    if (mode == 2) {   // a run's expected candidates stay well inside the warp's list
+    // candidate list length per warp (BGL_SEG_CAP < 512: tests force overflow)
+    static const int seg_cap = [] {
+        const char* e = getenv("BGL_SEG_CAP");
+        const int c = e ? atoi(e) : kSegCap;
+        return c < 1 ? 1 : (c > kSegCap ? kSegCap : c);
+    }();
+    if (mode == 2 && seg_cap == kSegCap) {   // a run's expected candidates stay well inside the list
         const double mu = fanout + mar[0] * std::sqrt((double)fanout) + mar[1];
         const int64_t rmax = std::max<int64_t>(1, (int64_t)(kSegCap / (1.5 * mu)));
         run = std::min<int64_t>(run, rmax);
@@ -895,7 +902,8 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     if (mode == 2) {
         sample_seg_kernel<<<blocks, kWarpsPerBlock * 32, 0, st>>>(
             indptr, indices, parents, num_parents_dev, fanout, table, draw_base, ss, w.deg_prefix, w.k_prefix,
-            w.heavy, w.heavy_count, out_ids, out_parent_idx, num_out_dev, bm, (int32_t)run, heavy_deg, mar[0], mar[1]);
+            w.heavy, w.heavy_count, out_ids, out_parent_idx, num_out_dev, bm, (int32_t)run, heavy_deg, mar[0], mar[1],
+            seg_cap);
         BGL_TRY(launch_status("sample_seg_kernel"));
     } else if (mode == 1) {
         sample_cand_kernel<<<blocks, kWarpsPerBlock * 32, 0, st>>>(

@@ -1,0 +1,39 @@
+"""GPU parity for the sampler's rare paths: hubs mixed into long runs (heavy
+gaps), candidate-list overflow and the exact top-k fallback (forced with a
+tiny list), and the A/B kernels (BGL_SAMPLER=cand|fused) — all bit-exact
+against the oracle on the same hub graph."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+import sampler_paths
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def ref_path(tmp_path_factory):
+    path = str(tmp_path_factory.mktemp("sampler_paths") / "expected.npz")
+    sampler_paths.expected(path)
+    return path
+
+
+def test_hubs_inside_long_runs(ref_path):
+    sampler_paths.check(ref_path)
+
+
+@pytest.mark.parametrize("env", [
+    {"BGL_SEG_CAP": "24", "BGL_RUNS_PER_SM": "1"},     # every run 32 parents, lists overflow
+    {"BGL_SEG_CAP": "1"},                              # almost every parent takes the fallback
+    {"BGL_SAMPLER": "cand"},
+    {"BGL_SAMPLER": "fused", "BGL_RUNS_PER_SM": "2"},
+])
+def test_rare_paths_under_env(env, ref_path):
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, os.path.join(HERE, "sampler_paths.py"), ref_path], env=e,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-4000:]
