@@ -540,6 +540,7 @@ def run_sharded(args, cfg):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     q, own, peer, hst = (int(x) for x in d[:4].tolist())
+    roof = sharded_roofline(args, pipe if args.exchange == "push" else None, feats, rb, flush)
     # e2e: every round the next round's seeds go H2D from pinned host (on the
     # sampling stream, ahead of the sampler) and the round's distinct IDs (the
     # AccessTrace row) + counters are stored into pinned host memory
@@ -603,6 +604,7 @@ def run_sharded(args, cfg):
         "peer_hit_pct": round(100.0 * peer / max(q, 1), 2),
         "e2e": {"value": round(world * n_e2e / (float(t.item()) * 1e-3), 2), "unit": UNIT,
                 "h2d_bytes_per_step": int(h2d / n_e2e), "d2h_bytes_per_step": int(d2h / n_e2e)},
+        "roofline": roof,
         "gpu_launches": launches * args.steps,
         "clocks": clk.summary(), "setup": dict(setup, torch_alloc_peak_gb=round(torch.cuda.max_memory_allocated() / 1e9, 2)),
     }
@@ -611,6 +613,60 @@ def run_sharded(args, cfg):
     if args.exchange == "push":
         pipe.close()
     dist.destroy_process_group()
+
+
+def sharded_roofline(args, pipe, feats, rb, flush, R=8):
+    """Roofline of the sharded engine's dominant kernel, the homes' miss gather
+    (bgl_gather_list over the rows this rank's shard misses, for every worker):
+    R eager steps after the timed region, events on the miss stream around the
+    gathers, rows read from the step's miss counts; max over ranks of the time."""
+    import torch
+    import torch.distributed as dist
+    if pipe is None:
+        return {"bound": "host_link" if args.features == "host" else "hbm", "achieved": None, "peak": None,
+                "unit": "GB/s", "frac": None, "traffic": None,
+                "kernel": "n/a for the NCCL all-to-all baseline (--exchange nccl)"}
+    pipe.miss_timing = []
+    rows = []
+    for _ in range(R):
+        r = (pipe.k + 1) % pipe.NR               # step k gathers the misses of round k + 1
+        flush.zero_()
+        pipe.step_eager()
+        torch.cuda.synchronize()
+        rows.append(int(pipe.miss_cnt[r].sum().item()))
+    ev = pipe.miss_timing
+    pipe.miss_timing = None
+    ms = sum(a.elapsed_time(b) for a, b, _ in ev)
+    t = torch.tensor([ms, float(sum(rows))], dtype=torch.float64, device="cuda")
+    tmax = t[:1].clone()
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    tot = t[1:].clone()
+    dist.all_reduce(tot)
+    world = dist.get_world_size()
+    # per rank and launch set: bytes this rank's gathers moved / their time (the slowest rank's)
+    per_rank_bytes = float(tot.item()) / world * rb
+    if args.features == "host":
+        peak_samples = [host_link_peak_gbs()]
+        try:
+            peak_samples.append(host_link_zero_copy_peak_gbs(feats, rb))
+        except Exception:  # noqa: BLE001 -- a shared store without .shape: memcpy sample only
+            pass
+        peak = max(peak_samples)
+        achieved = per_rank_bytes / (float(tmax.item()) / 1e3) / 1e9
+        return {"bound": "host_link", "achieved": round(achieved, 2), "peak": round(peak, 2), "unit": "GB/s",
+                "frac": round(achieved / peak, 3), "traffic": None,
+                "kernel": "gather_list_kernel (homes' misses, zero-copy host reads, rows pushed to the workers)",
+                "algorithmic_bytes_per_launch": int(per_rank_bytes / R),
+                "peak_source": f"per-rank host link: max of a pinned 256 MB cudaMemcpy and a sequential zero-copy "
+                               f"read of the feature store ({[round(x, 2) for x in peak_samples]}); "
+                               f"{R} eager steps after the timed region, max over ranks"}
+    hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    achieved = 2 * per_rank_bytes / (float(tmax.item()) / 1e3) / 1e9
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(achieved / hbm, 3), "traffic": None,
+            "kernel": "gather_list_kernel (homes' misses from HBM, read + write)",
+            "algorithmic_bytes_per_launch": int(2 * per_rank_bytes / R)}
 
 
 def run_reference(args, cfg):

@@ -364,15 +364,12 @@ class ShardedPipeline:
         self.s_sample = torch.cuda.Stream(priority=-1)      # sampling: high priority (pipeline.py)
         self.s_li, self.s_miss, self.s_back = (torch.cuda.Stream() for _ in range(3))
         self.s_result = torch.cuda.Stream()
-        self.sampled = [torch.cuda.Event() for _ in range(self.NSMP)]
-        self.parted = [torch.cuda.Event() for _ in range(self.NSMP)]
         self.reported = [torch.cuda.Event() for _ in range(self.NSMP)]   # result hand-off read the sampler
-        self.xdone = [torch.cuda.Event() for _ in range(R)]
-        self.li_done = [[torch.cuda.Event() for _ in range(W)] for _ in range(R)]
-        self.miss_done = [[torch.cuda.Event() for _ in range(W)] for _ in range(R)]
+        self._step_events()
         self.k = 0
         self.primed = False
         self._in_graph = False
+        self.miss_timing = None      # list -> _M records (start, end, round set) events (eager steps)
         self.graphs: dict = {}
         # per round (our kernels; the two NCCL barrier kernels not counted): stage + hops (sample + heavy)
         # + dedup (mark, emit, reset); partition (count, scan, push); per bucket: lookup, insert (2),
@@ -442,8 +439,14 @@ class ShardedPipeline:
         r, maxu, rb, eng = j % self.NR, self.maxu, self.rb, self.engine
         ctas = 0 if eng.features.is_cuda else eng.miss_ctas
         lib = _lib.load()
+        timing = self.miss_timing is not None and not self._in_graph
         with torch.cuda.stream(self.s_miss):
             st = _lib.stream_ptr(self.s_miss)
+            if timing:   # measurement pass (bench roofline): the gathers alone between two events
+                for w in range(self.world):
+                    self.s_miss.wait_event(self.li_done[r][w])
+                ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), r)
+                ev[0].record(self.s_miss)
             for w in range(self.world):
                 if not self._in_graph:
                     self.s_miss.wait_event(self.li_done[r][w])
@@ -453,6 +456,9 @@ class ShardedPipeline:
                                                self.worker_rows[w] + r * maxu * rb, self.recv_pos[r, w].data_ptr(),
                                                eng.miss_rows_in_flight, ctas, st))
                 self.miss_done[r][w].record(self.s_miss)
+            if timing:
+                ev[1].record(self.s_miss)
+                self.miss_timing.append(ev)
 
     def _B(self, j: int) -> None:
         r, maxu, rb, eng = j % self.NR, self.maxu, self.rb, self.engine
@@ -510,6 +516,7 @@ class ShardedPipeline:
         torch.cuda.synchronize()
         saved = self.batch_counter.clone()
         self._in_graph = True
+        self._events_captured = True
         try:
             for phase in range(self.PHASES):
                 g = torch.cuda.CUDAGraph()
@@ -538,6 +545,29 @@ class ShardedPipeline:
             main.wait_stream(self.s_result)     # result hand-offs outside the graphs (store_result)
             main.wait_stream(self.s_sample)     # e.g. host seeds copied on the sampling stream
             g.replay()
+        self.k += 1
+
+    def _step_events(self) -> None:
+        """Cross-step events of the eager path (fresh ones after a capture:
+        events recorded while capturing belong to the graphs)."""
+        R, W = self.NR, self.world
+        self.sampled = [torch.cuda.Event() for _ in range(self.NSMP)]
+        self.parted = [torch.cuda.Event() for _ in range(self.NSMP)]
+        self.xdone = [torch.cuda.Event() for _ in range(R)]
+        self.li_done = [[torch.cuda.Event() for _ in range(W)] for _ in range(R)]
+        self.miss_done = [[torch.cuda.Event() for _ in range(W)] for _ in range(R)]
+        self._events_captured = False
+
+    def step_eager(self) -> None:
+        """step() without the captured graphs (measurement passes); ordered
+        after earlier graph replays by the fork from the current stream."""
+        if self._events_captured:
+            self._step_events()
+        self.prime()
+        main = torch.cuda.current_stream()
+        main.wait_stream(self.s_result)
+        main.wait_stream(self.s_sample)
+        self._step_body(self.k)
         self.k += 1
 
     def store_result(self, j: int, host_ids_dev: int, host_meta_dev: int) -> None:
