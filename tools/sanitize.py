@@ -33,6 +33,12 @@ for rng in ("replay", "counter"):
         for _ in range(3):
             pipe.step_eager()
         torch.cuda.synchronize()
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import sampler_paths  # noqa: E402
+
+g_hub, seeds_hub = sampler_paths.inputs(num_seeds=600)     # hub parents inside runs (heavy gaps, CTA kernel)
+for f in ((5, 5), (32,)):
+    bgl.sample_batch(g_hub, seeds_hub, bgl.SamplingConfig(fanouts=f, seed=9), batch_seed=3)
 bgl.sampler.sample_batch_relabelled(hg, hg.train_nodes()[:64], bgl.SamplingConfig(fanouts=(5, 3), seed=1))
 sched = bgl.proximity_schedule(hg, 2, 100, seed=1)
 trace, _ = bgl.simulate_epoch(hg, None, sched, bgl.SamplingConfig(fanouts=(4, 2), seed=1))
