@@ -120,6 +120,14 @@ layouts["first_touch_epoch0"] = first_touch_layout(ep0)
 layouts["first_touch_epoch1"] = first_touch_layout(ep1)     # oracle placement (upper bound)
 rng = np.random.default_rng(0)
 layouts["random"] = rng.permutation(n)
+def pages(pos, misses, pg):
+    """mean distinct pg-byte pages touched per batch by the miss rows."""
+    return float(np.mean([np.unique(pos[m] * rb // pg).size for m in misses]))
+
+
+for name, pos in layouts.items():
+    print(f"{name:20s} pages/batch epoch1: 4K {pages(pos, miss1, 4096):.0f}  64K {pages(pos, miss1, 65536):.0f}  "
+          f"2M {pages(pos, miss1, 2 << 20):.0f}", flush=True)
 for name, pos in layouts.items():
     for g in (32, 64, 128):
         a0, r0 = cost(pos, miss0, g)
