@@ -41,6 +41,11 @@ CONFIGS = {
                         "FIFO cache 10% of nodes (11.1M rows) in HBM, proximity (BFS, S=4) ordering; 1 GPU",
                n=111_059_956, avg_degree=29, dim=128, labels=172, train=0.0108, fanouts=(15, 10, 5), b=1024,
                cache_frac=0.10, S=4),
+    "c5": dict(workload="1B-edge power-law graph (64M nodes, ~1B undirected edges, ~2B CSR entries), 128-d fp32 "
+                        "features (32.8 GB) in pinned host memory, fanout [15,10,5], batch 1024, FIFO cache 10% of "
+                        "nodes in HBM, proximity (BFS, S=4) ordering; 1 GPU",
+               n=64_000_000, avg_degree=31, dim=128, labels=64, train=0.01, fanouts=(15, 10, 5), b=1024,
+               cache_frac=0.10, S=4),
     "c1": dict(workload="synthetic power-law graph 100K nodes / 1M edges, 128-d fp32 features in pinned host "
                         "memory, fanout [10,5], batch 1024, FIFO cache 10% of nodes, BFS ordering",
                n=100_000, avg_degree=20, dim=128, labels=64, train=0.10, fanouts=(10, 5), b=1024,
@@ -49,11 +54,14 @@ CONFIGS = {
 METRIC = "mini-batches/sec (sample+cache+gather)"
 
 
-def workload_text(cfg, features):
-    """The config's workload line, with the feature store's location as run."""
+def workload_text(cfg, features, order="proximity"):
+    """The config's workload line, with the feature store's location and the
+    batch ordering as run."""
     w = cfg["workload"]
     if features == "hbm":
         w = w.replace("in pinned host memory", "resident in HBM (misses gathered from HBM)")
+    if order == "random":
+        w = w.replace("proximity (BFS, S=4) ordering", "random-shuffle ordering (gnnio random_shuffle_schedule)")
     return w
 UNIT = "mini-batches/s"
 GRAPH_SEED, RUN_SEED = 1, 1
@@ -133,7 +141,7 @@ def graph_data(cfg, kind: str) -> str:
     return "synthetic (GPU continuum-limit power-law generator, seed 1; hashed fp32 features)"
 
 
-def build_inputs(cfg, features_where: str, graph_kind: str = "exact", shared=None):
+def build_inputs(cfg, features_where: str, graph_kind: str = "exact", shared=None, order_kind: str = "proximity"):
     """shared = (local_rank, local_world, barrier): host features in ONE
     /dev/shm store registered by every GPU process of the box."""
     import torch
@@ -152,7 +160,12 @@ def build_inputs(cfg, features_where: str, graph_kind: str = "exact", shared=Non
                                    device_resident=(features_where == "hbm"))
     torch.cuda.synchronize()
     t2 = time.time()
-    order, _ = proximity_schedule_device(dg, cfg["S"], cfg["b"], seed=RUN_SEED)
+    if order_kind == "random":      # gnnio ordering.random_shuffle_schedule(g, b, seed): one permutation
+        from paper_2112_08541_b200.ordering import _train_ids
+        perm = np.random.default_rng(RUN_SEED).permutation(_train_ids(dg))
+        order = torch.from_numpy(perm.astype(np.int32)).cuda()
+    else:
+        order, _ = proximity_schedule_device(dg, cfg["S"], cfg["b"], seed=RUN_SEED)
     torch.cuda.synchronize()
     t3 = time.time()
     return dg, feats, order, {"graph_gen_s": round(t1 - t0, 3), "features_gen_s": round(t2 - t1, 3),
@@ -252,7 +265,7 @@ def run_bgl(args, cfg):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     peak_first = host_link_peak_gbs()           # before the feature store is pinned
-    dg, feats, order, setup = build_inputs(cfg, args.features, args.graph)
+    dg, feats, order, setup = build_inputs(cfg, args.features, args.graph, order_kind=args.order)
     b = cfg["b"]
     cap = int(cfg["cache_frac"] * cfg["n"]) // world
     rb = cfg["dim"] * 4
@@ -417,9 +430,10 @@ def run_bgl(args, cfg):
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32 ids / u53 PCG64 keys / fp32 rows moved",
         "data": graph_data(cfg, args.graph),
-        "config": {"workload": workload_text(cfg, args.features), "graph": args.graph, "num_nodes": cfg["n"], "csr_entries": dg.num_edges,
+        "config": {"workload": workload_text(cfg, args.features, args.order), "graph": args.graph, "num_nodes": cfg["n"], "csr_entries": dg.num_edges,
                    "max_degree": dg.max_degree, "feature_dim": cfg["dim"], "fanouts": list(cfg["fanouts"]),
                    "batch": b, "cache_rows_per_gpu": cap, "features": args.features, "sampler_rng": args.rng,
+                   "ordering": args.order,
                    "parallelism": f"replicas{world}" if world > 1 else "single",
                    "l2": "flushed between timed steps (256 MB write, outside the events)",
                    "batches_per_epoch": nb_total},
@@ -477,7 +491,7 @@ def run_sharded(args, cfg):
     torch.cuda.set_device(local_rank)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
-    dg, feats, order, setup = build_inputs(cfg, args.features, args.graph,
+    dg, feats, order, setup = build_inputs(cfg, args.features, args.graph, order_kind=args.order,
                                            shared=(local_rank, local_world, dist.barrier) if world > 1 else None)
     b, rb, dim = cfg["b"], cfg["dim"] * 4, cfg["dim"]
     cap = int(cfg["cache_frac"] * cfg["n"]) // world
@@ -589,7 +603,7 @@ def run_sharded(args, cfg):
         "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int32 ids / u53 PCG64 keys / fp32 rows moved",
         "data": graph_data(cfg, args.graph),
-        "config": {"workload": workload_text(cfg, args.features), "graph": args.graph, "num_nodes": cfg["n"],
+        "config": {"workload": workload_text(cfg, args.features, args.order), "graph": args.graph, "num_nodes": cfg["n"],
                    "csr_entries": dg.num_edges, "feature_dim": cfg["dim"], "fanouts": list(cfg["fanouts"]),
                    "batch": b, "cache_rows_per_gpu": cap, "features": args.features,
                    "parallelism": f"dp{world} + node-ID-sharded FIFO cache (home = v % {world}); " + (
@@ -598,7 +612,7 @@ def run_sharded(args, cfg):
                        if args.exchange == "push" else "IDs and rows by NCCL all-to-all (host-synchronised)"),
                    "l2": "flushed between timed steps (256 MB write, outside the events)",
                    "step": f"one round = {world} mini-batches (one per GPU)", "cuda_graphs": graphs,
-                   "sampler_rng": args.rng},
+                   "sampler_rng": args.rng, "ordering": args.order},
         "feature_gbs": round(q * rb / (total_ms * 1e-3) / 1e9, 2),
         "hit_pct": round(100.0 * (own + peer + hst) / max(q, 1), 2),
         "peer_hit_pct": round(100.0 * peer / max(q, 1), 2),
@@ -700,7 +714,7 @@ def run_reference(args, cfg):
         "warmup": args.warmup, "ms_per_step": round(1e3 * r["seconds"] / r["batches"], 2), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64 ids / fp64 priorities / fp32 rows moved",
         "data": graph_data(cfg, args.graph) + " (same graph and features, on the host)", "impl": "reference",
-        "config": {"workload": workload_text(cfg, args.features), "graph": args.graph, "num_nodes": cfg["n"],
+        "config": {"workload": workload_text(cfg, args.features, args.order), "graph": args.graph, "num_nodes": cfg["n"],
                    "csr_entries": int(hg.num_edges),
                    "fanouts": list(cfg["fanouts"]), "batch": cfg["b"]},
         "feature_gbs": round(r["feature_bytes"] / r["seconds"] / 1e9, 3),
@@ -725,6 +739,8 @@ def main():
                     help="exact: the reference generator's own graph (default for c1/c2); continuum: GPU model (c3)")
     ap.add_argument("--rng", choices=["replay", "counter"], default="replay",
                     help="replay: the reference's numpy stream bit for bit (default); counter: Philox + Floyd")
+    ap.add_argument("--order", choices=["proximity", "random"], default="proximity",
+                    help="batch ordering: proximity_schedule (BGL, default) or random_shuffle_schedule")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="sharded engine: eager steps (no CUDA graphs)")
     ap.add_argument("--sharded", action="store_true", help="use the multi-GPU sharded engine even at N=1")
@@ -735,7 +751,7 @@ def main():
         args.warmup = 3
     cfg = CONFIGS[args.config]
     if args.graph is None:
-        args.graph = "continuum" if args.config == "c3" else "exact"
+        args.graph = "continuum" if args.config in ("c3", "c5") else "exact"
     if args.impl == "reference":
         run_reference(args, cfg)
     elif dist_env()[2] > 1 or args.sharded:
