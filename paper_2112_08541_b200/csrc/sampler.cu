@@ -877,7 +877,9 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     const int mode = fanout <= 32 ? mode_env : 0;
     // candidate threshold keeps ~k + 2 sqrt(k) + 1 draws per parent (a sweep of
     // the margin at C2: (1, 1) 4027, (1.5, 1) 4079, (2, 1) 4102, (2.5, 2) 4046,
-    // (3, 3) 4032 b/s with HBM features -- a few % either way)
+    // (3, 3) 4032 b/s with HBM features -- a few % either way; the segmented
+    // walk: (1, 0.5) 4578, (1, 1) 4702, (1.5, 1) 4932, (2, 1) 4987, (2.5, 1)
+    // 4975, (3, 2) 4961)
     const float mar[2] = {2.0f, 1.0f};
     // candidate list length per warp (BGL_SEG_CAP < 512: tests force overflow)
     static const int seg_cap = [] {
