@@ -415,6 +415,27 @@ __global__ void copy_rows_kernel(const int32_t* __restrict__ plan, const int64_t
     const int lane = lane_id();
     const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    if ((rb & 15) == 0 && rb <= 512) {   // one 16-B piece per lane, two rows in flight per warp
+        const int64_t nr = (cnt + 1) >> 1;
+        for (int64_t r2 = gw; r2 < nr; r2 += nw) {
+            const int64_t ra = r2, rb2 = r2 + nr;
+            const bool two = rb2 < cnt;
+            const int2 pa = *reinterpret_cast<const int2*>(plan + 2 * ((int64_t)y * stride + ra));
+            int2 pb = make_int2(0, 0);
+            if (two) pb = *reinterpret_cast<const int2*>(plan + 2 * ((int64_t)y * stride + rb2));
+            const int64_t sa = row_index ? (int64_t)row_index[pa.x] : (int64_t)pa.x;
+            const int64_t sb = two ? (row_index ? (int64_t)row_index[pb.x] : (int64_t)pb.x) : 0;
+            const int64_t b = (int64_t)lane * 16;
+            if (b < rb) {
+                const uint4 va = *reinterpret_cast<const uint4*>(batch_rows + sa * rb + b);
+                uint4 vb = make_uint4(0, 0, 0, 0);
+                if (two) vb = *reinterpret_cast<const uint4*>(batch_rows + sb * rb + b);
+                *reinterpret_cast<uint4*>(rows + ((int64_t)y * C + pa.y) * rb + b) = va;
+                if (two) *reinterpret_cast<uint4*>(rows + ((int64_t)y * C + pb.y) * rb + b) = vb;
+            }
+        }
+        return;
+    }
     for (int64_t r = gw; r < cnt; r += nw) {
         const int32_t pos = plan[2 * ((int64_t)y * stride + r)];
         const int32_t slot = plan[2 * ((int64_t)y * stride + r) + 1];
