@@ -1,7 +1,8 @@
 """Full-size parity at the papers100M shape (111M nodes, 3.1B
 CSR entries, fanout [15,10,5], batch 1024): the bench's proximity batches
 sampled on the device (drop-in sample_batch and the pipeline's BatchSampler)
-equal the CPU oracle's frontiers and distinct sets bit for bit. The graph is
+equal the CPU oracle's frontiers and distinct sets bit for bit, and the
+device FIFO's per-batch counters on them equal the oracle's. The graph is
 the bench's C3 graph (GPU continuum generator); hubs above 2048 neighbours
 exercise the CTA kernel and the segmented walk's heavy-gap jumps."""
 import os
@@ -64,3 +65,28 @@ def test_c3_pipeline_sampler_distinct_matches_oracle(c3):
         u = int(s.num_uniq.item())
         _, _, d_o, _ = so.sample_batch(off, col, seeds.astype(np.int64), cfg["fanouts"], bench.RUN_SEED, i)
         assert np.array_equal(s.uniq[:u].cpu().numpy(), d_o), i
+
+
+@pytest.mark.parametrize("d,cap,host", [(1, 1_000_000, 0), (8, 150_000, 500_000)])
+def test_c3_fifo_counters_match_oracle(c3, d, cap, host):
+    """FIFO cache at the papers100M shape (rings wrap, d = 8 shards with peer
+    hits, the shared host level) vs the batch-parallel oracle, per batch."""
+    bench, cfg, dg, order, off, col = c3
+    import paper_2112_08541_b200 as bgl
+    from oracle import cache_oracle as co
+    from paper_2112_08541_b200.sampler import AccessTrace, BatchSampler, pcg_states, pcg_tables
+    b, nb = cfg["b"], 16
+    s = BatchSampler(dg, cfg["fanouts"], b, frontier_outputs=False)
+    tables = pcg_tables(pcg_states(bench.RUN_SEED, range(nb)))
+    batches = []
+    for i in range(nb):
+        s.load_seeds(torch.from_numpy(order[i * b:(i + 1) * b].astype(np.int32)).cuda())
+        s.run(tables[i])
+        batches.append(s.distinct().cpu().numpy().astype(np.int64))
+    rep = bgl.simulate(AccessTrace(batches=batches), bgl.CacheConfig(device_capacity=cap, host_capacity=host,
+                                                                     num_devices=d, feature_bytes_per_node=512))
+    want, _, _ = co.simulate_batched(batches, cap, host, d)
+    got = np.stack([rep.batch_queries, rep.batch_own_hits, rep.batch_peer_hits, rep.batch_host_hits,
+                    rep.batch_misses, rep.batch_insertions, rep.batch_evictions], axis=1)
+    assert np.array_equal(got, want)
+    assert want[:, 6].sum() > 0                 # the rings wrapped
