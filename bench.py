@@ -630,8 +630,8 @@ def run_sharded(args, cfg):
 
 
 def sharded_roofline(args, pipe, feats, rb, flush, R=8):
-    """Roofline of the sharded engine's dominant kernel, the homes' miss gather
-    (bgl_gather_list over the rows this rank's shard misses, for every worker):
+    """Roofline of the sharded engine's dominant kernel, the worker's miss
+    gather (bgl_gather_spans over this rank's own device-missed rows):
     R eager steps after the timed region, events on the miss stream around the
     gathers, rows read from the step's miss counts; max over ranks of the time."""
     import torch
@@ -647,7 +647,7 @@ def sharded_roofline(args, pipe, feats, rb, flush, R=8):
         flush.zero_()
         pipe.step_eager()
         torch.cuda.synchronize()
-        rows.append(int(pipe.miss_cnt[r].sum().item()))
+        rows.append(int(pipe.wmiss_cnt[r].item()))   # this rank's own misses (the worker fetches them)
     ev = pipe.miss_timing
     pipe.miss_timing = None
     ms = sum(a.elapsed_time(b) for a, b, _ in ev)
@@ -669,7 +669,7 @@ def sharded_roofline(args, pipe, feats, rb, flush, R=8):
         achieved = per_rank_bytes / (float(tmax.item()) / 1e3) / 1e9
         return {"bound": "host_link", "achieved": round(achieved, 2), "peak": round(peak, 2), "unit": "GB/s",
                 "frac": round(achieved / peak, 3), "traffic": None,
-                "kernel": "gather_list_kernel (homes' misses, zero-copy host reads, rows pushed to the workers)",
+                "kernel": "gather_span_kernel (the worker's own misses: TMA spans + 16-B zero-copy host reads)",
                 "algorithmic_bytes_per_launch": int(per_rank_bytes / R),
                 "peak_source": f"per-rank host link: max of a pinned 256 MB cudaMemcpy and a sequential zero-copy "
                                f"read of the feature store ({[round(x, 2) for x in peak_samples]}); "
@@ -679,7 +679,7 @@ def sharded_roofline(args, pipe, feats, rb, flush, R=8):
     achieved = 2 * per_rank_bytes / (float(tmax.item()) / 1e3) / 1e9
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(achieved / hbm, 3), "traffic": None,
-            "kernel": "gather_list_kernel (homes' misses from HBM, read + write)",
+            "kernel": "gather_span_kernel (the worker's own misses from HBM, read + write)",
             "algorithmic_bytes_per_launch": int(2 * per_rank_bytes / R)}
 
 

@@ -337,6 +337,12 @@ int bgl_partition_push(const int32_t* ids, const int64_t* n_dev, int64_t max_n, 
                        int64_t* counts_dev, void* workspace, void* stream);
 int bgl_scatter_rows(const int32_t* pos, const int64_t* n_dev, int64_t max_n, const void* rows,
                      int64_t row_bytes, void* out, void* stream);
+/* Ordered compaction: pos_out[0..*count_out) = the positions i < *n_dev with
+ * codes[i] >= min_code, ascending (the worker's device-missed rows: outcome
+ * codes H = 2 / M = 3 pushed back by the homes, cachesim.py:316-333 codes). */
+size_t bgl_compact_codes_workspace(int64_t max_n);
+int bgl_compact_codes(const uint8_t* codes, const int64_t* n_dev, int64_t max_n, int32_t min_code,
+                      int32_t* pos_out, int64_t* count_out, void* workspace, void* stream);
 /* Home-push gather (the row exchange fused into the gather): rows as in
  * bgl_gather_rows go to the local `out` (kept for the ring insert) AND to
  * push_out + push_pos[i] * row_bytes -- the worker GPU's output buffer,

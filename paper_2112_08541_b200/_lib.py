@@ -81,6 +81,8 @@ PROTOTYPES = {
     "bgl_partition_by_home": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "bgl_partition_push": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "bgl_scatter_rows": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp]),
+    "bgl_compact_codes_workspace": (c_sz, [c_i64]),
+    "bgl_compact_codes": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "bgl_gather_rows_push": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i32,
                                              c_i32, c_vp]),
     "bgl_ipc_get_handle": (ctypes.c_int, [c_vp, c_vp, ctypes.POINTER(c_i64)]),

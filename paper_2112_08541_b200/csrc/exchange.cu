@@ -3,13 +3,16 @@
 //   partition  stable split of a sorted batch by home -> H ascending buckets
 //              (the insert order each home needs, cachesim.py:527-528) and the
 //              position of every bucketed ID in the batch;
-//   scatter    rows returned by the homes back into batch order.
+//   scatter    rows returned by the homes back into batch order;
+//   compact    positions of a batch whose outcome code is >= a threshold
+//              (the worker's own device-missed rows, fetched by the worker).
 #include <dlfcn.h>
 
 #include <algorithm>
 #include <cstring>
 
 #include "common.cuh"
+#include "scan.cuh"
 
 namespace bgl {
 
@@ -178,6 +181,38 @@ __global__ void scatter_rows_kernel(const int32_t* __restrict__ pos, const int64
     __threadfence_system();   // `out` may be a peer GPU's buffer (codes pushed to the worker)
 }
 
+
+// Ordered stream compaction of code >= min_code (4 consecutive codes per
+// thread, block scan + decoupled look-back over tiles of kXTile).
+__global__ void __launch_bounds__(kXThreads)
+compact_codes_kernel(const uint8_t* __restrict__ codes, const int64_t* __restrict__ n_dev, int32_t min_code,
+                     ScanState ss, int32_t* __restrict__ pos_out, int64_t* __restrict__ count_out) {
+    __shared__ int64_t s_red[kXThreads / 32 + 1];
+    __shared__ int64_t s_agg[1], s_pre[1], s_tile;
+    const int64_t n = *n_dev;
+    const int64_t ntiles = n > 0 ? ceil_div(n, kXTile) : 1;
+    const int64_t tile = claim_tile(ss, &s_tile);
+    if (tile >= ntiles) return;
+    const int64_t base = tile * kXTile + (int64_t)threadIdx.x * kXRounds;
+    bool f[kXRounds];
+    int64_t cnt = 0;
+#pragma unroll
+    for (int u = 0; u < kXRounds; ++u) {
+        f[u] = base + u < n && (int32_t)codes[base + u] >= min_code;
+        cnt += f[u];
+    }
+    int64_t total;
+    const int64_t ex = block_excl_scan(cnt, s_red, &total);
+    if (threadIdx.x == 0) s_agg[0] = total;
+    __syncthreads();
+    lookback<1>(ss, tile, s_agg, s_pre);
+    int64_t r = s_pre[0] + ex;
+#pragma unroll
+    for (int u = 0; u < kXRounds; ++u)
+        if (f[u]) pos_out[r++] = (int32_t)(base + u);
+    if (tile == ntiles - 1 && threadIdx.x == 0) *count_out = s_pre[0] + total;
+}
+
 }  // namespace bgl
 
 using namespace bgl;
@@ -219,6 +254,23 @@ int bgl_partition_push(const int32_t* ids, const int64_t* n_dev, int64_t max_n, 
     home_push_kernel<<<(unsigned)ntiles, kXThreads, 0, st>>>(ids, n_dev, num_homes, tc, counts_dev, peer_ids,
                                                               peer_pos, peer_cnt);
     return launch_status("home_push_kernel");
+}
+
+size_t bgl_compact_codes_workspace(int64_t max_n) {
+    return scan_state_bytes(1, std::max<int64_t>(1, ceil_div(std::max<int64_t>(max_n, 1), kXTile)));
+}
+
+int bgl_compact_codes(const uint8_t* codes, const int64_t* n_dev, int64_t max_n, int32_t min_code, int32_t* pos_out,
+                      int64_t* count_out, void* workspace, void* stream) {
+    BGL_CHECK_ARG(codes && n_dev && pos_out && count_out && workspace, "bgl_compact_codes: null pointer");
+    BGL_CHECK_ARG(max_n >= 0, "bgl_compact_codes: max_n < 0");
+    cudaStream_t st = as_stream(stream);
+    const int64_t tiles = std::max<int64_t>(1, ceil_div(std::max<int64_t>(max_n, 1), kXTile));
+    BGL_TRY(reset_scan_state(workspace, 1, tiles, st));
+    compact_codes_kernel<<<(unsigned)tiles, kXThreads, 0, st>>>(codes, n_dev, min_code,
+                                                                 make_scan_state(workspace, 1, tiles), pos_out,
+                                                                 count_out);
+    return launch_status("compact_codes_kernel");
 }
 
 int bgl_scatter_rows(const int32_t* pos, const int64_t* n_dev, int64_t max_n, const void* rows, int64_t row_bytes,

@@ -284,14 +284,16 @@ class ShardedPipeline:
              order, so each shard's FIFO state machine sees the reference's
              batch sequence): lookup vs the pre-bucket state + index insert,
              outcome codes pushed into worker w's buffer
-      M(j)   per bucket: misses' rows over the host link (compacted list),
-             stored straight into worker w's output (peer memory)
-      B(j)   per bucket: ring hits pushed likewise, then the survivors' rows
-             into their ring slots (after the hits were read)
+      M(j)   the worker compacts its device-missed positions (codes H/M from
+             every home) and fetches those rows over its own host link into
+             its output (TMA spans over runs of consecutive IDs)
+      B(j)   per bucket: ring hits pushed into worker w's output (peer
+             memory), then the survivors' rows into the home's ring slots,
+             read from worker w's output (after the hits were read)
       Z(j)   barrier: every home's pushes of round j landed
-    Step k enqueues S(k+3), X(k+2), LI(k+2) || M(k+1) || B(k), Z(k): the host
-    link streams misses of round k+1 while round k+2's bookkeeping and round
-    k's ring traffic run beside it (the single-GPU pipeline.py schedule,
+    Step k enqueues S(k+3), X(k+2), LI(k+2) || M(k+1) || B(k), Z(k): every
+    host link streams its worker's misses of round k+1 while round k+2's
+    bookkeeping and round k's ring traffic run beside it (the single-GPU pipeline.py schedule,
     with buckets inside each stage). Dependencies point backwards only; the
     LI chain is strictly ordered, so every output equals the reference's.
     Buffers: receive areas, bucket state and outputs by round % 3 (X(k+3)
@@ -342,6 +344,11 @@ class ShardedPipeline:
         self.src_row = torch.empty((R, W, maxu), dtype=torch.int64, device=dev)
         self.miss_pos = torch.empty((R, W, maxu), dtype=torch.int32, device=dev)
         self.miss_cnt = torch.zeros((R, W), dtype=torch.int64, device=dev)
+        # worker side: this rank's own device-missed batch positions (codes H/M), per round set
+        self.wmiss_pos = torch.empty((R, maxu), dtype=torch.int32, device=dev)
+        self.wmiss_cnt = torch.zeros(R, dtype=torch.int64, device=dev)
+        self.compact_ws = torch.empty(int(_lib.load().bgl_compact_codes_workspace(maxu)), dtype=torch.uint8,
+                                      device=dev)
         self.plans = [[self.engine.plan_buffers() for _ in range(W)] for _ in range(R)]
         self.counters = torch.zeros(8, dtype=torch.int64, device=dev)
         self.part_counts = torch.zeros(W, dtype=torch.int64, device=dev)
@@ -372,9 +379,9 @@ class ShardedPipeline:
         self.miss_timing = None      # list -> _M records (start, end, round set) events (eager steps)
         self.graphs: dict = {}
         # per round (our kernels; the two NCCL barrier kernels not counted): stage + hops (sample + heavy)
-        # + dedup (mark, emit, reset); partition (count, scan, push); per bucket: lookup, insert (2),
-        # codes push, miss gather, hit gather, row copy
-        self.kernels_per_round = (1 + 2 * len(fanouts) + 3) + 3 + W * 7
+        # + dedup (mark, emit, reset); partition (count, scan, push); the worker's miss compaction +
+        # gather; per bucket: lookup, insert (2), codes push, hit gather, row copy
+        self.kernels_per_round = (1 + 2 * len(fanouts) + 3) + 3 + 2 + W * 6
 
     def close(self) -> None:
         lib = _lib.load()
@@ -395,6 +402,7 @@ class ShardedPipeline:
         with torch.cuda.stream(self.s_sample):
             if not self._in_graph:                                    # (a replayed step follows the whole
                 self.s_sample.wait_event(self.parted[slot])           # previous step: implicit there)
+                self.s_sample.wait_event(self.mdone[slot])
                 self.s_sample.wait_event(self.reported[slot])
             _lib.call("bgl_stage_batch", self.order.data_ptr(), self.order.numel(), self.b, self.num_batches,
                       self.tables.data_ptr(), self.batch_counter.data_ptr(), s.nodes.data_ptr(), s.counts.data_ptr(),
@@ -436,29 +444,40 @@ class ShardedPipeline:
                 self.li_done[r][w].record(self.s_li)
 
     def _M(self, j: int) -> None:
+        """The worker fetches its own device-missed rows (codes H/M, pushed
+        back by every home in LI(j)) from the feature store into its output:
+        its sorted distinct IDs keep their runs of consecutive IDs, so runs go
+        as TMA spans and the link sees the single-GPU access pattern (a home
+        gathering its bucket would read every world-th row only). The homes'
+        B(j) copy the survivors into their rings from this output."""
         r, maxu, rb, eng = j % self.NR, self.maxu, self.rb, self.engine
+        slot = j % self.NSMP
+        s = self.samplers[slot]
         ctas = 0 if eng.features.is_cuda else eng.miss_ctas
         lib = _lib.load()
         timing = self.miss_timing is not None and not self._in_graph
         with torch.cuda.stream(self.s_miss):
             st = _lib.stream_ptr(self.s_miss)
-            if timing:   # measurement pass (bench roofline): the gathers alone between two events
-                for w in range(self.world):
-                    self.s_miss.wait_event(self.li_done[r][w])
+            if timing:   # measurement pass (bench roofline): the compaction + gather between two events
                 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), r)
                 ev[0].record(self.s_miss)
-            for w in range(self.world):
-                if not self._in_graph:
-                    self.s_miss.wait_event(self.li_done[r][w])
-                # rows go only to worker w's output (peer memory); B(j) reads the survivors back from there
-                _lib.check(lib.bgl_gather_list(self.miss_pos[r, w].data_ptr(), self.miss_cnt[r, w:w + 1].data_ptr(),
-                                               maxu, self.recv_ids[r, w].data_ptr(), eng.table, rb, None,
-                                               self.worker_rows[w] + r * maxu * rb, self.recv_pos[r, w].data_ptr(),
+            _lib.check(lib.bgl_compact_codes(self.out_codes[r].data_ptr(), s.num_uniq.data_ptr(), maxu, 2,
+                                             self.wmiss_pos[r].data_ptr(), self.wmiss_cnt[r:r + 1].data_ptr(),
+                                             self.compact_ws.data_ptr(), st))
+            out = self.out_rows[r]
+            if eng.miss_spans and rb % 16 == 0:
+                _lib.check(lib.bgl_gather_spans(self.wmiss_pos[r].data_ptr(), self.wmiss_cnt[r:r + 1].data_ptr(),
+                                                maxu, s.uniq.data_ptr(), eng.table, rb, out.data_ptr(), ctas, st))
+            else:
+                _lib.check(lib.bgl_gather_list(self.wmiss_pos[r].data_ptr(), self.wmiss_cnt[r:r + 1].data_ptr(),
+                                               maxu, s.uniq.data_ptr(), eng.table, rb, out.data_ptr(), None, None,
                                                eng.miss_rows_in_flight, ctas, st))
-                self.miss_done[r][w].record(self.s_miss)
             if timing:
                 ev[1].record(self.s_miss)
                 self.miss_timing.append(ev)
+            self.mdone[slot].record(self.s_miss)
+            for w in range(self.world):
+                self.miss_done[r][w].record(self.s_miss)
 
     def _B(self, j: int) -> None:
         r, maxu, rb, eng = j % self.NR, self.maxu, self.rb, self.engine
@@ -487,6 +506,11 @@ class ShardedPipeline:
             self._S(j)
         self._X(0)
         self._LI(0)
+        # M(0) reads the codes every home pushed in LI(0): join + barrier first
+        main = torch.cuda.current_stream()
+        main.wait_stream(self.s_li)
+        self.barrier()
+        self.s_miss.wait_stream(main)
         self._M(0)
         self._X(1)
         self._LI(1)
@@ -553,6 +577,7 @@ class ShardedPipeline:
         R, W = self.NR, self.world
         self.sampled = [torch.cuda.Event() for _ in range(self.NSMP)]
         self.parted = [torch.cuda.Event() for _ in range(self.NSMP)]
+        self.mdone = [torch.cuda.Event() for _ in range(self.NSMP)]    # M(j) read sampler j's distinct IDs
         self.xdone = [torch.cuda.Event() for _ in range(R)]
         self.li_done = [[torch.cuda.Event() for _ in range(W)] for _ in range(R)]
         self.miss_done = [[torch.cuda.Event() for _ in range(W)] for _ in range(R)]
