@@ -607,8 +607,9 @@ def run_sharded(args, cfg):
                    "csr_entries": dg.num_edges, "feature_dim": cfg["dim"], "fanouts": list(cfg["fanouts"]),
                    "batch": b, "cache_rows_per_gpu": cap, "features": args.features,
                    "parallelism": f"dp{world} + node-ID-sharded FIFO cache (home = v % {world}); " + (
-                       "IDs pushed to the homes over peer memory by the partition kernel, rows/codes pushed back "
-                       "by the homes' gathers (CUDA IPC), NCCL one-int barriers, no host sync per round"
+                       "IDs pushed to the homes over peer memory by the partition kernel, codes and hit rows "
+                       "pushed back by the homes (CUDA IPC), misses fetched by each worker over its own host link, "
+                       "NCCL one-int barriers, no host sync per round"
                        if args.exchange == "push" else "IDs and rows by NCCL all-to-all (host-synchronised)"),
                    "l2": "flushed between timed steps (256 MB write, outside the events)",
                    "step": f"one round = {world} mini-batches (one per GPU)", "cuda_graphs": graphs,
