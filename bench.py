@@ -474,8 +474,9 @@ def run_sharded(args, cfg):
     """N GPUs, one process each: node-ID-sharded FIFO cache (home = v % N,
     cachesim.py:505-506), rank w samples batches i = j*N + w. Default engine:
     ShardedPipeline -- IDs pushed to the homes over peer memory by the
-    partition kernel, rows and codes pushed back by the homes' gathers, NCCL
-    only as a one-int barrier, no host synchronisation per round
+    partition kernel, codes and hit rows pushed back by the homes, misses
+    fetched by each worker over its own host link, NCCL only as a one-int
+    barrier, no host synchronisation per round
     (paper_2112_08541_b200/distributed.py). `--exchange nccl`: the all-to-all
     baseline (ShardedFeatureCache, host-synchronised per round).
     One step = one round = N mini-batches (one per GPU)."""
