@@ -649,7 +649,7 @@ def sharded_roofline(args, pipe, feats, rb, flush, R=8):
         flush.zero_()
         pipe.step_eager()
         torch.cuda.synchronize()
-        rows.append(int(pipe.wmiss_cnt[r].item()))   # this rank's own misses (the worker fetches them)
+        rows.append(int(pipe.own_misses(r)[1].item()))   # this rank's own misses (the worker fetches them)
     ev = pipe.miss_timing
     pipe.miss_timing = None
     ms = sum(a.elapsed_time(b) for a, b, _ in ev)

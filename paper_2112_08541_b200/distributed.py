@@ -461,23 +461,29 @@ class ShardedPipeline:
             if timing:   # measurement pass (bench roofline): the compaction + gather between two events
                 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), r)
                 ev[0].record(self.s_miss)
-            _lib.check(lib.bgl_compact_codes(self.out_codes[r].data_ptr(), s.num_uniq.data_ptr(), maxu, 2,
-                                             self.wmiss_pos[r].data_ptr(), self.wmiss_cnt[r:r + 1].data_ptr(),
-                                             self.compact_ws.data_ptr(), st))
+            pos, cnt = self.own_misses(r)
+            if self.world > 1:   # (one home: its lookup's compacted list is already the batch's)
+                _lib.check(lib.bgl_compact_codes(self.out_codes[r].data_ptr(), s.num_uniq.data_ptr(), maxu, 2,
+                                                 pos.data_ptr(), cnt.data_ptr(), self.compact_ws.data_ptr(), st))
             out = self.out_rows[r]
             if eng.miss_spans and rb % 16 == 0:
-                _lib.check(lib.bgl_gather_spans(self.wmiss_pos[r].data_ptr(), self.wmiss_cnt[r:r + 1].data_ptr(),
-                                                maxu, s.uniq.data_ptr(), eng.table, rb, out.data_ptr(), ctas, st))
+                _lib.check(lib.bgl_gather_spans(pos.data_ptr(), cnt.data_ptr(), maxu, s.uniq.data_ptr(), eng.table,
+                                                rb, out.data_ptr(), ctas, st))
             else:
-                _lib.check(lib.bgl_gather_list(self.wmiss_pos[r].data_ptr(), self.wmiss_cnt[r:r + 1].data_ptr(),
-                                               maxu, s.uniq.data_ptr(), eng.table, rb, out.data_ptr(), None, None,
-                                               eng.miss_rows_in_flight, ctas, st))
+                _lib.check(lib.bgl_gather_list(pos.data_ptr(), cnt.data_ptr(), maxu, s.uniq.data_ptr(), eng.table,
+                                               rb, out.data_ptr(), None, None, eng.miss_rows_in_flight, ctas, st))
             if timing:
                 ev[1].record(self.s_miss)
                 self.miss_timing.append(ev)
             self.mdone[slot].record(self.s_miss)
             for w in range(self.world):
                 self.miss_done[r][w].record(self.s_miss)
+
+    def own_misses(self, r: int):
+        """(positions, count) of this worker's device-missed rows of round set r."""
+        if self.world == 1:
+            return self.miss_pos[r, 0], self.miss_cnt[r, 0:1]
+        return self.wmiss_pos[r], self.wmiss_cnt[r:r + 1]
 
     def _B(self, j: int) -> None:
         r, maxu, rb, eng = j % self.NR, self.maxu, self.rb, self.engine
