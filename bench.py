@@ -362,7 +362,9 @@ def run_bgl(args, cfg):
         achieved = alg / (t_g * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 3), "traffic": None,
-                "kernel": "gather_span_kernel (misses) + gather_v4_kernel (hits), one launch each",
+                "kernel": ("gather_v4_kernel (every row in one pass: hits from the HBM ring, misses from the "
+                           "HBM-resident table)" if pipe.fused_hbm_gather else
+                           "gather_span_kernel (misses) + gather_v4_kernel (hits), one launch each"),
                 "algorithmic_bytes_per_launch": int(alg)}
     prof = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{args.features}.json")
     if os.path.exists(prof):
@@ -372,10 +374,14 @@ def run_bgl(args, cfg):
             roof["traffic"] = tr["miss_gather"]["pcie_read_bytes_per_launch"]
             roof["traffic_kind"] = "pcie_read_bytes (ncu, one launch)"
             roof["traffic_launch_algorithmic_bytes"] = tr["miss_gather"].get("algorithmic_bytes_per_launch")
+        elif pipe.fused_hbm_gather and "fused_gather" in tr:
+            roof["traffic"] = tr["fused_gather"]["dram_bytes_per_launch"]
+            roof["traffic_kind"] = "dram__bytes_read+write (ncu, one launch; writes that stay in L2 are not counted)"
         else:
             roof["traffic"] = tr["miss_gather"]["dram_bytes_per_launch"] + tr["hit_gather"]["dram_bytes_per_launch"]
             roof["traffic_kind"] = "dram__bytes_read+write (ncu, one launch of each gather; writes that stay in L2 are not counted)"
-        roof["traffic_source"] = tr.get("source")
+        roof["traffic_source"] = (tr["fused_gather"]["source"] if args.features != "host" and pipe.fused_hbm_gather
+                                  and "fused_gather" in tr else tr.get("source"))
 
     # e2e through the public API with host buffers: every step copies the next
     # batch's seeds from pinned host memory and reads this batch's distinct IDs

@@ -221,14 +221,17 @@ class FeatureCacheEngine:
                                        self.dev.rows_ptr() or None, self.table, self.row_bytes, out.data_ptr(), 2,
                                        ctas, st))
 
-    def back(self, ids, n_dev, max_n, out, src_row, plan, plan_count, stream=None, events=None):
-        """Hits' rows from the HBM ring, then the survivors' rows into the
-        ring (after the hits were read: the same-batch eviction hazard)."""
+    def back(self, ids, n_dev, max_n, out, src_row, plan, plan_count, stream=None, events=None,
+             with_misses: bool = False):
+        """Hits' rows from the HBM ring (with_misses: every row, misses from
+        the HBM-resident table in the same pass), then the survivors' rows
+        into the ring (after the hits were read: the same-batch eviction
+        hazard)."""
         lib = _lib.load()
         st = _lib.stream_ptr(stream)
         _lib.check(lib.bgl_gather_rows(ids.data_ptr(), src_row.data_ptr(), n_dev.data_ptr(), max_n,
-                                       self.dev.rows_ptr() or None, self.table, self.row_bytes, out.data_ptr(), 1,
-                                       0, st))
+                                       self.dev.rows_ptr() or None, self.table, self.row_bytes, out.data_ptr(),
+                                       0 if with_misses else 1, 0, st))
         if events is not None:
             events[0].record()
         if self.dev.rows_ptr():

@@ -77,6 +77,11 @@ class MiniBatchPipeline:
         self.miss_pos = [torch.empty(self.max_uniq, dtype=torch.int32, device="cuda") for _ in range(NB)]
         self.miss_count = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in range(NB)]
         self.compact_misses = True
+        # HBM-resident features: no host link to keep busy, so the misses are
+        # gathered in the back stage's pass over the batch (one kernel, rows
+        # from the ring or the table) instead of a miss stage of their own
+        self.fused_hbm_gather = bool(getattr(features, "is_cuda", False)) and \
+            os.environ.get("BGL_HBM_FUSED", "1") != "0"
         self.tables = pcg_tables(pcg_states(seed, range(self.num_batches)))
         self.table_stage = [torch.empty((_lib.PCG_TABLE_ROWS, 4), dtype=torch.int64, device="cuda") for _ in range(NS)]
         self.batch_counter = torch.zeros(1, dtype=torch.int64, device="cuda")
@@ -108,7 +113,7 @@ class MiniBatchPipeline:
         s = self.samplers[0]
         # stage + H x (sample, heavy) + dedup (mark seeds, emit, reset) + lookup + insert(2)
         # + miss gather + hit gather + row copy (= the ncu launch list of a step); host-fed: + d2h_result
-        self.kernels_per_step = 1 + 2 * s.H + 3 + 1 + 2 + 1 + 1 + 1
+        self.kernels_per_step = 1 + 2 * s.H + 3 + 1 + 2 + (0 if self.fused_hbm_gather else 1) + 1 + 1
 
     # -- stages ------------------------------------------------------------------
     def _sample(self, batch: int, stream=None, fed: bool = False, hooks=None, part: str = "all") -> None:
@@ -140,6 +145,8 @@ class MiniBatchPipeline:
                                   miss_count=self.miss_count[j])
 
     def _miss(self, batch: int, stream=None) -> None:
+        if self.fused_hbm_gather:
+            return
         s = self.samplers[batch % NS]
         j = batch % NB
         if self.compact_misses:
@@ -153,7 +160,7 @@ class MiniBatchPipeline:
         j = batch % NB
         plan, pcount = self.plans[j]
         self.engine.back(s.uniq, s.num_uniq, s.max_uniq, self.outs[j], self.src_row[j], plan, pcount,
-                         stream=stream, events=events)
+                         stream=stream, events=events, with_misses=self.fused_hbm_gather)
         if fed:
             _lib.call("bgl_d2h_result", s.uniq.data_ptr(), s.num_uniq.data_ptr(), s.max_uniq,
                       self.counters.data_ptr(), self._host_ids_dev[j], self._host_meta_dev[j],
