@@ -381,7 +381,8 @@ class ShardedPipeline:
         # per round (our kernels; the two NCCL barrier kernels not counted): stage + hops (sample + heavy)
         # + dedup (mark, emit, reset); partition (count, scan, push); the worker's miss compaction +
         # gather; per bucket: lookup, insert (2), codes push, hit gather, row copy
-        self.kernels_per_round = (1 + 2 * len(fanouts) + 3) + 3 + 2 + W * 6
+        per_hop = 1 if rng == "counter" else 2
+        self.kernels_per_round = (1 + per_hop * len(fanouts) + 3) + 3 + (2 if W > 1 else 1) + W * 6
 
     def close(self) -> None:
         lib = _lib.load()

@@ -111,9 +111,11 @@ class MiniBatchPipeline:
         self.k = 0                # batches completed (rows ready)
         self.primed = False
         s = self.samplers[0]
-        # stage + H x (sample, heavy) + dedup (mark seeds, emit, reset) + lookup + insert(2)
-        # + miss gather + hit gather + row copy (= the ncu launch list of a step); host-fed: + d2h_result
-        self.kernels_per_step = 1 + 2 * s.H + 3 + 1 + 2 + (0 if self.fused_hbm_gather else 1) + 1 + 1
+        # stage + H x (sample, heavy; counter RNG: one kernel per hop) + dedup (mark seeds, emit, reset)
+        # + lookup + insert(2) + miss gather + hit gather + row copy (= the ncu launch list of a step);
+        # host-fed: + d2h_result
+        per_hop = 1 if rng == "counter" else 2
+        self.kernels_per_step = 1 + per_hop * s.H + 3 + 1 + 2 + (0 if self.fused_hbm_gather else 1) + 1 + 1
 
     # -- stages ------------------------------------------------------------------
     def _sample(self, batch: int, stream=None, fed: bool = False, hooks=None, part: str = "all") -> None:
