@@ -21,11 +21,7 @@ from paper_2112_08541_b200.cachesim import CacheConfig  # noqa: E402
 from paper_2112_08541_b200.ordering import random_shuffle_schedule  # noqa: E402
 from paper_2112_08541_b200.pipeline import MiniBatchPipeline  # noqa: E402
 
-CONFIGS = dict(bench.CONFIGS)
-CONFIGS["c5"] = dict(workload="1B-edge power-law graph (64M nodes, avg degree 31), 128-d fp32 features in pinned "
-                              "host memory, fanout [15,10,5], batch 1024",
-                     n=64_000_000, avg_degree=31, dim=128, labels=128, train=0.01, fanouts=(15, 10, 5), b=1024,
-                     cache_frac=0.10, S=4)
+CONFIGS = dict(bench.CONFIGS)      # c1, c2, c3 (= the C4 sweep's graph), c5
 
 
 def run(cfg, order, cap, steps, warmup):
