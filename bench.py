@@ -446,6 +446,8 @@ def run_bgl(args, cfg):
         "feature_gbs": round(feat_gbs, 2), "hit_pct": round(100.0 * hits / max(queries, 1), 2),
         "rows_per_batch": round(queries / max(args.steps, 1) / 1, 1),
         "stages_ms": {k: round(statistics.mean(v), 4) for k, v in st_times.items()},
+        **sampler_report(dg, cfg, order, args.rng, statistics.mean(st_times["sample"]),
+                         statistics.mean(st_times["dedup"])),
         "roofline": roof,
         "e2e": {"value": round(n_e2e / (sum(e2e_ms) * 1e-3) * world, 2), "unit": UNIT,
                 "h2d_bytes_per_step": int(h2d / n_e2e), "d2h_bytes_per_step": int(d2h / n_e2e),
@@ -635,6 +637,42 @@ def run_sharded(args, cfg):
     if args.exchange == "push":
         pipe.close()
     dist.destroy_process_group()
+
+
+def sampler_report(dg, cfg, order, rng, sample_ms, dedup_ms, n=8):
+    """SURVEY §8d's separate sampler / dedup figures for the replay sampler:
+    PCG64 draws per batch (= steps of the replayed stream, ALU only) and their
+    rate over the bench's serialised sample stage, parents and outputs per hop,
+    the algorithmic bytes sum_h [P_h*16 + S_h*4 + S_h*8], dedup keys/s. Counts
+    from n batches of the bench's schedule sampled once more, outside the
+    timed region."""
+    if rng != "replay":
+        return {}
+    import torch
+    from paper_2112_08541_b200.sampler import BatchSampler, pcg_states, pcg_tables
+    b = cfg["b"]
+    s = BatchSampler(dg, cfg["fanouts"], b)
+    tables = pcg_tables(pcg_states(RUN_SEED, range(n)))
+    draws, counts = [], []
+    for i in range(n):
+        s.load_seeds(order[i * b:(i + 1) * b])
+        s.run(tables[i])
+        draws.append(int(s.draw_base[-1].item()))
+        counts.append(s.host_counts())
+    del s
+    torch.cuda.empty_cache()
+    c = np.mean(np.array(counts, dtype=np.float64), axis=0)
+    H = len(cfg["fanouts"])
+    parents, outs = c[:H], c[1:H + 1]
+    d = float(np.mean(draws))
+    keys = float(c.sum())
+    return {"sampler": {"draws_per_batch": round(d), "pcg64_draws_per_s": round(d / (sample_ms * 1e-3)),
+                        "parents_per_hop": [round(x) for x in parents], "outputs_per_hop": [round(x) for x in outs],
+                        "algorithmic_bytes_per_batch": round(float(np.sum(parents * 16 + outs * 12))),
+                        "bound": "integer ALU: one 128-bit LCG step + XSL-RR per draw (no bytes per draw)",
+                        "stage_ms": round(sample_ms, 4)},
+            "dedup": {"keys_per_batch": round(keys), "keys_per_s": round(keys / (dedup_ms * 1e-3)),
+                      "stage_ms": round(dedup_ms, 4)}}
 
 
 def sharded_roofline(args, pipe, feats, rb, flush, R=8):
