@@ -90,3 +90,27 @@ def test_c3_fifo_counters_match_oracle(c3, d, cap, host):
                     rep.batch_misses, rep.batch_insertions, rep.batch_evictions], axis=1)
     assert np.array_equal(got, want)
     assert want[:, 6].sum() > 0                 # the rings wrapped
+
+
+def test_c3_simulate_epoch_comm_report_matches_oracle(c3):
+    """simulate_epoch with an 8-way random partition at the papers100M shape:
+    trace rows and the EpochCommReport (local/remote accesses, seed and
+    request loads, parent_idx-propagated origins) vs the oracle."""
+    bench, cfg, dg, order, off, col = c3
+    import paper_2112_08541_b200 as bgl
+    b, k = cfg["b"], 8
+
+    class P:
+        pass
+
+    p = P()
+    p.part_of = np.random.default_rng(5).integers(0, k, dg.num_nodes).astype(np.int64)
+    p.k = k
+    batches = [order[i * b:(i + 1) * b].astype(np.int64) for i in range(3)]
+    sched = bgl.BatchSchedule(batches=batches, batch_size=b, policy="proximity-S4")
+    trace, rep = bgl.simulate_epoch(dg, p, sched, bgl.SamplingConfig(fanouts=cfg["fanouts"], seed=bench.RUN_SEED))
+    tr_o, local, remote, seed_load, request_load = so.simulate_epoch(off, col, p.part_of, k, batches, cfg["fanouts"],
+                                                                     bench.RUN_SEED)
+    assert all(np.array_equal(a, e) for a, e in zip(trace.batches, tr_o))
+    assert (rep.local_accesses, rep.remote_accesses) == (local, remote)
+    assert np.array_equal(rep.seed_load, seed_load) and np.array_equal(rep.request_load, request_load)
