@@ -32,6 +32,28 @@ def test_partition_and_scatter_kernels():
         assert np.array_equal(out.cpu().numpy(), ref)
 
 
+def test_compact_codes_kernel():
+    """bgl_compact_codes (the worker's own miss list): ascending positions with
+    code >= min_code, device count, empty / all / none and multi-tile sizes."""
+    from paper_2112_08541_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(3)
+    for n, cap in ((0, 16), (1, 16), (1000, 1000), (5000, 9000), (300_001, 400_000)):
+        for lo in (0, 2, 4):
+            codes = rng.integers(0, 4, size=max(cap, 1)).astype(np.uint8)
+            d_codes = torch.from_numpy(codes).cuda()
+            n_dev = torch.tensor([n], dtype=torch.int64, device="cuda")
+            pos = torch.full((max(cap, 1),), -7, dtype=torch.int32, device="cuda")
+            cnt = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+            ws = torch.empty(int(lib.bgl_compact_codes_workspace(cap)), dtype=torch.uint8, device="cuda")
+            _lib.check(lib.bgl_compact_codes(d_codes.data_ptr(), n_dev.data_ptr(), cap, lo, pos.data_ptr(),
+                                             cnt.data_ptr(), ws.data_ptr(), _lib.stream_ptr()))
+            want = np.flatnonzero(codes[:n] >= lo)
+            c = int(cnt.item())
+            assert c == want.size, (n, lo)
+            assert np.array_equal(pos[:c].cpu().numpy(), want), (n, lo)
+
+
 @pytest.mark.parametrize("world", [2, 4])
 def test_shard_engines_reproduce_reference_d_device_simulation(world):
     from paper_2112_08541_b200.distributed import GpuShardEngine, GpuShardOps
