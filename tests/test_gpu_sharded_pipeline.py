@@ -1,11 +1,12 @@
 """GPU test of the pipelined, host-sync-free sharded round (ShardedPipeline):
-two processes share one GPU (CUDA IPC works between processes of one device),
-each is home shard `rank` and worker of every other batch. IDs reach the homes
-through bgl_partition_push (peer stores), rows and codes come back through the
-homes' pushes; a host barrier stands in for the NCCL one (NCCL cannot put two
-ranks on one GPU). Every round's distinct set, per-node outcome codes and rows
-must equal the reference: the oracle sampler + the reference's 2-device FIFO
-simulation (cachesim.py:461-549) + F[ids]."""
+two (or three) processes share one GPU (CUDA IPC works between processes of
+one device), each is home shard `rank` and worker of every world-th batch.
+IDs reach the homes through bgl_partition_push (peer stores), codes and hit
+rows come back through the homes' pushes, each worker fetches its own misses;
+a host barrier stands in for the NCCL one (NCCL cannot put two ranks on one
+GPU). Every round's distinct set, per-node outcome codes and rows must equal
+the reference: the oracle sampler + the reference's d-device FIFO simulation
+(cachesim.py:461-549) + F[ids]."""
 
 import os
 import socket
@@ -32,14 +33,14 @@ def _graph():
 
 
 def _order():
-    dg_train = np.arange(N)[np.random.default_rng(1).permutation(N)][: 12 * B]
+    dg_train = np.arange(N)[np.random.default_rng(1).permutation(N)][: 24 * B]
     return dg_train.astype(np.int32)
 
 
-def _worker(rank, port, cap, where, rounds, path):
+def _worker(rank, world, port, cap, where, rounds, path):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
-    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2112_08541_b200.distributed import ShardedPipeline
     from paper_2112_08541_b200.features import synthetic_features
 
@@ -50,7 +51,7 @@ def _worker(rank, port, cap, where, rounds, path):
     dg = _graph()
     feats = synthetic_features(N, DIM, seed=8, device_resident=(where == "hbm"))
     order = torch.from_numpy(_order()).cuda()
-    pipe = ShardedPipeline(rank, WORLD, dg, FAN, B, order, SEED, cap, feats, num_batches=rounds * WORLD,
+    pipe = ShardedPipeline(rank, world, dg, FAN, B, order, SEED, cap, feats, num_batches=rounds * world,
                            barrier=host_barrier)
     out = {}
     for j in range(rounds):
@@ -76,14 +77,14 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("where,cap", [("host", 700), ("hbm", 300)])
-def test_sharded_pipeline_matches_reference(where, cap):
+@pytest.mark.parametrize("where,cap,world", [("host", 700, 2), ("hbm", 300, 2), ("host", 500, 3)])
+def test_sharded_pipeline_matches_reference(where, cap, world):
     rounds = 6
     with tempfile.TemporaryDirectory() as td:
         path = os.path.join(td, "res")
-        mp.spawn(_worker, args=(_free_port(), cap, where, rounds, path), nprocs=WORLD, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), cap, where, rounds, path), nprocs=world, join=True)
         res = {}
-        for r in range(WORLD):
+        for r in range(world):
             res.update({k + (f"_r{r}" if k == "counters" else ""): v for k, v in np.load(path + f".{r}.npz").items()})
     # reference: same graph on the host, oracle sampler, 2-device FIFO simulation
     from paper_2112_08541_b200.graph import power_law_edges
@@ -91,18 +92,18 @@ def test_sharded_pipeline_matches_reference(where, cap):
     edges, _, _ = power_law_edges(N, DEG, 3, 0.2, 4)
     off, col = go.csr_from_edges(edges.astype(np.int64), N)
     order = _order()
-    nb = rounds * WORLD
+    nb = rounds * world
     distinct = [so.sample_batch(off, col, order[i * B:(i + 1) * B].astype(np.int64), FAN, SEED, i)[2]
                 for i in range(nb)]
     # the pipeline's lookups run two rounds ahead (LI(k+2) in step k): rounds
     # 0..rounds+1, batch indices wrapping over the epoch
-    seq = [distinct[i % nb] for i in range((rounds + 2) * WORLD)]
-    ref_cnt, ref_codes = co.FifoEngine(cap, 0, WORLD).run(seq)
+    seq = [distinct[i % nb] for i in range((rounds + 2) * world)]
+    ref_cnt, ref_codes = co.FifoEngine(cap, 0, world).run(seq)
     for i in range(nb):
         assert np.array_equal(res[f"ids{i}"], distinct[i]), i
         assert np.array_equal(res[f"codes{i}"], ref_codes[i]), i
         assert np.array_equal(res[f"rows{i}"], fo.synthetic_features(distinct[i], DIM, seed=8)), i
-    tot = res["counters_r0"] + res["counters_r1"]
+    tot = sum(res[f"counters_r{r}"] for r in range(world))
     assert tot[:7].tolist() == np.asarray(ref_cnt).sum(axis=0)[:7].tolist()
 
 
