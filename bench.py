@@ -480,7 +480,7 @@ def run_bgl(args, cfg):
 
 def run_sharded(args, cfg):
     """N GPUs, one process each: node-ID-sharded FIFO cache (home = v % N,
-    cachesim.py:505-506), rank w samples batches i = j*N + w. Default engine:
+    cachesim.py:319-320), rank w samples batches i = j*N + w. Default engine:
     ShardedPipeline -- IDs pushed to the homes over peer memory by the
     partition kernel, codes and hit rows pushed back by the homes, misses
     fetched by each worker over its own host link, NCCL only as a one-int

@@ -138,7 +138,7 @@ int bgl_unique_reset(void* workspace, int64_t num_nodes, const int32_t* uniq,
 
 /* ---------------------------------------------------------------- FIFO cache
  * BGL's dynamic FIFO feature cache (gnnio.cachesim FifoLevel, cachesim.py:
- * 267-293, engine cachesim.py:376-389, simulate cachesim.py:461-549).
+ * 81-107, engine cachesim.py:190-203, simulate cachesim.py:275-363).
  * `num_shards` device rings of `shard_capacity` slots (node v lives on shard
  * v % num_shards), one shared host ring of `host_capacity` slots, a direct-
  * address index per level, and optionally `row_bytes` of feature storage per
@@ -155,12 +155,12 @@ int bgl_cache_reset(bgl_cache_t cache, void* stream);
 int bgl_cache_reserve_batch(bgl_cache_t cache, int64_t max_batch);
 /* Multi-GPU: this single-shard handle is shard `shard_index` of
  * `num_global_shards` (node v lives on GPU v % num_global_shards,
- * cachesim.py:505-506); lookups code a hit D when worker == shard_index,
+ * cachesim.py:319-320); lookups code a hit D when worker == shard_index,
  * else P. Single-process handles keep the default (0 of num_shards). */
 int bgl_cache_set_shard(bgl_cache_t cache, int32_t shard_index, int32_t num_global_shards);
 /* Device pointers of the ring feature rows ([num_shards*shard_capacity][row_bytes]). */
 void* bgl_cache_rows(bgl_cache_t cache);
-/* Classify every query against the pre-batch state (cachesim.py:504-525):
+/* Classify every query against the pre-batch state (cachesim.py:318-339):
  * codes[i] in {0:D own, 1:P peer, 2:H host, 3:M miss} (may be NULL);
  * src_row[i] = global ring row (shard*cap + slot) for D/P, -1 otherwise (may
  * be NULL); counters[0..4] += queries, own, peer, host, miss.
@@ -179,7 +179,7 @@ int bgl_cache_lookup(bgl_cache_t cache, const int32_t* ids, const int64_t* n_dev
 int bgl_cache_lookup_misses(bgl_cache_t cache, const int32_t* ids, const int64_t* n_dev, int64_t max_n,
                             int32_t worker, uint8_t* codes, int64_t* src_row, int64_t* counters,
                             int32_t* miss_pos, int64_t* miss_count, void* stream);
-/* Insert-after-batch (cachesim.py:527-530): device-missed into their home
+/* Insert-after-batch (cachesim.py:341-344): device-missed into their home
  * ring, full misses into the host ring, ascending; counters[5..6] +=
  * insertions, evictions. When batch_rows != NULL, row i of the batch output
  * (aligned with sorted_ids) is copied into the slot its node lands in. */
@@ -204,13 +204,13 @@ int bgl_cache_copy_rows_indexed(bgl_cache_t cache, const int32_t* plan, const in
                                 int64_t max_sorted, const void* batch_rows, const int32_t* row_index,
                                 void* stream);
 /* Synchronous export of the ring contents (int64, -1 = empty) and tails, in
- * the layout of FifoLevel.slots / .tail (cachesim.py:273-275). Any pointer may
+ * the layout of FifoLevel.slots / .tail (cachesim.py:87-89). Any pointer may
  * be NULL. dev_slots: [num_shards][shard_capacity]; dev_tails: [num_shards]. */
 int bgl_cache_export(bgl_cache_t cache, int64_t* dev_slots_host, int64_t* dev_tails_host,
                      int64_t* host_slots_host, int64_t* host_tail_host);
 
 /* ---------------------------------------------------------------- static-degree policy
- * gnnio.cachesim.warm_static (cachesim.py:392-410): per shard the capacity
+ * gnnio.cachesim.warm_static (cachesim.py:206-224): per shard the capacity
  * highest-degree nodes (ties to the lower ID), then the host level from the
  * rest; lookups then run through bgl_cache_lookup and nothing is inserted.
  * hist: int64 [num_shards][max_degree+1] (degrees clamped), nodes flagged in
@@ -231,7 +231,7 @@ int bgl_cache_warm(bgl_cache_t cache, const int32_t* dev_nodes, const int64_t* d
                    const int32_t* host_nodes, int64_t n_host, void* stream);
 
 /* ---------------------------------------------------------------- feature gather
- * Net-new (the reference only counts bytes, cachesim.py:447-458):
+ * Net-new (the reference only counts bytes, cachesim.py:261-272):
  * out[i] = src_row[i] >= 0 ? ring_rows[src_row[i]] : table[ids[i]], 128-bit
  * vectorised. `table` may be a device pointer (HBM-resident features) or the
  * device alias of pinned host memory (zero-copy miss path). src_row NULL:
@@ -317,7 +317,7 @@ int bgl_shuffling_tv(const int32_t* labels, const int32_t* order, int64_t total,
 
 /* ---------------------------------------------------------------- multi-GPU exchange
  * Node-ID sharding of the cache across GPUs (home of v = v % H,
- * cachesim.py:505-506). Stable split of a sorted batch into H ascending
+ * cachesim.py:319-320). Stable split of a sorted batch into H ascending
  * buckets (out_ids, home-major), out_pos[i] = position of out_ids[i] in the
  * batch, counts_dev[h] = bucket sizes. Then the homes' rows come back and
  * bgl_scatter_rows puts row i at out[pos[i]]. */
@@ -339,7 +339,7 @@ int bgl_scatter_rows(const int32_t* pos, const int64_t* n_dev, int64_t max_n, co
                      int64_t row_bytes, void* out, void* stream);
 /* Ordered compaction: pos_out[0..*count_out) = the positions i < *n_dev with
  * codes[i] >= min_code, ascending (the worker's device-missed rows: outcome
- * codes H = 2 / M = 3 pushed back by the homes, cachesim.py:316-333 codes). */
+ * codes H = 2 / M = 3 pushed back by the homes, cachesim.py:330-339 codes). */
 size_t bgl_compact_codes_workspace(int64_t max_n);
 int bgl_compact_codes(const uint8_t* codes, const int64_t* n_dev, int64_t max_n, int32_t min_code,
                       int32_t* pos_out, int64_t* count_out, void* workspace, void* stream);

@@ -5,14 +5,14 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 Follows `gnnio/cachesim.py`:
   * ring-buffer level: `slots` (-1 = empty), residency map, `tail`; insert is a
     no-op for capacity 0 or an already-resident node, otherwise evicts the
-    occupant of `slots[tail]`, writes, advances tail          (cachesim.py:81-107 / 267-293)
+    occupant of `slots[tail]`, writes, advances tail          (cachesim.py:81-107)
   * engine: d device levels (node n lives on n % d) + one shared host level
-                                                             (cachesim.py:190-203 / 383-389)
+                                                             (cachesim.py:190-203)
   * simulate: per batch, worker = batch_devices[i] or i % d; every node is
     classified against the pre-batch state as D (own device), P (peer
     device), H (host) or M (miss); after the batch the device-missed nodes
     (ascending) go to their home level and the full misses (ascending) to the
-    host level; per-batch counters                       (cachesim.py:461-549)
+    host level; per-batch counters                       (cachesim.py:275-363)
 
 `FifoEngine` is the literal sequential restatement; `simulate_batched` is the
 batch-parallel closed form the CUDA kernels implement.
@@ -27,7 +27,7 @@ CODE_CHARS = "DPHM"
 
 
 class FifoRing:
-    """One FIFO level (cachesim.py:267-293)."""
+    """One FIFO level (cachesim.py:81-107)."""
 
     def __init__(self, capacity: int):
         self.capacity = int(capacity)
@@ -57,7 +57,7 @@ class FifoRing:
 
 
 class FifoEngine:
-    """d device rings + a shared host ring (cachesim.py:376-389)."""
+    """d device rings + a shared host ring (cachesim.py:190-203)."""
 
     def __init__(self, device_capacity: int, host_capacity: int, num_devices: int):
         self.devices = [FifoRing(device_capacity) for _ in range(num_devices)]
@@ -159,7 +159,7 @@ def simulate_batched(batches, device_capacity, host_capacity, num_devices,
     return counters, codes_all, (dev_slots, dev_tails, host_slots, host_tail)
 
 
-# -- static-degree baseline (cachesim.py:250-265, 392-410) ----------------------------
+# -- static-degree baseline (cachesim.py:64-79, 206-224) ----------------------------
 
 def static_warm(row_offsets, device_capacity, host_capacity, num_devices):
     """Per device the `device_capacity` highest-degree owned nodes (ties to the

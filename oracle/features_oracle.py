@@ -4,7 +4,7 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 
 The reference never materialises features (`gnnio/graph.py:3-6`); it only
 counts bytes (`feature_bytes_per_node = 4 * feature_dim`, graph.py:41-43;
-peer / host / remote bytes, cachesim.py:447-458). The retrieval contract the
+peer / host / remote bytes, cachesim.py:261-272). The retrieval contract the
 build adds is `rows[i] = F[trace.batches[b][i]]`, byte-exact.
 
 `synthetic_features` restates the counter hash the product's synthetic

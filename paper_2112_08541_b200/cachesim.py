@@ -1,10 +1,10 @@
 """Dynamic FIFO feature cache on the B200 (drop-in for gnnio.cachesim).
 
 Same public surface as the reference module (`gnnio/cachesim.py`):
-`POLICIES` (:208), `CacheConfig` (:211-225), `CacheEngineState` (:376-380),
-`cold_state` (:383-389), `warm_static` (:392-410), `CacheSimReport`
-(:413-458), `simulate` (:461-549), `amortized_update_ops` (:552-561),
-`compare_policies` (:564-595).
+`POLICIES` (:22), `CacheConfig` (:25-39), `CacheEngineState` (:190-194),
+`cold_state` (:197-203), `warm_static` (:206-224), `CacheSimReport`
+(:227-272), `simulate` (:275-363), `amortized_update_ops` (:366-375),
+`compare_policies` (:378-409).
 
 The FIFO policy -- BGL's cache -- runs on the device (`bgl_cache_*`):
 per-batch classification against the pre-batch state, insert-after-batch in
@@ -105,7 +105,7 @@ class FifoCacheDevice:
 class FifoLevelView:
     """Read-only view of one ring with the FifoLevel attributes the reference
     exposes (`capacity`, `slots`, `tail`, `__contains__`, `__len__`,
-    cachesim.py:267-293). Reading synchronises with the device."""
+    cachesim.py:81-107). Reading synchronises with the device."""
 
     def __init__(self, state: "CacheEngineState", level: int):
         self._state = state
@@ -132,7 +132,7 @@ class FifoLevelView:
 
     @property
     def resident(self) -> frozenset:
-        """Resident node set (StaticLevel.resident, cachesim.py:255)."""
+        """Resident node set (StaticLevel.resident, cachesim.py:69)."""
         s = self.slots
         return frozenset(int(v) for v in s[s >= 0])
 
@@ -151,7 +151,7 @@ class FifoLevelView:
 @dataclass
 class CacheEngineState:
     """Device-resident cache state (the reference's CacheEngineState,
-    cachesim.py:376-380); `devices[h]` / `host` are views of the rings."""
+    cachesim.py:190-194); `devices[h]` / `host` are views of the rings."""
 
     cfg: CacheConfig
     engine: FifoCacheDevice
@@ -167,7 +167,7 @@ class CacheEngineState:
 
 
 def cold_state(cfg: CacheConfig, num_nodes: int = 1, row_bytes: int = 0) -> CacheEngineState:
-    """Empty caches (cachesim.py:383-389). The index grows on demand."""
+    """Empty caches (cachesim.py:197-203). The index grows on demand."""
     if cfg.policy == "static-degree":
         raise ValueError("static policy requires warm_static(g, cfg)")
     if cfg.policy != "fifo":
@@ -177,7 +177,7 @@ def cold_state(cfg: CacheConfig, num_nodes: int = 1, row_bytes: int = 0) -> Cach
 
 def _top_degree(dg, num_shards: int, capacity: int, exclude: torch.Tensor | None):
     """Per shard (v % num_shards) the `capacity` highest-degree nodes, ties to
-    the lower ID (np.lexsort((owned, -degs[owned])), cachesim.py:403-404),
+    the lower ID (np.lexsort((owned, -degs[owned])), cachesim.py:217-218),
     without a sort: degree histogram -> threshold degree t_h and the number
     of degree-t_h nodes still needed; ties ranked by ascending ID.
     Returns (device int32 nodes, shard by shard, each ascending; counts)."""
@@ -228,7 +228,7 @@ def _top_degree(dg, num_shards: int, capacity: int, exclude: torch.Tensor | None
 
 def warm_static(g, cfg: CacheConfig) -> CacheEngineState:
     """Pre-load every device level with the highest-degree nodes it owns and
-    the host level with the next-highest-degree nodes (cachesim.py:392-410),
+    the host level with the next-highest-degree nodes (cachesim.py:206-224),
     computed on the device; the levels never change afterwards."""
     if cfg.policy != "static-degree":
         raise ValueError("warm_static requires policy='static-degree'")
@@ -325,7 +325,7 @@ class _UniqueScratch:
 def simulate(trace, cfg: CacheConfig, g=None, batch_devices=None, state: CacheEngineState | None = None,
              record_outcomes: bool = False) -> CacheSimReport:
     """Replay an access trace through the two-level multi-device cache
-    (cachesim.py:461-549)."""
+    (cachesim.py:275-363)."""
     static = cfg.policy == "static-degree"
     if static:
         if state is None:
@@ -374,7 +374,7 @@ def simulate(trace, cfg: CacheConfig, g=None, batch_devices=None, state: CacheEn
         bptr = ids.data_ptr() + 4 * int(offs[i])
         nptr = lens.data_ptr() + 8 * i
         cptr = counters.data_ptr() + 64 * i
-        # sorted distinct set of the batch = the insert order (cachesim.py:527-530)
+        # sorted distinct set of the batch = the insert order (cachesim.py:341-344)
         _lib.check(lib.bgl_unique_sorted(bptr, 1, c_off, nptr, (_lib.c_i64 * 1)(n), eng.num_nodes,
                                          scratch.ws.data_ptr(), scratch.uniq.data_ptr(),
                                          scratch.count.data_ptr(), st))
@@ -382,7 +382,7 @@ def simulate(trace, cfg: CacheConfig, g=None, batch_devices=None, state: CacheEn
                                         scratch.count.data_ptr(), n,
                                         None if codes is None else codes.data_ptr() + int(offs[i]),
                                         None, cptr, st))
-        if not static:                         # static levels never change (StaticLevel.insert, cachesim.py:260-261)
+        if not static:                         # static levels never change (StaticLevel.insert, cachesim.py:74-75)
             _lib.check(lib.bgl_cache_insert(eng.handle, scratch.uniq.data_ptr(), n, None, cptr, st))
         _lib.check(lib.bgl_unique_reset(scratch.ws.data_ptr(), eng.num_nodes, scratch.uniq.data_ptr(),
                                         scratch.count.data_ptr(), n, st))
@@ -395,7 +395,7 @@ def simulate(trace, cfg: CacheConfig, g=None, batch_devices=None, state: CacheEn
 
 
 def amortized_update_ops(report: CacheSimReport) -> dict[str, float]:
-    """Per-batch mean operation counts (cachesim.py:552-561)."""
+    """Per-batch mean operation counts (cachesim.py:366-375)."""
     nb = max(1, len(report.batch_queries))
     return {
         "lookups_per_batch": report.total_queries / nb,
@@ -407,7 +407,7 @@ def amortized_update_ops(report: CacheSimReport) -> dict[str, float]:
 
 def compare_policies(g, trace, capacities, policies=("static-degree", "fifo"), num_devices: int = 1, host_capacity: int = 0,
                      feature_bytes_per_node: int = 512) -> list[dict]:
-    """Hit-ratio table over a (policy x capacity) sweep (cachesim.py:564-595).
+    """Hit-ratio table over a (policy x capacity) sweep (cachesim.py:378-409).
     The device runs the static-degree and FIFO cells (the default sweep)."""
     rows = []
     for policy in policies:

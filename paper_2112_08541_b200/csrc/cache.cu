@@ -1,5 +1,5 @@
 // K3/K4: BGL's dynamic FIFO feature cache, bit-exact with gnnio.cachesim's
-// FIFO policy (FifoLevel cachesim.py:267-293; simulate cachesim.py:461-549).
+// FIFO policy (FifoLevel cachesim.py:81-107; simulate cachesim.py:275-363).
 //
 // State (all device-resident):
 //   rings   int32 [d][C]   node in each slot, -1 empty   (FifoLevel.slots)

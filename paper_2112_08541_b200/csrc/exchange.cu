@@ -1,7 +1,7 @@
 // Multi-GPU exchange helpers for the node-ID-sharded cache (home of node v is
-// GPU v % H, gnnio/cachesim.py:505-506):
+// GPU v % H, gnnio/cachesim.py:319-320):
 //   partition  stable split of a sorted batch by home -> H ascending buckets
-//              (the insert order each home needs, cachesim.py:527-528) and the
+//              (the insert order each home needs, cachesim.py:341-342) and the
 //              position of every bucketed ID in the batch;
 //   scatter    rows returned by the homes back into batch order;
 //   compact    positions of a batch whose outcome code is >= a threshold

@@ -1,5 +1,5 @@
 // K5/K6: feature-row gather for a mini-batch (net-new: the reference only
-// counts bytes, cachesim.py:447-458; contract rows[i] = F[batch[i]]).
+// counts bytes, cachesim.py:261-272; contract rows[i] = F[batch[i]]).
 //
 // out[i] = src_row[i] >= 0 ? ring_rows[src_row[i]]   (cache hit, HBM)
 //                          : table[ids[i]]            (miss: zero-copy read of

@@ -1,5 +1,5 @@
 // Static-degree cache warm-up on the device (gnnio.cachesim.warm_static,
-// cachesim.py:392-410): per shard h (nodes v % d == h) the `capacity`
+// cachesim.py:206-224): per shard h (nodes v % d == h) the `capacity`
 // highest-degree nodes, ties to the lower ID; then the host level takes the
 // highest-degree nodes among the rest. Sort-free: a per-shard degree
 // histogram gives each shard's threshold degree t_h and how many nodes of

@@ -1,14 +1,14 @@
 """Node-ID-sharded FIFO feature cache across GPUs (one process per GPU).
 
 The reference routes every queried node to its home device `v % d`
-(cachesim.py:505-506): a hit on the worker's own device is D, on another
+(cachesim.py:319-320): a hit on the worker's own device is D, on another
 device P (peer), and device misses are inserted into their home level after
-the batch in ascending ID order (cachesim.py:527-528). The reference only
+the batch in ascending ID order (cachesim.py:341-342). The reference only
 *simulates* the d devices in one loop; here the d levels are d GPUs:
 
   round j: rank w samples batch i = j*d + w (batch rng keyed by i, so the
            sampler needs no exchange; worker of batch i is i % d as in
-           cachesim.py:495)
+           cachesim.py:309)
     1. partition   stable split of the sorted distinct IDs by home
                    (bgl_partition_by_home) -> d ascending buckets
     2. exchange    bucket sizes + IDs, NCCL all-to-all (the only data the
@@ -21,7 +21,7 @@ the batch in ascending ID order (cachesim.py:527-528). The reference only
     4. return      rows (+ outcome codes) back to the workers, all-to-all
     5. scatter     rows into batch order (bgl_scatter_rows)
 
-The host level of the reference is a single shared level (cachesim.py:388);
+The host level of the reference is a single shared level (cachesim.py:202);
 it is not sharded, so the multi-GPU engine requires host_capacity == 0 (the
 single-process engine covers it exactly).
 
@@ -270,13 +270,13 @@ def ipc_map(tensors, rank: int, world: int, group=None) -> list[list[int]]:
 
 class ShardedPipeline:
     """Pipelined, host-sync-free rounds of the node-ID-sharded cache; one
-    process per GPU (rank = home shard `rank` of `world`, cachesim.py:505-506).
+    process per GPU (rank = home shard `rank` of `world`, cachesim.py:319-320).
 
-    Round j, rank w = worker of batch i = j*world + w (cachesim.py:495). Its
+    Round j, rank w = worker of batch i = j*world + w (cachesim.py:309). Its
     stages:
       S(j)   sample the batch (side stream)
       X(j)   bgl_partition_push: bucket h of the sorted distinct IDs
-             (ascending = the insert order, cachesim.py:527-528) and the IDs'
+             (ascending = the insert order, cachesim.py:341-342) and the IDs'
              batch positions stored straight into home h's receive area over
              peer memory; then a barrier (NCCL all-reduce of one int -- the
              only collective on the data path)
@@ -302,8 +302,10 @@ class ShardedPipeline:
     worker's output; B(j) copies the survivors into the ring from there (a
     peer read of the miss bytes over NVLink). No host synchronisation:
     counts stay on the device and every launch is sized for the worst case.
-    Rows of round j are complete after step j (Z(j)) in out_rows[j % 3] and
-    stay valid until step j + 2 begins. `barrier` defaults to an NCCL
+    Rows of round j are complete after step j (Z(j)) in out_rows[j % 3];
+    round j's results (rows, codes, distinct IDs) are valid only until step
+    j + 1 is enqueued: that step's LI(j + 3) rewrites the codes of set j % 3
+    and its S(j + 4) the sampler slot (j % 4) holding round j's distinct IDs. `barrier` defaults to an NCCL
     all-reduce on the current stream; tests that put several processes on
     one GPU pass a host barrier.
     """
@@ -318,7 +320,8 @@ class ShardedPipeline:
         self.b = int(batch_size)
         self.order = order.to(device="cuda", dtype=torch.int32).contiguous()
         total = int(self.order.numel())
-        self.num_batches = int(num_batches or (total + self.b - 1) // self.b)
+        from .pipeline import check_num_batches
+        self.num_batches = check_num_batches(num_batches, total, self.b)
         self.samplers = [BatchSampler(dg, fanouts, self.b, rng=rng, frontier_outputs=False) for _ in range(self.NSMP)]
         maxu = self.maxu = self.samplers[0].max_uniq
         self.dim = features.shape[1]
@@ -498,7 +501,8 @@ class ShardedPipeline:
                 out_w = self.worker_rows[w] + r * maxu * rb
                 if not self._in_graph:
                     self.s_back.wait_event(self.miss_done[r][w])
-                _lib.check(lib.bgl_gather_rows_push(self.recv_ids[r, w].data_ptr(), self.src_row[r, w].data_ptr(),
+                _lib.check(lib.bgl_gather_rows_push(self.recv_ids[r, w].data_ptr(),
+                                                    self.src_row[r, w].data_ptr() if ring else None,
                                                     cnt.data_ptr(), maxu, ring, eng.table, rb, None, out_w,
                                                     self.recv_pos[r, w].data_ptr(), 1, 0, st))
                 if ring:   # survivors' rows into their ring slots, read back from worker w's output
@@ -521,6 +525,13 @@ class ShardedPipeline:
         self._M(0)
         self._X(1)
         self._LI(1)
+        # step 0 runs M(1), which reads the codes every home pushed in LI(1), and
+        # B(0), which reads every worker's M(0) rows: join both side streams and
+        # put a barrier behind them, as before M(0) (the end-of-step barrier
+        # gives the same ordering to every later step)
+        main.wait_stream(self.s_li)
+        main.wait_stream(self.s_miss)
+        self.barrier()
         self.primed = True
 
     PHASES = 12            # lcm(NR, NSMP): one captured graph per step phase

@@ -1,7 +1,7 @@
 """Feature retrieval through BGL's dynamic FIFO cache (net-new API).
 
 The reference never materialises features (`gnnio/graph.py:3-6`); it counts
-the bytes a batch would move (`cachesim.py:447-458`). This module adds the
+the bytes a batch would move (`cachesim.py:261-272`). This module adds the
 retrieval the paper describes without changing
 `simulate`'s signature: `FeatureCacheEngine.state` is a `CacheEngineState`,
 so `cachesim.simulate(trace, cfg, state=engine.state)` drives the same
@@ -124,6 +124,14 @@ class FeatureCacheEngine:
         # runs of consecutive IDs as TMA bulk copies (bgl_gather_spans); "0": per-row loads only
         self.miss_spans = os.environ.get("BGL_MISS_SPANS", "1") != "0"
 
+    def _ring_src(self, src_row: torch.Tensor):
+        """(ring rows pointer, src_row pointer) for the gathers. A cache of
+        device_capacity 0 (allowed by CacheConfig, cachesim.py:38-39) has no
+        ring rows and no hits: every row comes from the table, so no src_row
+        is passed either."""
+        ring = self.dev.rows_ptr() or None
+        return ring, (src_row.data_ptr() if ring else None)
+
     def retrieve_device(self, ids: torch.Tensor, n_dev: torch.Tensor, max_n: int, worker: int,
                         counters: torch.Tensor | None = None, stream=None, out: torch.Tensor | None = None,
                         events=None, codes: torch.Tensor | None = None):
@@ -142,16 +150,16 @@ class FeatureCacheEngine:
                                         cnt, st))
         if events is not None:
             events[0].record()
-        ring = self.dev.rows_ptr() or None
+        ring, src = self._ring_src(self.src_row)
         if self.features.is_cuda:
-            _lib.check(lib.bgl_gather_rows(ids.data_ptr(), self.src_row.data_ptr(), n_dev.data_ptr(), max_n, ring,
+            _lib.check(lib.bgl_gather_rows(ids.data_ptr(), src, n_dev.data_ptr(), max_n, ring,
                                            self.table, self.row_bytes, out.data_ptr(), 0, 0, st))
         else:
             # hits from HBM with the whole GPU, then misses over the host link
             # with ~150 warps (keeps the SMs free for the overlapped sampler)
-            _lib.check(lib.bgl_gather_rows(ids.data_ptr(), self.src_row.data_ptr(), n_dev.data_ptr(), max_n, ring,
+            _lib.check(lib.bgl_gather_rows(ids.data_ptr(), src, n_dev.data_ptr(), max_n, ring,
                                            self.table, self.row_bytes, out.data_ptr(), 1, 0, st))
-            _lib.check(lib.bgl_gather_rows(ids.data_ptr(), self.src_row.data_ptr(), n_dev.data_ptr(), max_n, ring,
+            _lib.check(lib.bgl_gather_rows(ids.data_ptr(), src, n_dev.data_ptr(), max_n, ring,
                                            self.table, self.row_bytes, out.data_ptr(), 2, self.miss_ctas, st))
         if events is not None:
             events[1].record()
@@ -171,10 +179,10 @@ class FeatureCacheEngine:
         _lib.check(lib.bgl_cache_lookup(h, ids.data_ptr(), n_dev.data_ptr(), max_n, worker, ids.data_ptr(),
                                         n_dev.data_ptr(), max_n, codes.data_ptr(), self.src_row.data_ptr(),
                                         counters.data_ptr(), st))
-        ring = self.dev.rows_ptr() or None
+        ring, src = self._ring_src(self.src_row)
         passes = [(0, 0)] if self.features.is_cuda else [(1, 0), (2, self.miss_ctas)]
         for mode, ctas in passes:
-            _lib.check(lib.bgl_gather_rows_push(ids.data_ptr(), self.src_row.data_ptr(), n_dev.data_ptr(), max_n,
+            _lib.check(lib.bgl_gather_rows_push(ids.data_ptr(), src, n_dev.data_ptr(), max_n,
                                                 ring, self.table, self.row_bytes, out.data_ptr(), push_rows,
                                                 push_pos.data_ptr(), mode, ctas, st))
         _lib.check(lib.bgl_cache_insert(h, ids.data_ptr(), max_n, out.data_ptr(), counters.data_ptr(), st))
@@ -217,9 +225,9 @@ class FeatureCacheEngine:
                                            self.table, self.row_bytes, out.data_ptr(), None, None,
                                            self.miss_rows_in_flight, ctas, st))
             return
-        _lib.check(lib.bgl_gather_rows(ids.data_ptr(), src_row.data_ptr(), n_dev.data_ptr(), max_n,
-                                       self.dev.rows_ptr() or None, self.table, self.row_bytes, out.data_ptr(), 2,
-                                       ctas, st))
+        ring, src = self._ring_src(src_row)
+        _lib.check(lib.bgl_gather_rows(ids.data_ptr(), src, n_dev.data_ptr(), max_n, ring, self.table,
+                                       self.row_bytes, out.data_ptr(), 2, ctas, st))
 
     def back(self, ids, n_dev, max_n, out, src_row, plan, plan_count, stream=None, events=None,
              with_misses: bool = False):
@@ -229,9 +237,9 @@ class FeatureCacheEngine:
         hazard)."""
         lib = _lib.load()
         st = _lib.stream_ptr(stream)
-        _lib.check(lib.bgl_gather_rows(ids.data_ptr(), src_row.data_ptr(), n_dev.data_ptr(), max_n,
-                                       self.dev.rows_ptr() or None, self.table, self.row_bytes, out.data_ptr(),
-                                       0 if with_misses else 1, 0, st))
+        ring, src = self._ring_src(src_row)
+        _lib.check(lib.bgl_gather_rows(ids.data_ptr(), src, n_dev.data_ptr(), max_n, ring, self.table,
+                                       self.row_bytes, out.data_ptr(), 0 if with_misses else 1, 0, st))
         if events is not None:
             events[0].record()
         if self.dev.rows_ptr():

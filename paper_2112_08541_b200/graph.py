@@ -55,6 +55,25 @@ class Graph:
     def num_train(self) -> int:
         return int(self.train_mask.sum())
 
+    def validate(self) -> None:
+        """Check the CSR invariants of graph.py:62-75; raises AssertionError
+        on violation (vectorised: the same checks as the reference's per-node
+        loop, with the same messages)."""
+        off, col = np.asarray(self.row_offsets), np.asarray(self.col_indices)
+        assert off[0] == 0 and off[-1] == self.num_edges
+        assert len(off) == self.num_nodes + 1
+        assert np.all(np.diff(off) >= 0)
+        if self.num_edges:
+            assert col.min() >= 0 and col.max() < self.num_nodes
+            row = np.repeat(np.arange(self.num_nodes, dtype=np.int64), np.diff(off))
+            same = row[1:] == row[:-1]
+            bad = np.flatnonzero(same & (np.diff(col.astype(np.int64)) <= 0))
+            assert bad.size == 0, f"adjacency of {int(row[bad[0] + 1]) if bad.size else -1} not sorted/deduped"
+            loops = np.flatnonzero(col == row)
+            assert loops.size == 0, f"self-loop at {int(row[loops[0]]) if loops.size else -1}"
+        if self.labels is not None:
+            assert np.all(self.labels[self.train_mask] >= 0)
+
 
 class DeviceGraph:
     """CSR in HBM: indptr int64[n+1], indices int32[E]."""
@@ -84,7 +103,7 @@ class DeviceGraph:
 
     def to_host(self) -> Graph:
         ro = self.indptr.cpu().numpy()
-        ci = self.indices.cpu().numpy()
+        ci = self.indices.cpu().numpy().astype(np.int64)      # the reference's dtype (graph.py:31)
         tm = self.train_mask.cpu().numpy() if self.train_mask is not None else None
         lb = self.labels.cpu().numpy() if self.labels is not None else None
         return Graph(self.num_nodes, int(ci.size), ro, ci, labels=lb, train_mask=tm)

@@ -52,6 +52,21 @@ NF = 2                 # host-fed seed buffers
 PHASES = 30            # lcm(NS, NB, NF)
 
 
+def check_num_batches(num_batches, total: int, b: int) -> int:
+    """Batches per epoch of a schedule of `total` seeds in batches of `b`
+    (the last may be short, ordering.py:148-151). An explicit count beyond
+    ceil(total / b) would stage batches past the schedule's end."""
+    if b < 1:
+        raise ValueError("batch_size must be >= 1")
+    full = (total + b - 1) // b
+    if full < 1:
+        raise ValueError("empty schedule")
+    nb = int(num_batches or full)
+    if not 1 <= nb <= full:
+        raise ValueError(f"num_batches must be in [1, {full}] for {total} seeds in batches of {b}")
+    return nb
+
+
 class MiniBatchPipeline:
     lookahead = 4      # batch k+4 is staged (and its first hops sampled) during step k
 
@@ -64,7 +79,7 @@ class MiniBatchPipeline:
         self.b = int(batch_size)
         self.order = order.to(device="cuda", dtype=torch.int32).contiguous()
         total = int(self.order.numel())
-        self.num_batches = int(num_batches or (total + self.b - 1) // self.b)
+        self.num_batches = check_num_batches(num_batches, total, self.b)
         self.samplers = [BatchSampler(dg, fanouts, self.b, max_ctas=sampler_ctas, rng=rng, frontier_outputs=False)
                          for _ in range(NS)]
         self.max_uniq = self.samplers[0].max_uniq

@@ -13,7 +13,7 @@ What is pinned (the reference ships no golden arrays):
     as `sample_batch` does (sampler.py:97-116), `sample_batch`'s distinct set,
     and `simulate_epoch` traces + EpochCommReport (sampler.py:119-167);
   * cache: per-batch counters, per-node outcome codes and the ring contents +
-    tail of every level after every batch (cachesim.py:81-107, 461-549);
+    tail of every level after every batch (cachesim.py:81-107, 275-363);
   * ordering: `generate_bfs_sequences`, `proximity_schedule`,
     `random_shuffle_schedule` (ordering.py:57-207).
 """
@@ -433,12 +433,60 @@ def make_c2(nbatches: int = 3):
     np.savez_compressed(os.path.join(HERE, "c2.npz"), **out)
 
 
+def digest(a) -> int:
+    """Order-sensitive 61-bit polynomial digest of an int array (the C2 window
+    fixture stores digests instead of ~30 MB of raw rows)."""
+    a = np.asarray(a, dtype=np.int64).ravel()
+    w = np.arange(a.size, dtype=np.int64) % 1000003 + 1
+    return int(((a % (1 << 31)) * w).sum() % ((1 << 61) - 1))
+
+
+_C2 = {}
+
+
+def _c2_sample(i):
+    g, sched, cfg = _C2["g"], _C2["sched"], _C2["cfg"]
+    return sp.sample_batch(g, sched.batches[i], cfg, batch_seed=i)[1]
+
+
+def make_c2_window(nbatches: int = 25, procs: int = 0):
+    """The bench's whole default window (W=5 warm-up + K=20 timed batches of
+    BASELINE.json configs[1]) by the reference itself: same graph / schedule /
+    sampler / FIFO as make_c2 for batches 0..nbatches-1 (sample_batch over a
+    process pool, batches are independent: SPEC.md:355), stored as per-batch
+    sizes, sums and digests of the trace row and of the outcome codes, plus the
+    counters and the ring's tail + a digest of its slots after the window."""
+    import multiprocessing as mp
+    g = generate_power_law(2_400_000, 51, seed=1, train_fraction=0.08, num_labels=47)
+    sched = od.proximity_schedule(g, 4, 1024, seed=1)
+    cfg = sp.SamplingConfig(fanouts=(15, 10, 5), batch_size=1024, seed=1)
+    _C2.update(g=g, sched=sched, cfg=cfg)
+    with mp.get_context("fork").Pool(procs or os.cpu_count()) as pool:
+        batches = pool.map(_c2_sample, range(nbatches), chunksize=1)
+    state = cs.cold_state(cs.CacheConfig(device_capacity=240_000, policy="fifo", feature_bytes_per_node=400))
+    rep = cs.simulate(sp.AccessTrace(batches=batches),
+                      cs.CacheConfig(device_capacity=240_000, policy="fifo", feature_bytes_per_node=400),
+                      state=state, record_outcomes=True)
+    codes = [np.array(["DPHM".index(c) for c in o], dtype=np.int64) for o in rep.outcomes]
+    out = {"size": np.array([b.size for b in batches], dtype=np.int64),
+           "sum": np.array([int(b.sum()) for b in batches], dtype=np.int64),
+           "trace_digest": np.array([digest(b) for b in batches], dtype=np.int64),
+           "codes_digest": np.array([digest(c) for c in codes], dtype=np.int64),
+           "counters": np.array([rep.batch_queries, rep.batch_own_hits, rep.batch_peer_hits, rep.batch_host_hits,
+                                 rep.batch_misses, rep.batch_insertions, rep.batch_evictions], dtype=np.int64).T,
+           "ring_tail": np.array([state.devices[0].tail], dtype=np.int64),
+           "ring_digest": np.array([digest(state.devices[0].slots)], dtype=np.int64),
+           "schedule_digest": np.array([digest(np.concatenate(sched.batches))], dtype=np.int64)}
+    np.savez_compressed(os.path.join(HERE, "c2_window.npz"), **out)
+
+
 if __name__ == "__main__":
-    parts = sys.argv[1:] or ["sampler", "cache", "ordering", "static", "shuffle", "graphgen", "c1", "c2", "policies"]
+    parts = sys.argv[1:] or ["sampler", "cache", "ordering", "static", "shuffle", "graphgen", "c1", "c2", "policies",
+                             "c2_window"]
     gs = graphs()
     makers = {"sampler": lambda: make_sampler(gs), "cache": make_cache, "ordering": lambda: make_ordering(gs),
               "static": lambda: make_static(gs), "shuffle": lambda: make_shuffle(gs), "graphgen": make_graphgen,
-              "c1": make_c1, "c2": make_c2, "policies": lambda: make_policies(gs)}
+              "c1": make_c1, "c2": make_c2, "policies": lambda: make_policies(gs), "c2_window": make_c2_window}
     for part in parts:
         makers[part]()
         f = part + ".npz"

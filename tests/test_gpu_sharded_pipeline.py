@@ -6,7 +6,7 @@ rows come back through the homes' pushes, each worker fetches its own misses;
 a host barrier stands in for the NCCL one (NCCL cannot put two ranks on one
 GPU). Every round's distinct set, per-node outcome codes and rows must equal
 the reference: the oracle sampler + the reference's d-device FIFO simulation
-(cachesim.py:461-549) + F[ids]."""
+(cachesim.py:275-363) + F[ids]."""
 
 import os
 import socket

@@ -109,7 +109,7 @@ def test_fifo_sequential_oracle_matches_reference(golden):
             c, cd = eng.run([b], [bd[i] if bd else i % d])
             assert np.array_equal(cd[0], codes[i])
             assert np.array_equal(c[0], cnt[i][:7])
-            assert cnt[i][7] == 0   # FIFO never updates metadata (cachesim.py:240-241)
+            assert cnt[i][7] == 0   # FIFO never updates metadata (cachesim.py:49, 94-104)
             assert np.array_equal(np.concatenate([r.slots for r in eng.devices]) if cap else np.empty(0), dsl[i])
             assert [r.tail for r in eng.devices] == dtl[i].tolist()
             assert np.array_equal(eng.host.slots, hsl[i])
