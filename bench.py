@@ -218,41 +218,200 @@ def host_link_zero_copy_peak_gbs(feats, rb):
 
 # ----------------------------------------------------------------------------- CPU reference
 
+def import_gnnio():
+    """The reference package itself: `baseline/_ref` (pip-installed from
+    /root/reference, travels to the GPU box with the snapshot), else the
+    read-only tree of the build container; None when neither exists (the
+    numpy oracle port stands in)."""
+    for p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(p, "gnnio")):
+            if p not in sys.path:
+                sys.path.insert(0, p)
+            import gnnio  # noqa: F401
+            from gnnio import cachesim, graph, ordering, sampler
+            return {"graph": graph, "sampler": sampler, "cachesim": cachesim, "ordering": ordering, "path": p}
+    return None
+
+
+def bench_config(cfg, args, world, csr_entries, max_degree, nb_total):
+    """The `config` object of the JSON line -- built the same way by every arm
+    (GPU single, GPU sharded, CPU reference) so the driver can compare them."""
+    return {"workload": workload_text(cfg, args.features, args.order), "graph": args.graph,
+            "num_nodes": cfg["n"], "csr_entries": int(csr_entries), "max_degree": int(max_degree),
+            "feature_dim": cfg["dim"], "fanouts": list(cfg["fanouts"]), "batch": cfg["b"],
+            "cache_rows_per_gpu": int(cfg["cache_frac"] * cfg["n"]) // world, "features": args.features,
+            "sampler_rng": args.rng, "ordering": args.order,
+            "parallelism": "single" if world == 1 else f"dp{world}: batch i on GPU i % {world}, node-ID-sharded "
+                                                       f"FIFO cache (home of v = v % {world})",
+            "l2": "flushed between timed steps (256 MB write, outside the events)",
+            "batches_per_epoch": int(nb_total)}
+
+
 _REF = {}
 
 
 def _ref_sample(i):
-    from oracle import sampler_oracle as so
+    """One mini-batch's sampling by the reference: gnnio sample_batch keyed
+    like simulate_epoch (batch_seed = batch index, sampler.py:138)."""
     r = _REF
-    _, _, distinct, _ = so.sample_batch(r["off"], r["col"], r["batches"][i], r["fanouts"], RUN_SEED, i)
-    return distinct
+    nb = len(r["batches"])
+    if r["gnnio"] is not None:
+        sp = r["gnnio"]["sampler"]
+        return sp.sample_batch(r["g"], r["batches"][i % nb], r["scfg"], batch_seed=i % nb)[1]
+    from oracle import sampler_oracle as so
+    return so.sample_batch(r["off"], r["col"], r["batches"][i % nb], r["fanouts"], RUN_SEED, i % nb)[2]
 
 
-def cpu_reference(hg, batches, cfg, feats_host, idx, cores):
-    """Reference algorithm on the host: sampler (per batch, `cores` processes),
-    FIFO cache (sequential state machine, 1 core), numpy gather."""
-    import multiprocessing as mp
-    from oracle import cache_oracle as co
-    _REF.update(off=hg.row_offsets, col=hg.col_indices, batches=batches, fanouts=cfg["fanouts"])
-    fifo = co.FifoEngine(int(cfg["cache_frac"] * cfg["n"]), 0, 1)
-    t0 = time.time()
-    if cores > 1:
-        with mp.get_context("fork").Pool(cores) as pool:
-            traces = pool.map(_ref_sample, idx, chunksize=1)
-    else:
-        traces = [_ref_sample(i) for i in idx]
-    t1 = time.time()
-    fb = 0
-    for tr in traces:
-        fifo.run([tr], [0])
-        rows = feats_host[tr]
-        fb += rows.nbytes
-    t2 = time.time()
-    return {"batches": len(idx), "seconds": t2 - t0, "sample_s": t1 - t0, "cache_gather_s": t2 - t1,
-            "feature_bytes": fb}
+class RefPath:
+    """The reference's per-mini-batch path on the host CPU, on the same inputs
+    as the GPU arm: graph = gnnio.graph.generate_power_law's (built by the C
+    restatement oracle/powerlaw_ref.c, bit-identical, seconds instead of ~10
+    minutes), features = the same hashed fp32 table, schedule = gnnio's own
+    proximity_schedule / random_shuffle_schedule. One mini-batch =
+    gnnio sample_batch (sampler.py:97-116) -> gnnio simulate(FIFO) on the
+    persistent state (cachesim.py:275-363) -> numpy gather F[distinct]."""
+
+    def __init__(self, cfg, args, arrays=None, order=None, feats=None, world: int = 1):
+        from oracle import features_oracle as fo
+        from oracle import graph_oracle as go
+        self.ref = import_gnnio()
+        self.cfg = cfg
+        n, dim = cfg["n"], cfg["dim"]
+        t0 = time.time()
+        if arrays is None:
+            if args.graph != "exact":
+                raise SystemExit("--impl reference builds the reference's own graph (--graph exact)")
+            off, col, train, labels = go.generate_power_law_c(n, cfg["avg_degree"], GRAPH_SEED, cfg["train"],
+                                                              cfg["labels"])
+        else:
+            off, col, train, labels = arrays
+        t1 = time.time()
+        self.off, self.col, self.train = off, col, train
+        self.max_degree = int(np.diff(off).max()) if n else 0
+        if feats is None:
+            feats = np.empty((n, dim), dtype=np.float32)
+            step = 1 << 18
+            for lo in range(0, n, step):
+                hi = min(n, lo + step)
+                feats[lo:hi] = fo.synthetic_features(np.arange(lo, hi), dim, seed=GRAPH_SEED)
+        self.feats = feats
+        self.world = world
+        cap = int(cfg["cache_frac"] * n) // world     # per device, as the GPU arms shard it
+        t2 = time.time()
+        b = cfg["b"]
+        if self.ref is not None:
+            G = self.ref["graph"].Graph
+            self.g = G(num_nodes=n, num_edges=int(col.size), row_offsets=off, col_indices=col, labels=labels,
+                       train_mask=train, feature_dim=dim)
+            od = self.ref["ordering"]
+            if order is not None:
+                sched = [np.asarray(order[i:i + b], dtype=np.int64) for i in range(0, len(order), b)]
+            elif args.order == "random":
+                sched = od.random_shuffle_schedule(self.g, b, seed=RUN_SEED).batches
+            else:
+                sched = od.proximity_schedule(self.g, cfg["S"], b, seed=RUN_SEED).batches
+            self.scfg = self.ref["sampler"].SamplingConfig(fanouts=tuple(cfg["fanouts"]), batch_size=b, seed=RUN_SEED)
+            cs = self.ref["cachesim"]
+            self.ccfg = cs.CacheConfig(device_capacity=cap, num_devices=world, policy="fifo",
+                                       feature_bytes_per_node=dim * 4)
+            self.state = cs.cold_state(self.ccfg)
+            self.kind = "reference"
+        else:
+            from oracle import cache_oracle as co
+            from oracle import ordering_oracle as oo
+            self.g, self.scfg = None, None
+            if order is not None:
+                sched = [np.asarray(order[i:i + b], dtype=np.int64) for i in range(0, len(order), b)]
+            elif args.order == "random":
+                perm = np.random.default_rng(RUN_SEED).permutation(np.flatnonzero(train))
+                sched = [perm[i:i + b] for i in range(0, perm.size, b)]
+            else:
+                sched = oo.proximity_schedule(off, col, train, cfg["S"], b, RUN_SEED)
+            self.fifo = co.FifoEngine(cap, 0, world)
+            self.kind = "port"
+        self.batches = sched
+        _REF.update(gnnio=self.ref, g=self.g, scfg=self.scfg, batches=sched, off=off, col=col,
+                    fanouts=tuple(cfg["fanouts"]))
+        self.setup = {"graph_s": round(t1 - t0, 2), "features_s": round(t2 - t1, 2),
+                      "schedule_s": round(time.time() - t2, 2)}
+
+    def what(self) -> str:
+        if self.kind == "reference":
+            return f"gnnio (the reference package, {self.ref['path']})"
+        return "the numpy oracle port of gnnio (reference package not found)"
+
+    def cache_and_gather(self, i: int, distinct) -> int:
+        """FIFO simulate of batch i on the persistent state (worker i % d,
+        cachesim.py:309) + F[distinct]."""
+        w = i % self.world
+        if self.kind == "reference":
+            sp, cs = self.ref["sampler"], self.ref["cachesim"]
+            cs.simulate(sp.AccessTrace(batches=[distinct]), self.ccfg, batch_devices=[w], state=self.state)
+        else:
+            self.fifo.run([distinct], [w])
+        rows = self.feats[distinct]
+        return int(rows.nbytes)
+
+    def run(self, idx, procs: int):
+        """Batches `idx` in order: sampling in a pool of `procs` processes
+        (batches are independent), the cache state machine and
+        the gather in this process in batch order as the samples arrive."""
+        import multiprocessing as mp
+        t0 = time.time()
+        fb, ts = 0, 0.0
+        if procs > 1:
+            with mp.get_context("fork").Pool(procs) as pool:
+                for i, d in zip(idx, pool.imap(_ref_sample, idx, chunksize=1)):
+                    t = time.time()
+                    fb += self.cache_and_gather(i, d)
+                    ts += time.time() - t
+        else:
+            for i in idx:
+                d = _ref_sample(i)
+                t = time.time()
+                fb += self.cache_and_gather(i, d)
+                ts += time.time() - t
+        return {"batches": len(idx), "seconds": time.time() - t0, "cache_gather_s": ts, "feature_bytes": fb}
+
+
+def host_procs(per_proc_gb: float) -> int:
+    """Worker processes for the reference sampler: every core this process may
+    run on, capped so the pool fits in the memory available."""
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except AttributeError:
+        cores = os.cpu_count() or 1
+    avail = None
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                avail = int(line.split()[1]) / 1e6
+    except OSError:
+        pass
+    if avail:
+        cores = max(1, min(cores, int(avail * 0.7 / per_proc_gb)))
+    return cores
 
 
 # ----------------------------------------------------------------------------- arms
+
+def cpu_baseline(cfg, args, dg, feats, order_host, nsample: int = 2):
+    """The reference's CPU path (gnnio sample_batch + simulate + numpy
+    gather, RefPath) timed on one core of this box on a bounded sample: the
+    first `nsample` timed batches of the same schedule after the warm-up
+    batches, on the same graph (copied from the device), features and cache."""
+    hg = dg.to_host()
+    fh = feats.cpu().numpy() if feats.is_cuda else feats.numpy()
+    rp = RefPath(cfg, args, arrays=(hg.row_offsets, hg.col_indices, hg.train_mask, hg.labels), order=order_host,
+                 feats=fh)
+    rp.run(list(range(args.warmup)), procs=1 if args.warmup <= 1 else min(args.warmup, host_procs(2.0)))
+    r = rp.run(list(range(args.warmup, args.warmup + nsample)), procs=1)
+    return {"value": round(r["batches"] / r["seconds"], 4), "unit": UNIT, "cores": 1, "kind": rp.kind,
+            "sample": f"batches {args.warmup}..{args.warmup + nsample - 1} of this schedule after the "
+                      f"{args.warmup} warm-up batches (their cache state replayed untimed): {rp.what()} "
+                      f"sample_batch + FIFO simulate + numpy F[distinct], 1 core, {r['seconds']:.1f}s "
+                      f"({r['cache_gather_s']:.2f}s cache + gather)"}
+
 
 def run_bgl(args, cfg):
     import torch
@@ -343,11 +502,19 @@ def run_bgl(args, cfg):
     gather_ms = statistics.mean(g_ms)
     host_bytes = statistics.mean(g_bytes_host)
     if args.features == "host":
-        achieved = host_bytes / (gather_ms * 1e-3) / 1e9
+        # the timed steps' own miss bytes over the timed time: the K lookups of
+        # the window (batches W+2 .. W+K+1; step k gathers batch k+1's misses,
+        # so the window's gathers are batches W+1 .. W+K: one batch shifted)
+        miss_bytes_timed = (d[3] + d[4]) * rb
+        achieved = miss_bytes_timed / (total_ms * 1e-3) / 1e9
+        kernel_alone = host_bytes / (gather_ms * 1e-3) / 1e9
         roof = {"bound": "host_link", "achieved": round(achieved, 2), "peak": round(peak_host, 2), "unit": "GB/s",
                 "frac": round(achieved / peak_host, 3),
                 "traffic": None, "kernel": "gather_span_kernel (compacted misses: TMA spans + 16-B zero-copy host reads)",
-                "algorithmic_bytes_per_launch": int(host_bytes),
+                "achieved_method": "H+M rows of the timed steps' lookups x row bytes / the timed steps' CUDA-event "
+                                   "time (the step is the miss gather, the other branches run beside it)",
+                "achieved_serialised_kernel": round(kernel_alone, 2),
+                "algorithmic_bytes_per_launch": int(miss_bytes_timed / max(args.steps, 1)),
                 "peak_source": "max over this run of the pinned host->device cudaMemcpy (256 MB, best of 8; at "
                                "start-up, before the timed region, after the stage breakdown: "
                                f"{[round(x, 2) for x in peak_samples]}) and a sequential zero-copy read of 256 MB "
@@ -436,13 +603,7 @@ def run_bgl(args, cfg):
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32 ids / u53 PCG64 keys / fp32 rows moved",
         "data": graph_data(cfg, args.graph),
-        "config": {"workload": workload_text(cfg, args.features, args.order), "graph": args.graph, "num_nodes": cfg["n"], "csr_entries": dg.num_edges,
-                   "max_degree": dg.max_degree, "feature_dim": cfg["dim"], "fanouts": list(cfg["fanouts"]),
-                   "batch": b, "cache_rows_per_gpu": cap, "features": args.features, "sampler_rng": args.rng,
-                   "ordering": args.order,
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
-                   "l2": "flushed between timed steps (256 MB write, outside the events)",
-                   "batches_per_epoch": nb_total},
+        "config": bench_config(cfg, args, world, dg.num_edges, dg.max_degree, nb_total),
         "feature_gbs": round(feat_gbs, 2), "hit_pct": round(100.0 * hits / max(queries, 1), 2),
         "rows_per_batch": round(queries / max(args.steps, 1) / 1, 1),
         "stages_ms": {k: round(statistics.mean(v), 4) for k, v in st_times.items()},
@@ -461,17 +622,7 @@ def run_bgl(args, cfg):
         "setup": dict(setup, torch_alloc_peak_gb=round(torch.cuda.max_memory_allocated() / 1e9, 2)),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from oracle import ordering_oracle  # noqa: F401  (the oracle is the checker/baseline only)
-        hg = dg.to_host()
-        batches = [order_host[i * b:(i + 1) * b].astype(np.int64) for i in range(nb_total)]
-        fh = feats.cpu().numpy() if feats.is_cuda else feats.numpy()
-        nsample = 2 if args.config == "c2" else 8
-        r = cpu_reference(hg, batches, cfg, fh, list(range(nsample)), cores=1)
-        out["cpu_baseline"] = {"value": round(r["batches"] / r["seconds"], 4), "unit": UNIT, "cores": 1,
-                               "kind": "port",
-                               "sample": f"{nsample} batches of this schedule: oracle sample_batch (numpy lexsort, "
-                                         f"sampler.py:65-116) {r['sample_s']:.1f}s + FIFO simulate + numpy F[ids] "
-                                         f"{r['cache_gather_s']:.2f}s, 1 core"}
+        out["cpu_baseline"] = cpu_baseline(cfg, args, dg, feats, order_host)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -480,14 +631,20 @@ def run_bgl(args, cfg):
 
 def run_sharded(args, cfg):
     """N GPUs, one process each: node-ID-sharded FIFO cache (home = v % N,
-    cachesim.py:319-320), rank w samples batches i = j*N + w. Default engine:
-    ShardedPipeline -- IDs pushed to the homes over peer memory by the
-    partition kernel, codes and hit rows pushed back by the homes, misses
-    fetched by each worker over its own host link, NCCL only as a one-int
-    barrier, no host synchronisation per round
+    cachesim.py:319-320), rank w samples batches i = j*N + w (worker i % N,
+    cachesim.py:309). Default engine: ShardedPipeline -- IDs pushed to the
+    homes over peer memory by the partition kernel, codes and hit rows pushed
+    back by the homes, misses fetched by each worker over its own host link,
+    NCCL only as a one-int barrier, no host synchronisation per round
     (paper_2112_08541_b200/distributed.py). `--exchange nccl`: the all-to-all
     baseline (ShardedFeatureCache, host-synchronised per round).
-    One step = one round = N mini-batches (one per GPU)."""
+    One step = one round = N mini-batches (one per GPU).
+
+    Shared-GPU mode (fewer visible GPUs than ranks, e.g. the 1-GPU test box):
+    ranks share devices round-robin, the process group is gloo (NCCL refuses
+    two ranks on one GPU), the data-path barrier is a host barrier and steps
+    run eagerly -- the same kernels and peer stores (CUDA IPC within a device),
+    for correctness and launcher checks, not for speed."""
     import torch
     import torch.distributed as dist
     from paper_2112_08541_b200.distributed import GpuShardEngine, GpuShardOps, ShardedFeatureCache, ShardedPipeline
@@ -497,9 +654,37 @@ def run_sharded(args, cfg):
         os.environ.update(RANK="0", LOCAL_RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
                           MASTER_PORT=os.environ.get("MASTER_PORT", "29531"))
     rank, local_rank, world = dist_env()
-    torch.cuda.set_device(local_rank)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    ndev = torch.cuda.device_count()
+    shared_gpu = ndev < local_world
+    dev_index = local_rank % ndev
+    torch.cuda.set_device(dev_index)
+    if shared_gpu:
+        dist.init_process_group("gloo")
+        if args.exchange != "push":
+            raise SystemExit("--exchange nccl needs one GPU per rank")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+    cpu_coll = shared_gpu
+
+    def allreduce(t, op=dist.ReduceOp.SUM):
+        if cpu_coll:
+            c = t.cpu()
+            dist.all_reduce(c, op=op)
+            t.copy_(c)
+        else:
+            dist.all_reduce(t, op=op)
+        return t
+
+    def allgather_list(vals):
+        out = [None] * world
+        dist.all_gather_object(out, vals)
+        return out
+
+    def host_barrier():
+        torch.cuda.synchronize()
+        dist.barrier()
+
     dg, feats, order, setup = build_inputs(cfg, args.features, args.graph, order_kind=args.order,
                                            shared=(local_rank, local_world, dist.barrier) if world > 1 else None)
     b, rb, dim = cfg["b"], cfg["dim"] * 4, cfg["dim"]
@@ -510,11 +695,12 @@ def run_sharded(args, cfg):
     seeds_pinned = torch.from_numpy(order_host).pin_memory()
 
     if args.exchange == "push":
-        pipe = ShardedPipeline(rank, world, dg, cfg["fanouts"], b, order, RUN_SEED, cap, feats, rng=args.rng)
+        pipe = ShardedPipeline(rank, world, dg, cfg["fanouts"], b, order, RUN_SEED, cap, feats, rng=args.rng,
+                               barrier=host_barrier if shared_gpu else None)
         counters = pipe.counters
         launches = pipe.kernels_per_round
-        graphs = "off"
-        if not args.no_graphs:
+        graphs = "off (shared-GPU mode: host barriers)" if shared_gpu else "off"
+        if not args.no_graphs and not shared_gpu:
             try:
                 pipe.capture()                    # one CUDA graph per step phase, NCCL barriers inside
                 graphs = "on"
@@ -548,7 +734,7 @@ def run_sharded(args, cfg):
     dist.barrier()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev_index) as clk:
         for k in range(args.steps):
             flush.zero_()
             ev[k][0].record()
@@ -556,14 +742,15 @@ def run_sharded(args, cfg):
             ev[k][1].record()
         torch.cuda.synchronize()
     dist.barrier()
-    total_ms = sum(s.elapsed_time(e) for s, e in ev)
-    d = counters - c0
-    dist.all_reduce(d)
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms_rank = sum(s.elapsed_time(e) for s, e in ev)
+    d_rank = (counters - c0).clone()
+    per_rank = allgather_list([int(x) for x in d_rank.cpu().tolist()] + [total_ms_rank])
+    d = allreduce(d_rank.clone())
+    t = allreduce(torch.tensor([total_ms_rank], dtype=torch.float64, device="cuda"), dist.ReduceOp.MAX)
     total_ms = float(t.item())
     q, own, peer, hst = (int(x) for x in d[:4].tolist())
-    roof = sharded_roofline(args, pipe if args.exchange == "push" else None, feats, rb, flush)
+    roof = sharded_roofline(args, pipe if args.exchange == "push" else None, feats, rb, flush, allreduce,
+                            allgather_list, shared_gpu)
     # e2e: every round the next round's seeds go H2D from pinned host (on the
     # sampling stream, ahead of the sampler) and the round's distinct IDs (the
     # AccessTrace row) + counters are stored into pinned host memory
@@ -604,28 +791,31 @@ def run_sharded(args, cfg):
     u_last = int(host_meta[0])
     assert torch.equal(host_ids[:u_last], s.uniq[:u_last].cpu()), "host-side result differs from the device"
     d2h = n_e2e * (u_last * 4 + 72)
-    t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t = allreduce(torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda"), dist.ReduceOp.MAX)
+    ranks = []
+    for r, v in enumerate(per_rank):
+        rq = max(v[0], 1)
+        ranks.append({"rank": r, "queries": v[0], "hit_pct": round(100.0 * (v[1] + v[2] + v[3]) / rq, 2),
+                      "peer_hit_pct": round(100.0 * v[2] / rq, 2), "miss_pct": round(100.0 * v[4] / rq, 2),
+                      "timed_ms": round(v[8], 3)})
     out = {
         "metric": METRIC, "value": round(world * args.steps / (total_ms * 1e-3), 2), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int32 ids / u53 PCG64 keys / fp32 rows moved",
         "data": graph_data(cfg, args.graph),
-        "config": {"workload": workload_text(cfg, args.features, args.order), "graph": args.graph, "num_nodes": cfg["n"],
-                   "csr_entries": dg.num_edges, "feature_dim": cfg["dim"], "fanouts": list(cfg["fanouts"]),
-                   "batch": b, "cache_rows_per_gpu": cap, "features": args.features,
-                   "parallelism": f"dp{world} + node-ID-sharded FIFO cache (home = v % {world}); " + (
-                       "IDs pushed to the homes over peer memory by the partition kernel, codes and hit rows "
-                       "pushed back by the homes (CUDA IPC), misses fetched by each worker over its own host link, "
-                       "NCCL one-int barriers, no host sync per round"
-                       if args.exchange == "push" else "IDs and rows by NCCL all-to-all (host-synchronised)"),
-                   "l2": "flushed between timed steps (256 MB write, outside the events)",
-                   "step": f"one round = {world} mini-batches (one per GPU)", "cuda_graphs": graphs,
-                   "sampler_rng": args.rng, "ordering": args.order},
+        "config": bench_config(cfg, args, world, dg.num_edges, dg.max_degree, nb_total),
+        "engine": {"step": f"one round = {world} mini-batches (one per GPU)", "cuda_graphs": graphs,
+                   "exchange": ("IDs pushed to the homes over peer memory by the partition kernel, codes and hit "
+                                "rows pushed back by the homes (CUDA IPC), misses fetched by each worker over its "
+                                "own host link, NCCL one-int barriers, no host sync per round"
+                                if args.exchange == "push" else "IDs and rows by NCCL all-to-all (host-synchronised)"),
+                   "shared_gpu": (f"{world} ranks on {ndev} visible GPU(s): gloo + host barriers, eager steps "
+                                  f"(correctness/launcher mode, not a speed number)") if shared_gpu else False},
         "feature_gbs": round(q * rb / (total_ms * 1e-3) / 1e9, 2),
         "hit_pct": round(100.0 * (own + peer + hst) / max(q, 1), 2),
         "peer_hit_pct": round(100.0 * peer / max(q, 1), 2),
+        "per_rank": ranks,
         "e2e": {"value": round(world * n_e2e / (float(t.item()) * 1e-3), 2), "unit": UNIT,
                 "h2d_bytes_per_step": int(h2d / n_e2e), "d2h_bytes_per_step": int(d2h / n_e2e)},
         "roofline": roof,
@@ -635,6 +825,7 @@ def run_sharded(args, cfg):
     if rank == 0:
         print(json.dumps(out), flush=True)
     if args.exchange == "push":
+        dist.barrier()
         pipe.close()
     dist.destroy_process_group()
 
@@ -675,102 +866,143 @@ def sampler_report(dg, cfg, order, rng, sample_ms, dedup_ms, n=8):
                       "stage_ms": round(dedup_ms, 4)}}
 
 
-def sharded_roofline(args, pipe, feats, rb, flush, R=8):
+NVLINK_PEER_GBS = 770.0     # measured peer copy per direction (B200_PROFILING.md; 900 nominal)
+
+
+def sharded_roofline(args, pipe, feats, rb, flush, allreduce, allgather_list, shared_gpu, R=8):
     """Roofline of the sharded engine's dominant kernel, the worker's miss
-    gather (bgl_gather_spans over this rank's own device-missed rows):
-    R eager steps after the timed region, events on the miss stream around the
-    gathers, rows read from the step's miss counts; max over ranks of the time."""
+    gather (bgl_gather_spans over this rank's own device-missed rows): R eager
+    steps after the timed region, events on the miss stream around the
+    gathers, rows read from the step's miss counts; max over ranks of the time.
+    Also the peer (NVLink) side: the rows each home pushed into other GPUs'
+    outputs (its P hits) over its B stage (events on the back stream), and the
+    host-link peak measured with every rank copying at once."""
     import torch
     import torch.distributed as dist
     if pipe is None:
         return {"bound": "host_link" if args.features == "host" else "hbm", "achieved": None, "peak": None,
                 "unit": "GB/s", "frac": None, "traffic": None,
                 "kernel": "n/a for the NCCL all-to-all baseline (--exchange nccl)"}
-    pipe.miss_timing = []
-    rows = []
+    world = dist.get_world_size()
+    pipe.miss_timing, pipe.back_timing = [], []
+    rows, peer_rows = [], []
     for _ in range(R):
         r = (pipe.k + 1) % pipe.NR               # step k gathers the misses of round k + 1
+        c0 = pipe.counters.clone()
         flush.zero_()
         pipe.step_eager()
         torch.cuda.synchronize()
         rows.append(int(pipe.own_misses(r)[1].item()))   # this rank's own misses (the worker fetches them)
-    ev = pipe.miss_timing
-    pipe.miss_timing = None
-    ms = sum(a.elapsed_time(b) for a, b, _ in ev)
-    t = torch.tensor([ms, float(sum(rows))], dtype=torch.float64, device="cuda")
-    tmax = t[:1].clone()
-    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    tot = t[1:].clone()
-    dist.all_reduce(tot)
-    world = dist.get_world_size()
-    # per rank and launch set: bytes this rank's gathers moved / their time (the slowest rank's)
-    per_rank_bytes = float(tot.item()) / world * rb
+        # P hits served by this home (looked up in LI(k+2)); in steady state the
+        # same count its B(k) pushes to other GPUs
+        peer_rows.append(int((pipe.counters - c0)[2].item()))
+    ms = sum(a.elapsed_time(b) for a, b, _ in pipe.miss_timing)
+    bms = sum(a.elapsed_time(b) for a, b in pipe.back_timing)
+    pipe.miss_timing, pipe.back_timing = None, None
+    t = allreduce(torch.tensor([ms, bms], dtype=torch.float64, device="cuda"), dist.ReduceOp.MAX)
+    tot = allreduce(torch.tensor([float(sum(rows)), float(sum(peer_rows))], dtype=torch.float64, device="cuda"))
+    tmax, bmax = float(t[0].item()), float(t[1].item())
+    per_rank_bytes = float(tot[0].item()) / world * rb
+    peer_bytes = float(tot[1].item()) / world * rb
+    nvl = {"peer_push_bytes_per_round": int(peer_bytes / R), "b_stage_ms_per_round": round(bmax / R, 4),
+           "achieved": round(peer_bytes / (bmax * 1e-3) / 1e9, 2) if bmax > 0 else None, "unit": "GB/s",
+           "peak": NVLINK_PEER_GBS,
+           "peak_source": "measured peer copy per direction, /opt/skills/guides/B200_PROFILING.md (900 nominal)",
+           "kernel": "gather_v4_kernel in home-push mode (bgl_gather_rows_push: ring hits stored into the worker "
+                     "GPU's output over peer memory) + the ring survivor copy, per home over its B stage"}
+    if nvl["achieved"] is not None:
+        nvl["frac"] = round(nvl["achieved"] / NVLINK_PEER_GBS, 3)
+    if shared_gpu:
+        nvl["note"] = "shared-GPU mode: the 'peer' stores stay inside one device (no NVLink crossed)"
     if args.features == "host":
-        peak_samples = [host_link_peak_gbs()]
+        dist.barrier()
+        alone = host_link_peak_gbs()
+        dist.barrier()
+        together = host_link_peak_gbs()          # every rank copying at once
+        peaks = allgather_list([alone, together])
         try:
-            peak_samples.append(host_link_zero_copy_peak_gbs(feats, rb))
-        except Exception:  # noqa: BLE001 -- a shared store without .shape: memcpy sample only
-            pass
-        peak = max(peak_samples)
-        achieved = per_rank_bytes / (float(tmax.item()) / 1e3) / 1e9
+            zc = host_link_zero_copy_peak_gbs(feats, rb)
+        except Exception:  # noqa: BLE001 -- a shared store without .shape: memcpy samples only
+            zc = 0.0
+        peak = min(p[1] for p in peaks)          # the link rate a rank gets while all ranks copy
+        achieved = per_rank_bytes / (tmax / 1e3) / 1e9
         return {"bound": "host_link", "achieved": round(achieved, 2), "peak": round(peak, 2), "unit": "GB/s",
                 "frac": round(achieved / peak, 3), "traffic": None,
                 "kernel": "gather_span_kernel (the worker's own misses: TMA spans + 16-B zero-copy host reads)",
                 "algorithmic_bytes_per_launch": int(per_rank_bytes / R),
-                "peak_source": f"per-rank host link: max of a pinned 256 MB cudaMemcpy and a sequential zero-copy "
-                               f"read of the feature store ({[round(x, 2) for x in peak_samples]}); "
-                               f"{R} eager steps after the timed region, max over ranks"}
+                "peak_source": f"per-rank pinned 256 MB cudaMemcpy with all {world} ranks copying at once (min over "
+                               f"ranks); alone / together per rank: {[[round(a, 2), round(b, 2)] for a, b in peaks]}; "
+                               f"rank 0 zero-copy sequential read {round(zc, 2)}; {R} eager steps after the timed "
+                               f"region, max over ranks",
+                "nvlink": nvl}
     hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
-    achieved = 2 * per_rank_bytes / (float(tmax.item()) / 1e3) / 1e9
+    achieved = 2 * per_rank_bytes / (tmax / 1e3) / 1e9
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(achieved / hbm, 3), "traffic": None,
             "kernel": "gather_span_kernel (the worker's own misses from HBM, read + write)",
-            "algorithmic_bytes_per_launch": int(2 * per_rank_bytes / R)}
+            "algorithmic_bytes_per_launch": int(2 * per_rank_bytes / R), "nvlink": nvl}
+
+
+REF_GB_PER_PROC = {"c1": 0.3, "c2": 2.0, "c3": 4.0, "c5": 4.0}
 
 
 def run_reference(args, cfg):
-    rank, local_rank, world = dist_env()
+    """The reference's CPU implementation of the path (gnnio itself, see
+    RefPath) on every host core it can use, on the GPU arms' config. Touches
+    neither CUDA nor the product library. Under torchrun only rank 0 runs."""
+    rank, _, world = dist_env()
     if rank != 0:
         return
-    import torch
-    torch.cuda.set_device(local_rank)
-    from oracle import ordering_oracle as oo
-    # identical inputs: the same generated graph, copied to the host
-    dg = make_graph(cfg, args.graph)
-    hg = dg.to_host()
-    del dg
-    torch.cuda.empty_cache()
-    from oracle import features_oracle as fo
-    feats = fo.synthetic_features(np.arange(cfg["n"]), cfg["dim"], seed=GRAPH_SEED)
-    t0 = time.time()
-    batches = oo.proximity_schedule(hg.row_offsets, hg.col_indices, hg.train_mask, cfg["S"], cfg["b"], RUN_SEED)
-    order_s = time.time() - t0
-    cores = os.cpu_count() or 1
-    nb = len(batches)
-    # bounded sample: a reference step is seconds of CPU work, so at most 64
-    # timed (and 3 warm-up) steps are run; the metric is a rate
-    wi = [i % nb for i in range(min(args.warmup, 3))]
-    ti = [(args.warmup + i) % nb for i in range(min(args.steps, 64))]
-    cpu_reference(hg, batches, cfg, feats, wi, cores)
-    r = cpu_reference(hg, batches, cfg, feats, ti, cores)
+    rp = RefPath(cfg, args, world=world)
+    procs = host_procs(REF_GB_PER_PROC.get(args.config, 2.0))
+    # the GPU arms time batches W .. W+K-1 after W warm-up batches from a cold
+    # cache: the same window here, K rounded up to whole waves of the pool
+    K = -(-args.steps // procs) * procs
+    W = args.warmup
+    rp.run(list(range(W)), procs)
+    r = rp.run(list(range(W, W + K)), procs)
     value = r["batches"] / r["seconds"]
     out = {
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 * r["seconds"] / r["batches"], 2), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64 ids / fp64 priorities / fp32 rows moved",
-        "data": graph_data(cfg, args.graph) + " (same graph and features, on the host)", "impl": "reference",
-        "config": {"workload": workload_text(cfg, args.features, args.order), "graph": args.graph, "num_nodes": cfg["n"],
-                   "csr_entries": int(hg.num_edges),
-                   "fanouts": list(cfg["fanouts"]), "batch": cfg["b"]},
+        "data": (f"synthetic: gnnio.graph.generate_power_law({cfg['n']}, {cfg['avg_degree']}, seed={GRAPH_SEED}, "
+                 f"train_fraction={cfg['train']}, num_labels={cfg['labels']}) built on the host by the C "
+                 f"restatement oracle/powerlaw_ref.c (bit-identical to gnnio's, tests/test_oracle_golden.py); the "
+                 f"same hashed fp32 features; the schedule by gnnio's own ordering"),
+        "impl": "reference",
+        "config": bench_config(cfg, args, world, rp.col.size, rp.max_degree, len(rp.batches)),
         "feature_gbs": round(r["feature_bytes"] / r["seconds"] / 1e9, 3),
-        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{r['batches']} batches: numpy oracle of gnnio sample_batch on {cores} "
-                                   f"processes ({r['sample_s']:.1f}s) + sequential FIFO simulate + numpy gather "
-                                   f"({r['cache_gather_s']:.1f}s); proximity schedule {order_s:.1f}s untimed"},
+        "timed_batches": r["batches"],
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": procs, "kind": rp.kind,
+                         "sample": f"batches {W}..{W + K - 1} of the schedule after {W} warm-up batches from a cold "
+                                   f"cache ({K} = --steps rounded up to whole waves of {procs} worker processes): "
+                                   f"{rp.what()} sample_batch per batch in a fork pool of {procs} processes, its "
+                                   f"FIFO simulate on the persistent state + numpy F[distinct] in batch order in the "
+                                   f"main process ({r['cache_gather_s']:.1f}s of {r['seconds']:.1f}s); untimed setup "
+                                   f"{rp.setup}"},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "isolation": reference_isolation(),
     }
     print(json.dumps(out), flush=True)
+
+
+def reference_isolation() -> dict:
+    """Evidence that the reference arm ran without the product: no product
+    module imported, no in-repo shared library mapped, torch (and so CUDA)
+    never imported."""
+    mapped = set()
+    try:
+        for line in open("/proc/self/maps"):
+            p = line.split()[-1]
+            if p.endswith(".so") and p.startswith(ROOT):
+                mapped.add(os.path.relpath(p, ROOT))
+    except OSError:
+        pass
+    return {"product_modules": sorted(m for m in sys.modules if m.startswith("paper_2112_08541_b200")),
+            "repo_so_mapped": sorted(mapped), "torch_imported": "torch" in sys.modules,
+            "reference_package": (import_gnnio() or {}).get("path")}
 
 
 def main():
@@ -798,12 +1030,35 @@ def main():
     cfg = CONFIGS[args.config]
     if args.graph is None:
         args.graph = "continuum" if args.config in ("c3", "c5") else "exact"
+    world = dist_env()[2]
     if args.impl == "reference":
+        if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+            os.environ["WORLD_SIZE"] = str(args.gpus)      # rank 0 alone runs; the config is the N-GPU one
         run_reference(args, cfg)
-    elif dist_env()[2] > 1 or args.sharded:
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch(args.gpus)                                # one process per GPU, as the driver's torchrun
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1 or args.sharded:
         run_sharded(args, cfg)
     else:
         run_bgl(args, cfg)
+
+
+def relaunch(n: int) -> None:
+    """`bench.py --gpus N` without torchrun: re-exec under
+    torch.distributed.run with N local ranks (rendezvous on 127.0.0.1),
+    exactly as the driver launches N > 1."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
 
 
 if __name__ == "__main__":

@@ -213,3 +213,62 @@ def csr_from_edges(edges: np.ndarray, n: int):
     off = np.zeros(n + 1, dtype=np.int64)
     np.add.at(off, src + 1, 1)
     return np.cumsum(off), dst
+
+
+# -- the same restatement in C (oracle/powerlaw_ref.c), for full-size shapes ----------
+
+_CLIB = None
+
+
+def _clib():
+    """ctypes handle of oracle/_build/liboracle_graph.so (built by
+    `make -C oracle`, which __graft_entry__.build() runs; built on first use
+    when missing -- gcc is part of the image on the GPU box too)."""
+    global _CLIB
+    if _CLIB is None:
+        import ctypes
+        import os
+        import subprocess
+        here = os.path.dirname(os.path.abspath(__file__))
+        so = os.path.join(here, "_build", "liboracle_graph.so")
+        if not os.path.exists(so):
+            subprocess.run(["make", "-s", "-C", here], check=True)
+        lib = ctypes.CDLL(so)
+        i64, vp = ctypes.c_int64, ctypes.c_void_p
+        lib.ref_power_law_edge_bound.restype = i64
+        lib.ref_power_law_edge_bound.argtypes = [i64, i64, ctypes.c_int32]
+        lib.ref_power_law_generate.restype = ctypes.c_int
+        lib.ref_power_law_generate.argtypes = [i64, i64, ctypes.c_int32, ctypes.c_double, i64, vp, vp, vp, vp]
+        lib.ref_csr_from_edges.restype = i64
+        lib.ref_csr_from_edges.argtypes = [vp, i64, i64, vp, vp]
+        _CLIB = lib
+    return _CLIB
+
+
+def generate_power_law_c(n: int, avg_degree: int, seed: int, train_fraction: float = 0.1, num_labels: int = 1,
+                         cross_fraction: float = 0.05):
+    """gnnio.graph.generate_power_law (graph.py:218-297) through the C
+    restatement: (row_offsets int64 [n+1], col_indices int64 [E], train_mask
+    bool [n], labels int64 [n]) -- the arrays the reference's Graph holds."""
+    lib = _clib()
+    m = max(1, int(round(avg_degree / 2)))                       # graph.py:251
+    st = np.random.default_rng(seed).bit_generator.state
+    s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+    state = np.array([s >> 64, s & M64, inc >> 64, inc & M64, st["has_uint32"], st["uinteger"]], dtype=np.uint64)
+    bound = int(lib.ref_power_law_edge_bound(n, m, num_labels))
+    edges = np.empty((bound, 2), dtype=np.int32)
+    ne = np.zeros(1, dtype=np.int64)
+    train = np.zeros(n, dtype=np.uint8)
+    rc = lib.ref_power_law_generate(n, m, num_labels, float(cross_fraction), int(math.floor(train_fraction * n)),
+                                    state.ctypes.data, edges.ctypes.data, ne.ctypes.data, train.ctypes.data)
+    if rc != 0:
+        raise ValueError("generate_power_law_c: endpoint list beyond 2^32 entries (not restated)")
+    E = int(ne[0])
+    off = np.empty(n + 1, dtype=np.int64)
+    col = np.empty(2 * E, dtype=np.int64)
+    nnz = int(lib.ref_csr_from_edges(edges.ctypes.data, E, n, off.ctypes.data, col.ctypes.data))
+    del edges
+    col = col[:nnz].copy()
+    bounds = np.array([i * n // num_labels for i in range(num_labels + 1)], dtype=np.int64)
+    labels = (np.searchsorted(bounds, np.arange(n, dtype=np.int64), side="right") - 1).astype(np.int64)
+    return off, col, train.astype(bool), labels

@@ -380,6 +380,7 @@ class ShardedPipeline:
         self.primed = False
         self._in_graph = False
         self.miss_timing = None      # list -> _M records (start, end, round set) events (eager steps)
+        self.back_timing = None      # list -> _B records (start, end) events (eager steps)
         self.graphs: dict = {}
         # per round (our kernels; the two NCCL barrier kernels not counted): stage + hops (sample + heavy)
         # + dedup (mark, emit, reset); partition (count, scan, push); the worker's miss compaction +
@@ -493,14 +494,19 @@ class ShardedPipeline:
         r, maxu, rb, eng = j % self.NR, self.maxu, self.rb, self.engine
         h, ring = eng.dev.handle, eng.dev.rows_ptr() or None
         lib = _lib.load()
+        timing = self.back_timing is not None and not self._in_graph
         with torch.cuda.stream(self.s_back):
             st = _lib.stream_ptr(self.s_back)
+            if timing:   # measurement pass (bench roofline, peer-push rate): the whole B stage
+                bev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             for w in range(self.world):
                 plan, pcount = self.plans[r][w]
                 cnt = self.recv_cnt[r, w:w + 1]
                 out_w = self.worker_rows[w] + r * maxu * rb
                 if not self._in_graph:
                     self.s_back.wait_event(self.miss_done[r][w])
+                if timing and w == 0:
+                    bev[0].record(self.s_back)     # after the first wait: the stage's own time
                 _lib.check(lib.bgl_gather_rows_push(self.recv_ids[r, w].data_ptr(),
                                                     self.src_row[r, w].data_ptr() if ring else None,
                                                     cnt.data_ptr(), maxu, ring, eng.table, rb, None, out_w,
@@ -508,6 +514,9 @@ class ShardedPipeline:
                 if ring:   # survivors' rows into their ring slots, read back from worker w's output
                     _lib.check(lib.bgl_cache_copy_rows_indexed(h, plan.data_ptr(), pcount.data_ptr(), maxu, out_w,
                                                                self.recv_pos[r, w].data_ptr(), st))
+            if timing:
+                bev[1].record(self.s_back)
+                self.back_timing.append(bev)
 
     def prime(self) -> None:
         """Prologue: S(0..2), X(0), LI(0), M(0), X(1), LI(1)."""

@@ -41,8 +41,25 @@ def test_bgl_arm_line():
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
 
 
-def test_reference_arm_line():
-    d = _run("--impl", "reference", "--config", "c1", "--steps", "1", "--warmup", "3")
-    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "mini-batches/s"
-    assert d["cpu_baseline"]["value"] == d["value"] and d["cpu_baseline"]["cores"] >= 1
-    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+def test_reference_arm_same_config():
+    """Both arms describe the same workload with the same config object (the
+    driver compares them); the reference arm itself is tested on the CPU
+    (tests/test_bench_launcher.py)."""
+    g = _run("--config", "c1", "--steps", "4", "--warmup", "3", "--no-cpu-baseline")
+    r = _run("--impl", "reference", "--config", "c1", "--steps", "4", "--warmup", "3")
+    assert g["config"] == r["config"]
+    assert r["isolation"]["product_modules"] == [] and not r["isolation"]["torch_imported"]
+
+
+def test_gpus_flag_launches_ranks():
+    """`bench.py --gpus 2` without torchrun re-launches itself with two ranks
+    (shared-GPU mode when the box has one GPU) and prints ONE line whose
+    n_gpus is 2, with the per-rank hit rates."""
+    import torch
+    d = _run("--gpus", "2", "--config", "c1", "--steps", "4", "--warmup", "3")
+    assert d["n_gpus"] == 2 and len(d["per_rank"]) == 2 and d["value"] > 0
+    assert d["config"]["parallelism"].startswith("dp2")
+    assert 0 <= d["peer_hit_pct"] <= d["hit_pct"] <= 100
+    if torch.cuda.device_count() < 2:
+        assert d["engine"]["shared_gpu"]
+    assert "nvlink" in d["roofline"]

@@ -256,3 +256,29 @@ def test_oracle_reproduces_reference_c1_epoch(golden):
     cnt, codes = co.FifoEngine(10_000, 0, 1).run(trace)
     assert np.array_equal(cnt, npz["counters"])
     assert all(np.array_equal(a, b) for a, b in zip(codes, get(npz, "codes")))
+
+
+def test_graph_generator_c_restatement_matches_reference(golden):
+    """oracle/powerlaw_ref.c (the C restatement bench.py's reference arm builds
+    its graph with) reproduces gnnio.graph.generate_power_law on every golden
+    graph, including the ones too large for the pure-Python restatement."""
+    from oracle import graph_oracle as go
+    npz = golden("graphgen")
+    for (n, d, seed, tf, nl, cf), off, col, train, labels in _graphgen_cases(npz):
+        o, c, tr, lab = go.generate_power_law_c(n, d, seed, tf, nl, cf)
+        assert np.array_equal(o, off) and np.array_equal(c, col), (n, d, seed)
+        assert np.array_equal(tr, train), (n, d, seed)
+        assert np.array_equal(lab, labels), (n, d, seed)
+
+
+def test_graph_generator_c_restatement_c2_checksum(golden):
+    """BASELINE.json configs[1]: the C restatement's products-shaped graph has
+    the CSR size, checksum and offsets tail of the graph gnnio generated
+    (tests/golden/c2.npz; ~10 minutes of reference CPU time, seconds here)."""
+    from oracle import graph_oracle as go
+    npz = golden("c2")
+    off, col, train, _ = go.generate_power_law_c(2_400_000, 51, 1, 0.08, 47)
+    assert col.size == int(npz["csr_entries"][0])
+    assert int((col * (np.arange(col.size) % 1000003 + 1)).sum() % (1 << 61)) == int(npz["csr_checksum"][0])
+    assert np.array_equal(off[-1000:], npz["offsets_tail"])
+    assert int(train.sum()) == int(0.08 * 2_400_000)
