@@ -395,6 +395,51 @@ def host_procs(per_proc_gb: float) -> int:
 
 # ----------------------------------------------------------------------------- arms
 
+def dropin_e2e(args, cfg, dg, feats, order_host, max_uniq):
+    """The same window through the gnnio-signature drop-in functions, as a
+    gnnio caller switching packages would run it (host-synchronous API, wall
+    clock): sampler.simulate_epoch over the schedule's first W+K batches
+    (sampler.py:119-167; batch rng keyed by the batch index), then per batch
+    FeatureCacheEngine.retrieve (lookup + gather + insert, the rows F[batch]
+    on the device; its state is the CacheEngineState that
+    cachesim.simulate(trace, cfg, state=engine.state) drives), and separately
+    cachesim.simulate over the same trace (cachesim.py:275-363, the counters
+    only, no rows). Rows per batch are checked against the pipeline's."""
+    import torch
+    from paper_2112_08541_b200.cachesim import CacheConfig, simulate
+    from paper_2112_08541_b200.features import FeatureCacheEngine
+    from paper_2112_08541_b200.ordering import BatchSchedule
+    from paper_2112_08541_b200.sampler import SamplingConfig, simulate_epoch
+    b, nb = cfg["b"], args.warmup + args.steps
+    sched = BatchSchedule(batches=[order_host[i * b:(i + 1) * b].astype(np.int64) for i in range(nb)],
+                          batch_size=b, policy="proximity")
+    scfg = SamplingConfig(fanouts=tuple(cfg["fanouts"]), batch_size=b, seed=RUN_SEED, rng=args.rng)
+    ccfg = CacheConfig(device_capacity=int(cfg["cache_frac"] * cfg["n"]), feature_bytes_per_node=cfg["dim"] * 4)
+    eng = FeatureCacheEngine(ccfg, feats, max_uniq)
+    simulate_epoch(dg, None, BatchSchedule(batches=sched.batches[:2], batch_size=b), scfg)   # warm the kernels
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    trace, _ = simulate_epoch(dg, None, sched, scfg)
+    t1 = time.perf_counter()
+    qbytes = 0
+    for i, ids in enumerate(trace.batches):
+        rows, codes = eng.retrieve(ids, i)
+        qbytes += ids.size * 4
+    codes_last = codes.cpu()                  # the step's result back on the host
+    t2 = time.perf_counter()
+    rep = simulate(trace, ccfg)
+    t3 = time.perf_counter()
+    assert rep.total_queries == sum(x.size for x in trace.batches)
+    return {"value": round(nb / (t2 - t0), 2), "unit": UNIT, "batches": nb,
+            "api": "sampler.simulate_epoch (trace to the host) + FeatureCacheEngine.retrieve per batch (ids H2D, "
+                   "rows F[batch] in HBM, codes D2H at the end); wall clock, host-synchronous gnnio-style calls",
+            "simulate_epoch_ms_per_batch": round(1e3 * (t1 - t0) / nb, 3),
+            "retrieve_ms_per_batch": round(1e3 * (t2 - t1) / nb, 3),
+            "simulate_ms_per_batch": round(1e3 * (t3 - t2) / nb, 3),
+            "h2d_bytes_per_step": int(qbytes / nb + b * 8),
+            "d2h_bytes_per_step": int(qbytes * 2 / nb + codes_last.numel() / nb)}
+
+
 def cpu_baseline(cfg, args, dg, feats, order_host, nsample: int = 2):
     """The reference's CPU path (gnnio sample_batch + simulate + numpy
     gather, RefPath) timed on one core of this box on a bounded sample: the
@@ -595,6 +640,8 @@ def run_bgl(args, cfg):
     u_mean = float((pipe.counters - ce0)[0].item()) / n_e2e
     d2h = int(u_mean * 4 + 9 * 8) * n_e2e
 
+    dropin = dropin_e2e(args, cfg, dg, feats, order_host, pipe.max_uniq)
+
     value = world * args.steps / (total_ms * 1e-3)
     ms_per_step = total_ms / args.steps
     feat_gbs = queries * rb / (total_ms * 1e-3) / 1e9
@@ -617,6 +664,7 @@ def run_bgl(args, cfg):
                        "the step, inside its timed region); the step's distinct IDs (the AccessTrace row) + "
                        "cache counters are stored into pinned host memory by bgl_d2h_result (zero-copy, no "
                        "per-step host sync); checked on the host"},
+        "e2e_dropin": dropin,
         "gpu_launches": pipe.kernels_per_step * args.steps,
         "clocks": clk.summary(),
         "setup": dict(setup, torch_alloc_peak_gb=round(torch.cuda.max_memory_allocated() / 1e9, 2)),
@@ -924,7 +972,9 @@ def sharded_roofline(args, pipe, feats, rb, flush, allreduce, allgather_list, sh
             zc = host_link_zero_copy_peak_gbs(feats, rb)
         except Exception:  # noqa: BLE001 -- a shared store without .shape: memcpy samples only
             zc = 0.0
-        peak = min(p[1] for p in peaks)          # the link rate a rank gets while all ranks copy
+        # the link rate a rank gets while all ranks copy (shared-GPU mode: the
+        # ranks time-slice one GPU and its link, so each gather runs alone)
+        peak = min(p[0] if shared_gpu else p[1] for p in peaks)
         achieved = per_rank_bytes / (tmax / 1e3) / 1e9
         return {"bound": "host_link", "achieved": round(achieved, 2), "peak": round(peak, 2), "unit": "GB/s",
                 "frac": round(achieved / peak, 3), "traffic": None,

@@ -208,6 +208,12 @@ int bgl_cache_copy_rows_indexed(bgl_cache_t cache, const int32_t* plan, const in
  * be NULL. dev_slots: [num_shards][shard_capacity]; dev_tails: [num_shards]. */
 int bgl_cache_export(bgl_cache_t cache, int64_t* dev_slots_host, int64_t* dev_tails_host,
                      int64_t* host_slots_host, int64_t* host_tail_host);
+/* Synchronous copy of the per-level operation counters the reference keeps on
+ * every level (_Level.insertions / .evictions, cachesim.py:45-49; FifoLevel
+ * increments them at cachesim.py:100,104): out_host[2 * y] = insertions,
+ * out_host[2 * y + 1] = evictions of level y (y < num_shards: device rings,
+ * y == num_shards: the host level). Cumulative since create / reset. */
+int bgl_cache_level_stats(bgl_cache_t cache, int64_t* out_host);
 
 /* ---------------------------------------------------------------- static-degree policy
  * gnnio.cachesim.warm_static (cachesim.py:206-224): per shard the capacity
@@ -372,6 +378,13 @@ int bgl_stage_batch(const int32_t* order, int64_t total, int64_t batch_size, int
                     const uint64_t* tables, int64_t* batch_counter, int32_t* seeds_out,
                     int64_t* seed_count_out, uint64_t* table_out, int64_t* batch_index_out,
                     const int64_t* fed_count_dev, int64_t batch_stride, int64_t batch_offset, void* stream);
+/* Append one batch's sorted distinct IDs to a device-resident trace without
+ * a host round trip (simulate_epoch, sampler.py:157): dst[off[b] ..
+ * off[b] + n) = src[0 .. n), off[b + 1] = off[b] + n, with n = *n_dev and
+ * `off` a device int64 array (off[0] = 0) -- the AccessTrace rows of an epoch
+ * are copied to the host once at its end. */
+int bgl_trace_append(const int32_t* src, const int64_t* n_dev, int64_t max_n, int32_t* dst, int64_t* off,
+                     int64_t batch, void* stream);
 /* Sync-free result hand-off: host_ids[0..n) = ids[0..*n_dev) and host_meta =
  * {n, counters[0..8)} written straight into mapped pinned host memory
  * (device aliases from bgl_host_device_pointer). counters may be NULL. */

@@ -58,6 +58,8 @@ PROTOTYPES = {
     "bgl_cache_copy_rows": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "bgl_cache_copy_rows_indexed": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "bgl_cache_export":(ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "bgl_cache_level_stats": (ctypes.c_int, [c_vp, c_vp]),
+    "bgl_trace_append": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp]),
     "bgl_degree_histogram": (ctypes.c_int, [c_vp, c_i64, c_i32, c_i64, c_vp, c_vp, c_vp]),
     "bgl_select_flags": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp]),
     "bgl_compact_workspace": (c_sz, [c_i64]),

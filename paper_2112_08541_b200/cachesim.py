@@ -90,6 +90,13 @@ class FifoCacheDevice:
     def rows_ptr(self) -> int:
         return _lib.load().bgl_cache_rows(self.handle) or 0
 
+    def level_stats(self) -> np.ndarray:
+        """int64 [d+1, 2]: cumulative (insertions, evictions) per level, the
+        host level last (_Level counters, cachesim.py:45-49)."""
+        out = np.zeros((self.cfg.num_devices + 1, 2), dtype=np.int64)
+        _lib.check(_lib.load().bgl_cache_level_stats(self.handle, out.ctypes.data))
+        return out
+
     def export(self):
         c = self.cfg
         d, C, Ch = c.num_devices, c.device_capacity, c.host_capacity
@@ -104,8 +111,9 @@ class FifoCacheDevice:
 
 class FifoLevelView:
     """Read-only view of one ring with the FifoLevel attributes the reference
-    exposes (`capacity`, `slots`, `tail`, `__contains__`, `__len__`,
-    cachesim.py:81-107). Reading synchronises with the device."""
+    exposes (`capacity`, `slots`, `tail`, `residency`, `insertions`,
+    `evictions`, `metadata_updates`, `__contains__`, `__len__`,
+    cachesim.py:42-107). Reading synchronises with the device."""
 
     def __init__(self, state: "CacheEngineState", level: int):
         self._state = state
@@ -129,6 +137,26 @@ class FifoLevelView:
     @property
     def tail(self) -> int:
         return self._snap()[1]
+
+    def _stat(self, k: int) -> int:
+        y = self._state.cfg.num_devices if self._level < 0 else self._level
+        return int(self._state.engine.level_stats()[y, k])
+
+    @property
+    def insertions(self) -> int:
+        """_Level.insertions (cachesim.py:47, incremented at :104)."""
+        return 0 if self._state.policy == "static-degree" else self._stat(0)
+
+    @property
+    def evictions(self) -> int:
+        """_Level.evictions (cachesim.py:48, incremented at :100)."""
+        return 0 if self._state.policy == "static-degree" else self._stat(1)
+
+    @property
+    def metadata_updates(self) -> int:
+        """_Level.metadata_updates (cachesim.py:49): FIFO and static levels
+        never update metadata (only LRU/LFU do, :118-131, :150-174)."""
+        return 0
 
     @property
     def resident(self) -> frozenset:
@@ -366,26 +394,43 @@ def simulate(trace, cfg: CacheConfig, g=None, batch_devices=None, state: CacheEn
     scratch = _UniqueScratch(eng.num_nodes, maxb)
     seg_off = _lib.c_i64 * 1
     c_off = seg_off(0)
+    # AccessTrace rows are sorted and distinct (np.unique, sampler.py:157): such a
+    # batch is its own insert order, so only other batches need the device unique
+    if flat.size:
+        inc = np.diff(flat) > 0
+        bstart = np.zeros(flat.size, dtype=bool)
+        bstart[offs[1:-1][offs[1:-1] < flat.size]] = True
+        bad = np.flatnonzero(~inc & ~bstart[1:]) + 1          # positions breaking strict increase in a batch
+        unsorted = np.zeros(nb, dtype=bool)
+        unsorted[np.searchsorted(offs, bad, side="right") - 1] = True
+    else:
+        unsorted = np.zeros(nb, dtype=bool)
+    if batch_devices is not None:
+        bd = np.asarray(batch_devices, dtype=np.int64)
+        if bd.size < nb or (nb and (bd[:nb].min() < 0 or bd[:nb].max() >= d)):
+            raise ValueError("worker device out of range")
     for i in range(nb):
         worker = int(batch_devices[i]) if batch_devices is not None else i % d
-        if not 0 <= worker < d:
-            raise ValueError("worker device out of range")
         n = int(sizes[i])
         bptr = ids.data_ptr() + 4 * int(offs[i])
         nptr = lens.data_ptr() + 8 * i
         cptr = counters.data_ptr() + 64 * i
         # sorted distinct set of the batch = the insert order (cachesim.py:341-344)
-        _lib.check(lib.bgl_unique_sorted(bptr, 1, c_off, nptr, (_lib.c_i64 * 1)(n), eng.num_nodes,
-                                         scratch.ws.data_ptr(), scratch.uniq.data_ptr(),
-                                         scratch.count.data_ptr(), st))
-        _lib.check(lib.bgl_cache_lookup(eng.handle, bptr, nptr, n, worker, scratch.uniq.data_ptr(),
-                                        scratch.count.data_ptr(), n,
+        if unsorted[i]:
+            _lib.check(lib.bgl_unique_sorted(bptr, 1, c_off, nptr, (_lib.c_i64 * 1)(n), eng.num_nodes,
+                                             scratch.ws.data_ptr(), scratch.uniq.data_ptr(),
+                                             scratch.count.data_ptr(), st))
+            sptr, scnt = scratch.uniq.data_ptr(), scratch.count.data_ptr()
+        else:
+            sptr, scnt = bptr, nptr
+        _lib.check(lib.bgl_cache_lookup(eng.handle, bptr, nptr, n, worker, sptr, scnt, n,
                                         None if codes is None else codes.data_ptr() + int(offs[i]),
                                         None, cptr, st))
         if not static:                         # static levels never change (StaticLevel.insert, cachesim.py:74-75)
-            _lib.check(lib.bgl_cache_insert(eng.handle, scratch.uniq.data_ptr(), n, None, cptr, st))
-        _lib.check(lib.bgl_unique_reset(scratch.ws.data_ptr(), eng.num_nodes, scratch.uniq.data_ptr(),
-                                        scratch.count.data_ptr(), n, st))
+            _lib.check(lib.bgl_cache_insert(eng.handle, sptr, n, None, cptr, st))
+        if unsorted[i]:
+            _lib.check(lib.bgl_unique_reset(scratch.ws.data_ptr(), eng.num_nodes, scratch.uniq.data_ptr(),
+                                            scratch.count.data_ptr(), n, st))
     host_counters = counters[:nb].cpu().numpy()
     host_codes = None
     if record_outcomes:

@@ -40,6 +40,7 @@ struct bgl_cache {
     int64_t max_tiles = 0;
     int32_t shard_index = 0;     // global shard of this handle (multi-GPU: rank)
     int32_t global_shards = 0;   // 0 = d (single process)
+    int64_t* level_stats = nullptr;   // [d+1][2] insertions, evictions per level (_Level counters, cachesim.py:45-49)
 };
 
 namespace bgl {
@@ -299,7 +300,7 @@ __global__ void insert_kernel(const int32_t* __restrict__ sorted_ids, int32_t d,
                               const int64_t* __restrict__ mcount, const int32_t* __restrict__ lists, int64_t list_cap,
                               const unsigned char* __restrict__ batch_rows, unsigned char* __restrict__ rows,
                               int64_t rb, int64_t* __restrict__ counters, int32_t* __restrict__ plan,
-                              int64_t plan_stride) {
+                              int64_t plan_stride, int64_t* __restrict__ level_stats) {
     const int y = blockIdx.y;
     const bool host = (y == d);
     const int64_t cap = host ? Ch : C;
@@ -344,7 +345,10 @@ __global__ void insert_kernel(const int32_t* __restrict__ sorted_ids, int32_t d,
             }
         }
     }
-    if (lane == 0 && ev) atomicAdd((unsigned long long*)&counters[6], (unsigned long long)ev);
+    if (lane == 0 && ev) {
+        atomicAdd((unsigned long long*)&counters[6], (unsigned long long)ev);
+        atomicAdd((unsigned long long*)&level_stats[2 * y + 1], (unsigned long long)ev);
+    }
 }
 
 // The same insert with one THREAD per touched slot: index/ring/plan updates
@@ -354,7 +358,8 @@ __global__ void insert_index_kernel(const int32_t* __restrict__ sorted_ids, int3
                                     int32_t* __restrict__ slot_of, int32_t* __restrict__ hslot_of,
                                     const int64_t* __restrict__ tails, const int64_t* __restrict__ mcount,
                                     const int32_t* __restrict__ lists, int64_t list_cap,
-                                    int64_t* __restrict__ counters, int32_t* __restrict__ plan, int64_t plan_stride) {
+                                    int64_t* __restrict__ counters, int32_t* __restrict__ plan, int64_t plan_stride,
+                                    int64_t* __restrict__ level_stats) {
     const int y = blockIdx.y;
     const bool host = (y == d);
     const int64_t cap = host ? Ch : C;
@@ -384,12 +389,15 @@ __global__ void insert_index_kernel(const int32_t* __restrict__ sorted_ids, int3
         }
     }
     const int64_t wev = warp_sum_i64(ev);
-    if (lane_id() == 0 && wev) atomicAdd((unsigned long long*)&counters[6], (unsigned long long)wev);
+    if (lane_id() == 0 && wev) {
+        atomicAdd((unsigned long long*)&counters[6], (unsigned long long)wev);
+        atomicAdd((unsigned long long*)&level_stats[2 * y + 1], (unsigned long long)wev);
+    }
 }
 
 __global__ void insert_finalize_kernel(int32_t d, int64_t C, int64_t Ch, int64_t* __restrict__ tails,
                                        const int64_t* __restrict__ mcount, int64_t* __restrict__ counters,
-                                       int64_t* __restrict__ plan_count) {
+                                       int64_t* __restrict__ plan_count, int64_t* __restrict__ level_stats) {
     if (threadIdx.x != 0) return;
     int64_t ins = 0, ev = 0;
     for (int y = 0; y <= d; ++y) {
@@ -400,6 +408,8 @@ __global__ void insert_finalize_kernel(int32_t d, int64_t C, int64_t Ch, int64_t
         tails[y] = (tails[y] + M) % cap;
         ins += M;
         ev += M > cap ? M - cap : 0;
+        level_stats[2 * y] += M;                       // every insert of a distinct miss counts (cachesim.py:104)
+        level_stats[2 * y + 1] += M > cap ? M - cap : 0;   // inserts evicted by later inserts of the batch
     }
     counters[5] += ins;
     counters[6] += ev;
@@ -477,6 +487,7 @@ void free_cache(bgl_cache* c) {
     cudaFree(c->rows);
     cudaFree(c->lists);
     cudaFree(c->tile_counts);
+    cudaFree(c->level_stats);
 }
 
 }  // namespace
@@ -506,6 +517,8 @@ int bgl_cache_create(int64_t num_nodes, int32_t num_shards, int64_t shard_capaci
         if ((st = alloc_fill((void**)&c->hring, (size_t)host_capacity * 4, 0xFF, "cache host ring")) != BGL_OK) break;
         if ((st = alloc_fill((void**)&c->tails, (size_t)(num_shards + 1) * 8, 0, "cache tails")) != BGL_OK) break;
         if ((st = alloc_fill((void**)&c->mcount, (size_t)(num_shards + 1) * 8, 0, "cache mcount")) != BGL_OK) break;
+        if ((st = alloc_fill((void**)&c->level_stats, (size_t)(num_shards + 1) * 16, 0, "cache level stats")) != BGL_OK)
+            break;
         if (row_bytes > 0 &&
             (st = alloc_fill((void**)&c->rows, (size_t)num_shards * shard_capacity * row_bytes, 0, "cache rows")) != BGL_OK)
             break;
@@ -574,6 +587,7 @@ int bgl_cache_reset(bgl_cache_t c, void* stream) {
     if (c->hslot_of) BGL_TRY(cuda_status(cudaMemsetAsync(c->hslot_of, 0xFF, c->n * 4, st), "reset"));
     if (c->rings) BGL_TRY(cuda_status(cudaMemsetAsync(c->rings, 0xFF, (size_t)c->d * c->C * 4, st), "reset"));
     if (c->hring) BGL_TRY(cuda_status(cudaMemsetAsync(c->hring, 0xFF, (size_t)c->Ch * 4, st), "reset"));
+    BGL_TRY(cuda_status(cudaMemsetAsync(c->level_stats, 0, (size_t)(c->d + 1) * 16, st), "reset"));
     return cuda_status(cudaMemsetAsync(c->tails, 0, (size_t)(c->d + 1) * 8, st), "reset");
 }
 
@@ -639,10 +653,12 @@ int bgl_cache_insert(bgl_cache_t c, const int32_t* sorted_ids, int64_t max_sorte
         dim3 grid(gx, c->d + 1);
         insert_kernel<<<grid, threads, 0, st>>>(sorted_ids, c->d, c->C, c->Ch, c->rings, c->hring, c->slot_of,
                                                 c->hslot_of, c->tails, c->mcount, c->lists, c->list_cap,
-                                                (const unsigned char*)batch_rows, c->rows, c->rb, counters, nullptr, 0);
+                                                (const unsigned char*)batch_rows, c->rows, c->rb, counters, nullptr, 0,
+                                                c->level_stats);
         BGL_TRY(launch_status("insert_kernel"));
     }
-    insert_finalize_kernel<<<1, 32, 0, st>>>(c->d, c->C, c->Ch, c->tails, c->mcount, counters, nullptr);
+    insert_finalize_kernel<<<1, 32, 0, st>>>(c->d, c->C, c->Ch, c->tails, c->mcount, counters, nullptr,
+                                             c->level_stats);
     return launch_status("insert_finalize_kernel");
 }
 
@@ -660,10 +676,11 @@ int bgl_cache_insert_plan(bgl_cache_t c, const int32_t* sorted_ids, int64_t max_
         dim3 grid(grid_for(work, 256, 8), c->d + 1);
         insert_index_kernel<<<grid, 256, 0, st>>>(sorted_ids, c->d, c->C, c->Ch, c->rings, c->hring, c->slot_of,
                                                   c->hslot_of, c->tails, c->mcount, c->lists, c->list_cap,
-                                                  counters, plan, stride);
+                                                  counters, plan, stride, c->level_stats);
         BGL_TRY(launch_status("insert_index_kernel"));
     }
-    insert_finalize_kernel<<<1, 32, 0, st>>>(c->d, c->C, c->Ch, c->tails, c->mcount, counters, plan_count);
+    insert_finalize_kernel<<<1, 32, 0, st>>>(c->d, c->C, c->Ch, c->tails, c->mcount, counters, plan_count,
+                                             c->level_stats);
     return launch_status("insert_finalize_kernel");
 }
 
@@ -689,6 +706,13 @@ int bgl_cache_copy_rows_indexed(bgl_cache_t c, const int32_t* plan, const int64_
     copy_rows_kernel<<<grid, 256, 0, as_stream(stream)>>>(plan, plan_count, stride, c->C,
                                                           (const unsigned char*)batch_rows, c->rows, c->rb, row_index);
     return launch_status("copy_rows_kernel");
+}
+
+int bgl_cache_level_stats(bgl_cache_t c, int64_t* out_host) {
+    BGL_CHECK_ARG(c && out_host, "bgl_cache_level_stats: null pointer");
+    BGL_TRY(cuda_status(cudaDeviceSynchronize(), "level stats sync"));
+    return cuda_status(cudaMemcpy(out_host, c->level_stats, (size_t)(c->d + 1) * 16, cudaMemcpyDeviceToHost),
+                       "level stats copy");
 }
 
 int bgl_cache_export(bgl_cache_t c, int64_t* dev_slots_host, int64_t* dev_tails_host, int64_t* host_slots_host,

@@ -51,6 +51,18 @@ __global__ void d2h_result_kernel(const int32_t* __restrict__ ids, const int64_t
 
 using namespace bgl;
 
+namespace bgl {
+// off[batch] is only read here; one thread writes off[batch + 1]
+__global__ void trace_append_kernel(const int32_t* __restrict__ src, const int64_t* __restrict__ n_dev,
+                                    int32_t* __restrict__ dst, int64_t* __restrict__ off, int64_t batch) {
+    const int64_t n = *n_dev;
+    const int64_t o = off[batch];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[o + i] = src[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0) off[batch + 1] = o + n;
+}
+}  // namespace bgl
+
 extern "C" {
 
 int bgl_stage_batch(const int32_t* order, int64_t total, int64_t batch_size, int64_t num_batches,
@@ -66,6 +78,14 @@ int bgl_stage_batch(const int32_t* order, int64_t total, int64_t batch_size, int
                                                           batch_index_out, fed_count_dev, batch_stride,
                                                           batch_offset);
     return launch_status("stage_batch_kernel");
+}
+
+int bgl_trace_append(const int32_t* src, const int64_t* n_dev, int64_t max_n, int32_t* dst, int64_t* off,
+                     int64_t batch, void* stream) {
+    BGL_CHECK_ARG(src && n_dev && dst && off && batch >= 0, "bgl_trace_append: bad argument");
+    if (max_n <= 0) max_n = 1;
+    trace_append_kernel<<<grid_for(max_n, 256, 4), 256, 0, as_stream(stream)>>>(src, n_dev, dst, off, batch);
+    return launch_status("trace_append_kernel");
 }
 
 int bgl_d2h_result(const int32_t* ids, const int64_t* n_dev, int64_t max_n, const int64_t* counters,

@@ -249,12 +249,17 @@ class FeatureCacheEngine:
     def retrieve(self, batch_ids, batch_index: int):
         """rows = F[batch_ids] for one sorted distinct batch; returns
         (rows [U, dim] on the device, outcome codes uint8 [U])."""
-        ids = torch.as_tensor(np.asarray(batch_ids, dtype=np.int64) if not isinstance(batch_ids, torch.Tensor)
-                              else batch_ids).to(device="cuda", dtype=torch.int32)
+        if isinstance(batch_ids, torch.Tensor):
+            ids = batch_ids.to(device="cuda", dtype=torch.int32)
+            unsorted = ids.numel() > 1 and not bool((ids[1:] > ids[:-1]).all())
+        else:   # host batch (an AccessTrace row): checked on the host, one H2D copy
+            b = np.asarray(batch_ids)
+            unsorted = b.size > 1 and not bool(np.all(b[1:] > b[:-1]))
+            ids = torch.from_numpy(np.ascontiguousarray(b, dtype=np.int32)).to("cuda", non_blocking=True)
         n = int(ids.numel())
         if n > self.max_batch:
             raise ValueError("batch larger than the engine was sized for")
-        if n > 1 and not bool((ids[1:] > ids[:-1]).all()):
+        if unsorted:
             raise ValueError("retrieve expects a sorted, duplicate-free batch (an AccessTrace batch)")
         self.n_dev.fill_(n)
         worker = batch_index % self.cfg.num_devices

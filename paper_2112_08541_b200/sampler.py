@@ -262,6 +262,21 @@ def _to_i32_device(a) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.int64)).astype(np.int32)).cuda()
 
 
+_TABLES: dict = {}
+
+
+def _batch_table(seed: int, batch_seed: int) -> torch.Tensor:
+    """PCG64 jump table of default_rng((seed, batch_seed)) (sampler.py:61-62),
+    built once per (seed, batch) on this device and reused by later calls."""
+    key = (int(seed), int(batch_seed), torch.cuda.current_device())
+    t = _TABLES.get(key)
+    if t is None:
+        if len(_TABLES) >= 4096:
+            _TABLES.clear()
+        t = _TABLES[key] = pcg_tables(pcg_states(seed, [batch_seed]))[0]
+    return t
+
+
 def sample_batch(g, seeds, cfg: SamplingConfig, batch_seed: int = 0):
     """Per-hop frontiers (with duplicates) and the sorted distinct-node set
     (sampler.py:97-116)."""
@@ -269,9 +284,9 @@ def sample_batch(g, seeds, cfg: SamplingConfig, batch_seed: int = 0):
     if len(seeds) == 0:
         raise ValueError("seeds must be nonempty")
     s = _sampler_for(g, cfg.fanouts, len(seeds), rng=cfg.rng)
-    table = pcg_tables(pcg_states(cfg.seed, [batch_seed]))
+    table = _batch_table(cfg.seed, batch_seed)
     s.load_seeds(_to_i32_device(seeds))
-    s.run(table[0])
+    s.run(table)
     counts = s.host_counts()
     frontiers = [s.frontier(h, counts).cpu().numpy().astype(np.int64) for h in range(s.H)]
     distinct = s.distinct().cpu().numpy().astype(np.int64)
@@ -286,9 +301,8 @@ def sample_batch_relabelled(g, seeds, cfg: SamplingConfig, batch_seed: int = 0):
     if len(seeds) == 0:
         raise ValueError("seeds must be nonempty")
     s = _sampler_for(g, cfg.fanouts, len(seeds), relabel=True, rng=cfg.rng)
-    table = pcg_tables(pcg_states(cfg.seed, [batch_seed]))
     s.load_seeds(_to_i32_device(seeds))
-    s.run(table[0])
+    s.run(_batch_table(cfg.seed, batch_seed))
     counts = s.host_counts()
     edges = []
     for h in range(s.H):
@@ -324,6 +338,10 @@ def simulate_epoch(g, p, schedule, cfg: SamplingConfig):
         offs = np.concatenate([[0], np.cumsum([len(b) for b in batches])])
         flat_dev = _to_i32_device(flat)
         origins = [torch.empty(max(c, 1), dtype=torch.int32, device="cuda") for c in s.caps]
+        # the epoch's trace, appended batch by batch on the device: at most
+        # min(n, b * (1 + sum of prod fanouts)) distinct IDs per batch
+        trace_buf = torch.empty(max(1, len(batches) * s.max_uniq), dtype=torch.int32, device="cuda")
+        trace_off = torch.zeros(len(batches) + 1, dtype=torch.int64, device="cuda")
         lib = _lib.load()
         st = _lib.stream_ptr()
         base = s.nodes.data_ptr()
@@ -347,7 +365,12 @@ def simulate_epoch(g, p, schedule, cfg: SamplingConfig):
                                             s.caps[h + 1], origins[h + 1].data_ptr(), st))
 
             s.run(tables[i], hooks=account)
-            trace.append(s.distinct().cpu().numpy().astype(np.int64))
+            # the batch's row of the trace stays on the device (no host sync per batch)
+            _lib.check(lib.bgl_trace_append(s.uniq.data_ptr(), s.num_uniq.data_ptr(), s.max_uniq,
+                                            trace_buf.data_ptr(), trace_off.data_ptr(), i, st))
+        off = trace_off.cpu().numpy()
+        flat_trace = trace_buf[: int(off[-1])].cpu().numpy().astype(np.int64)
+        trace = [flat_trace[off[i]:off[i + 1]] for i in range(len(batches))]
     lr = local_remote.cpu().tolist()
     return (AccessTrace(batches=trace),
             EpochCommReport(local_accesses=int(lr[0]), remote_accesses=int(lr[1]),

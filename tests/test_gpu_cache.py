@@ -280,3 +280,34 @@ def test_compare_policies_and_amortized_ops_match_reference(golden):
                                                                       num_devices=2)))
     assert [amort[k] for k in ("lookups_per_batch", "insertions_per_batch", "evictions_per_batch",
                                "metadata_updates_per_batch")] == npz["amortized"].tolist()
+
+
+@pytest.mark.parametrize("d,cap,hcap", [(1, 40, 0), (3, 17, 8), (4, 0, 16), (2, 64, 64)])
+def test_level_counters_match_reference_levels(d, cap, hcap):
+    """FifoLevelView.insertions / .evictions / .metadata_updates of every
+    device level and of the host level equal the reference levels' counters
+    (_Level, cachesim.py:45-49; FifoLevel.insert :94-104) after a run of
+    sorted, unsorted and duplicated batches (the oracle's FifoRing keeps the
+    same per-level counters and is pinned to the reference's rings)."""
+    from paper_2112_08541_b200.cachesim import CacheConfig, cold_state, simulate
+    from paper_2112_08541_b200.sampler import AccessTrace
+    rng = np.random.default_rng(11 + d + cap)
+    batches = []
+    for i in range(30):
+        b = rng.choice(300, size=int(rng.integers(1, 90)), replace=False)
+        if i % 3 == 0:
+            b = np.sort(b)
+        elif i % 3 == 1:
+            b = np.concatenate([b, b[: max(1, b.size // 4)]])
+        batches.append(b.astype(np.int64))
+    cfg = CacheConfig(device_capacity=cap, host_capacity=hcap, num_devices=d, feature_bytes_per_node=16)
+    state = cold_state(cfg)
+    rep = simulate(AccessTrace(batches=batches), cfg, state=state)
+    ref = co.FifoEngine(cap, hcap, d)
+    cnt, _ = ref.run(batches)
+    assert rep.batch_insertions == cnt[:, 5].tolist() and rep.batch_evictions == cnt[:, 6].tolist()
+    for h in range(d):
+        lv = state.devices[h]
+        assert (lv.insertions, lv.evictions, lv.metadata_updates) == (ref.devices[h].insertions,
+                                                                      ref.devices[h].evictions, 0), h
+    assert (state.host.insertions, state.host.evictions) == (ref.host.insertions, ref.host.evictions)
