@@ -358,6 +358,20 @@ int bgl_gather_rows_push(const int32_t* ids, const int64_t* src_row, const int64
                          const void* ring_rows, const void* table, int64_t row_bytes, void* out,
                          void* push_out, const int32_t* push_pos, int32_t mode, int32_t ctas,
                          void* stream);
+/* Shared host level in the multi-GPU engine (the reference's single host
+ * level, cachesim.py:202, lookups :330-334, inserts :343-344), owned by one
+ * GPU. bgl_push_pairs: dst_ids[i] = ids[pos[i]], dst_pos[i] = pos[i] for
+ * i < *n_dev and *dst_cnt = *n_dev (the worker's ascending device-missed IDs
+ * into the owner's receive area; dst may be peer memory; system fence).
+ * bgl_host_level_codes: dst_codes[pos[i]] = hl_codes[i] == D ? H : M (the
+ * owner's single-level FIFO standing in for the host level: its hits are host
+ * hits). bgl_host_level_account: counters[3] += hl[1], counters[4] -= hl[1],
+ * counters[5..6] += hl[5..6], then hl = 0. */
+int bgl_push_pairs(const int32_t* ids, const int32_t* pos, const int64_t* n_dev, int64_t max_n, int32_t* dst_ids,
+                   int32_t* dst_pos, int64_t* dst_cnt, void* stream);
+int bgl_host_level_codes(const uint8_t* hl_codes, const int32_t* pos, const int64_t* n_dev, int64_t max_n,
+                         uint8_t* dst_codes, void* stream);
+int bgl_host_level_account(int64_t* hl_counters, int64_t* counters, void* stream);
 /* CUDA IPC of device buffers between the per-GPU processes (64-byte handles).
  * The handle names the whole allocation; *offset_out is dev_ptr's offset in
  * it (add it to the pointer bgl_ipc_open_handle returns). */

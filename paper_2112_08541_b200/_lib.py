@@ -87,6 +87,9 @@ PROTOTYPES = {
     "bgl_compact_codes": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "bgl_gather_rows_push": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i32,
                                              c_i32, c_vp]),
+    "bgl_push_pairs": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "bgl_host_level_codes": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "bgl_host_level_account": (ctypes.c_int, [c_vp, c_vp, c_vp]),
     "bgl_ipc_get_handle": (ctypes.c_int, [c_vp, c_vp, ctypes.POINTER(c_i64)]),
     "bgl_ipc_open_handle": (ctypes.c_int, [c_vp, ctypes.POINTER(c_vp)]),
     "bgl_ipc_close": (ctypes.c_int, [c_vp]),

@@ -213,6 +213,46 @@ compact_codes_kernel(const uint8_t* __restrict__ codes, const int64_t* __restric
     if (tile == ntiles - 1 && threadIdx.x == 0) *count_out = s_pre[0] + total;
 }
 
+// Host-level hand-off (the reference's one shared host level, cachesim.py:
+// 202, 330-344, owned by one GPU): the worker's device-missed IDs (ascending)
+// and their batch positions stored into the owner's receive area (peer memory).
+__global__ void push_pairs_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ pos,
+                                  const int64_t* __restrict__ n_dev, int32_t* __restrict__ dst_ids,
+                                  int32_t* __restrict__ dst_pos, int64_t* __restrict__ dst_cnt) {
+    const int64_t n = *n_dev;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t p = pos[i];
+        dst_ids[i] = ids[p];
+        dst_pos[i] = p;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *dst_cnt = n;
+    __threadfence_system();   // peer stores visible system-wide before the caller's barrier
+}
+
+// Owner side: the host level's lookup codes of a worker's device-missed IDs
+// (a single-level FIFO whose hits are the host hits) become H / M at their
+// batch positions in the worker's outcome codes (peer stores).
+__global__ void host_level_codes_kernel(const uint8_t* __restrict__ hl_codes, const int32_t* __restrict__ pos,
+                                        const int64_t* __restrict__ n_dev, uint8_t* __restrict__ dst_codes) {
+    const int64_t n = *n_dev;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst_codes[pos[i]] = hl_codes[i] == 0 ? (uint8_t)2 : (uint8_t)3;
+    __threadfence_system();
+}
+
+// Fold the host level's counters into the cache counters: its hits turn
+// device misses (counted M by the homes) into H; its inserts / evictions are
+// the host level's (CacheSimReport.batch_host_hits / _misses / _insertions /
+// _evictions, cachesim.py:346-356).
+__global__ void host_level_account_kernel(int64_t* __restrict__ hl_counters, int64_t* __restrict__ counters) {
+    if (threadIdx.x != 0) return;
+    counters[3] += hl_counters[1];
+    counters[4] -= hl_counters[1];
+    counters[5] += hl_counters[5];
+    counters[6] += hl_counters[6];
+    for (int k = 0; k < 8; ++k) hl_counters[k] = 0;
+}
+
 }  // namespace bgl
 
 using namespace bgl;
@@ -281,6 +321,28 @@ int bgl_scatter_rows(const int32_t* pos, const int64_t* n_dev, int64_t max_n, co
     scatter_rows_kernel<<<grid_for(max_n * 32, 256, 8), 256, 0, as_stream(stream)>>>(
         pos, n_dev, (const unsigned char*)rows, row_bytes, (unsigned char*)out);
     return launch_status("scatter_rows_kernel");
+}
+
+int bgl_push_pairs(const int32_t* ids, const int32_t* pos, const int64_t* n_dev, int64_t max_n, int32_t* dst_ids,
+                   int32_t* dst_pos, int64_t* dst_cnt, void* stream) {
+    BGL_CHECK_ARG(ids && pos && n_dev && dst_ids && dst_pos && dst_cnt, "bgl_push_pairs: null pointer");
+    push_pairs_kernel<<<grid_for(std::max<int64_t>(max_n, 1), 256, 4), 256, 0, as_stream(stream)>>>(
+        ids, pos, n_dev, dst_ids, dst_pos, dst_cnt);
+    return launch_status("push_pairs_kernel");
+}
+
+int bgl_host_level_codes(const uint8_t* hl_codes, const int32_t* pos, const int64_t* n_dev, int64_t max_n,
+                         uint8_t* dst_codes, void* stream) {
+    BGL_CHECK_ARG(hl_codes && pos && n_dev && dst_codes, "bgl_host_level_codes: null pointer");
+    host_level_codes_kernel<<<grid_for(std::max<int64_t>(max_n, 1), 256, 4), 256, 0, as_stream(stream)>>>(
+        hl_codes, pos, n_dev, dst_codes);
+    return launch_status("host_level_codes_kernel");
+}
+
+int bgl_host_level_account(int64_t* hl_counters, int64_t* counters, void* stream) {
+    BGL_CHECK_ARG(hl_counters && counters, "bgl_host_level_account: null pointer");
+    host_level_account_kernel<<<1, 32, 0, as_stream(stream)>>>(hl_counters, counters);
+    return launch_status("host_level_account_kernel");
 }
 
 int bgl_ipc_get_handle(void* dev_ptr, void* handle_out, int64_t* offset_out) {

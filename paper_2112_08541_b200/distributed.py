@@ -21,9 +21,12 @@ the batch in ascending ID order (cachesim.py:341-342). The reference only
     4. return      rows (+ outcome codes) back to the workers, all-to-all
     5. scatter     rows into batch order (bgl_scatter_rows)
 
-The host level of the reference is a single shared level (cachesim.py:202);
-it is not sharded, so the multi-GPU engine requires host_capacity == 0 (the
-single-process engine covers it exactly).
+The host level of the reference is a single shared level (cachesim.py:202),
+not sharded: `ShardedPipeline(host_capacity=...)` keeps it on one owner GPU,
+which is fed every worker's device-missed IDs in batch order and turns the
+codes of its hits from M into H (the rows are read from the host feature store
+either way, so it is accounting on the side, off the row path). The
+all-to-all baseline (`ShardedFeatureCache`) still requires host_capacity == 0.
 
 `ShardedFeatureCache` is written against two small interfaces -- `ops`
 (partition / scatter) and `engine` (serve one worker's bucket) -- whose
@@ -33,6 +36,9 @@ the test oracle in to check the exchange protocol without GPUs.
 
 from __future__ import annotations
 
+import math
+
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -314,7 +320,9 @@ class ShardedPipeline:
 
     def __init__(self, rank: int, world: int, dg, fanouts, batch_size: int, order: torch.Tensor, seed: int,
                  shard_capacity: int, features: torch.Tensor, num_batches: int | None = None, group=None,
-                 barrier=None, rng: str = "replay"):
+                 barrier=None, rng: str = "replay", host_capacity: int = 0, batch_devices=None,
+                 host_owner: int = 0):
+        from .cachesim import FifoCacheDevice
         from .sampler import BatchSampler, pcg_states, pcg_tables
         self.rank, self.world, self.group = rank, world, group
         self.b = int(batch_size)
@@ -353,13 +361,49 @@ class ShardedPipeline:
         self.compact_ws = torch.empty(int(_lib.load().bgl_compact_codes_workspace(maxu)), dtype=torch.uint8,
                                       device=dev)
         self.plans = [[self.engine.plan_buffers() for _ in range(W)] for _ in range(R)]
+        # batch -> worker routing (cachesim.py:309): round j's batches (j*W + p) % nb, p = 0..W-1, run on
+        # batch_devices[...]; each round must use every worker once (one batch per GPU per step)
+        self.route = None
+        if batch_devices is not None:
+            bd = np.asarray(batch_devices, dtype=np.int64)
+            if bd.size < self.num_batches or (bd[:self.num_batches] < 0).any() or (bd[:self.num_batches] >= W).any():
+                raise ValueError("worker device out of range")
+            period = self.num_batches // math.gcd(self.num_batches, W)
+            route = np.array([[bd[(j * W + q) % self.num_batches] for q in range(W)] for j in range(period)])
+            if any(sorted(r.tolist()) != list(range(W)) for r in route):
+                raise ValueError("batch_devices: every round of world consecutive batches must use each GPU once")
+            if not all(r.tolist() == list(range(W)) for r in route):
+                self.route = route
+        # the shared host level (cachesim.py:202): one FIFO level on the owner GPU, fed the workers' device-missed
+        # IDs in batch order; its hits turn those rows' codes from M into H (accounting only: H and M rows are
+        # both read from the host feature store)
+        self.host_capacity, self.host_owner = int(host_capacity), int(host_owner)
+        hl = self.host_capacity > 0
+        own = hl and rank == host_owner
+        self.hl = None
+        if own:
+            self.hl = FifoCacheDevice(CacheConfig(device_capacity=self.host_capacity, num_devices=1),
+                                      dg.num_nodes, 0)
+            self.hl.reserve(dg.num_nodes, maxu)
+            self.hl_codes = torch.empty(maxu, dtype=torch.uint8, device=dev)
+            self.hl_src = torch.empty(maxu, dtype=torch.int64, device=dev)
+            self.hl_mpos = torch.empty(maxu, dtype=torch.int32, device=dev)
+            self.hl_mcnt = torch.zeros(1, dtype=torch.int64, device=dev)
+            self.hl_counters = torch.zeros(8, dtype=torch.int64, device=dev)
+        shape = (R, W, maxu) if own else (1,)
+        self.hl_ids = torch.zeros(shape, dtype=torch.int32, device=dev)      # owner's receive area
+        self.hl_pos = torch.zeros(shape, dtype=torch.int32, device=dev)
+        self.hl_cnt = torch.zeros((R, W) if own else (1,), dtype=torch.int64, device=dev)
         self.counters = torch.zeros(8, dtype=torch.int64, device=dev)
         self.part_counts = torch.zeros(W, dtype=torch.int64, device=dev)
         lib = _lib.load()
         self.part_ws = torch.empty(int(lib.bgl_partition_workspace(maxu, W)), dtype=torch.uint8, device=dev)
-        ptrs, self._opened = ipc_map([self.recv_ids, self.recv_pos, self.recv_cnt, self.out_rows, self.out_codes],
-                                     rank, world, group)
-        rid, rpos, rcnt, orow, ocode = ptrs
+        ptrs, self._opened = ipc_map([self.recv_ids, self.recv_pos, self.recv_cnt, self.out_rows, self.out_codes,
+                                      self.hl_ids, self.hl_pos, self.hl_cnt], rank, world, group)
+        rid, rpos, rcnt, orow, ocode, hid, hpos, hcnt = ptrs
+        # this rank's slot in the host-level owner's receive area, per round set
+        self.hl_dst = [(hid[host_owner] + (r * W + rank) * maxu * 4, hpos[host_owner] + (r * W + rank) * maxu * 4,
+                        hcnt[host_owner] + (r * W + rank) * 8) for r in range(R)] if hl else None
         # this rank's slot in every home's receive area, per round set: [R][W] addresses
         slot = [[(r * W + rank) for _ in range(W)] for r in range(R)]
         self.peer_ids = torch.tensor([[rid[h] + slot[r][h] * maxu * 4 for h in range(W)] for r in range(R)],
@@ -386,7 +430,10 @@ class ShardedPipeline:
         # + dedup (mark, emit, reset); partition (count, scan, push); the worker's miss compaction +
         # gather; per bucket: lookup, insert (2), codes push, hit gather, row copy
         per_hop = 1 if rng == "counter" else 2
-        self.kernels_per_round = (1 + per_hop * len(fanouts) + 3) + 3 + (2 if W > 1 else 1) + W * 6
+        self.kernels_per_round = (1 + per_hop * len(fanouts) + 3) + 3 + (2 if W > 1 else 1) + W * 6 + \
+            ((1 + (W * 3 + 1 if own else 0)) if hl else 0)
+        self.s_hl = torch.cuda.Stream() if own else None
+        self.hl_done = torch.cuda.Event() if own else None
 
     def close(self) -> None:
         lib = _lib.load()
@@ -394,8 +441,22 @@ class ShardedPipeline:
             lib.bgl_ipc_close(p)
         self._opened = []
 
+    def position(self, j: int, w: int | None = None) -> int:
+        """Position (0..world-1) of worker w's batch in round j (w = this rank)."""
+        w = self.rank if w is None else w
+        if self.route is None:
+            return w
+        return int(np.flatnonzero(self.route[j % len(self.route)] == w)[0])
+
+    def workers(self, j: int) -> list[int]:
+        """Workers of round j's batches in batch order (the order every home
+        serves its buckets in: the global batch order of the reference)."""
+        if self.route is None:
+            return list(range(self.world))
+        return [int(w) for w in self.route[j % len(self.route)]]
+
     def batch_of(self, j: int) -> int:
-        return (j * self.world + self.rank) % self.num_batches
+        return (j * self.world + self.position(j)) % self.num_batches
 
     # -- stages ------------------------------------------------------------------
     def _S(self, j: int) -> None:
@@ -411,7 +472,7 @@ class ShardedPipeline:
                 self.s_sample.wait_event(self.reported[slot])
             _lib.call("bgl_stage_batch", self.order.data_ptr(), self.order.numel(), self.b, self.num_batches,
                       self.tables.data_ptr(), self.batch_counter.data_ptr(), s.nodes.data_ptr(), s.counts.data_ptr(),
-                      self.table_stage[slot].data_ptr(), None, None, self.world, self.rank,
+                      self.table_stage[slot].data_ptr(), None, None, self.world, self.position(j),
                       _lib.stream_ptr(self.s_sample))
             s.run(self.table_stage[slot], stream=self.s_sample)
             self.sampled[slot].record(self.s_sample)
@@ -435,7 +496,7 @@ class ShardedPipeline:
         with torch.cuda.stream(self.s_li):
             st = _lib.stream_ptr(self.s_li)
             self.s_li.wait_event(self.xdone[r])
-            for w in range(self.world):
+            for w in self.workers(j):            # batch order of the round
                 ids, pos, cnt = self.recv_ids[r, w], self.recv_pos[r, w], self.recv_cnt[r, w:w + 1]
                 plan, pcount = self.plans[r][w]
                 _lib.check(lib.bgl_cache_lookup_misses(h, ids.data_ptr(), cnt.data_ptr(), maxu, w,
@@ -477,6 +538,10 @@ class ShardedPipeline:
             else:
                 _lib.check(lib.bgl_gather_list(pos.data_ptr(), cnt.data_ptr(), maxu, s.uniq.data_ptr(), eng.table,
                                                rb, out.data_ptr(), None, None, eng.miss_rows_in_flight, ctas, st))
+            if self.hl_dst is not None:   # device-missed IDs + positions to the host level's owner
+                di, dp, dc = self.hl_dst[r]
+                _lib.check(lib.bgl_push_pairs(s.uniq.data_ptr(), pos.data_ptr(), cnt.data_ptr(), maxu, di, dp, dc,
+                                              st))
             if timing:
                 ev[1].record(self.s_miss)
                 self.miss_timing.append(ev)
@@ -499,13 +564,13 @@ class ShardedPipeline:
             st = _lib.stream_ptr(self.s_back)
             if timing:   # measurement pass (bench roofline, peer-push rate): the whole B stage
                 bev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-            for w in range(self.world):
-                plan, pcount = self.plans[r][w]
+            for wi, w in enumerate(self.workers(j)):   # batch order: a bucket's survivors land before the
+                plan, pcount = self.plans[r][w]          # next bucket's hits read the ring
                 cnt = self.recv_cnt[r, w:w + 1]
                 out_w = self.worker_rows[w] + r * maxu * rb
                 if not self._in_graph:
                     self.s_back.wait_event(self.miss_done[r][w])
-                if timing and w == 0:
+                if timing and wi == 0:
                     bev[0].record(self.s_back)     # after the first wait: the stage's own time
                 _lib.check(lib.bgl_gather_rows_push(self.recv_ids[r, w].data_ptr(),
                                                     self.src_row[r, w].data_ptr() if ring else None,
@@ -517,6 +582,35 @@ class ShardedPipeline:
             if timing:
                 bev[1].record(self.s_back)
                 self.back_timing.append(bev)
+
+    def _HL(self, j: int) -> None:
+        """Owner of the shared host level: per batch of round j in batch order,
+        the worker's device-missed IDs (pushed in M(j)) are looked up in the
+        host level (one FIFO level: hits = H, cachesim.py:330-334) and the
+        full misses inserted in ascending order (:343-344); the codes go back
+        to the worker as H / M at the rows' batch positions."""
+        if self.hl is None:
+            return
+        r, maxu = j % self.NR, self.maxu
+        lib = _lib.load()
+        h = self.hl.handle
+        with torch.cuda.stream(self.s_hl):
+            st = _lib.stream_ptr(self.s_hl)
+            for w in self.workers(j):
+                ids, pos, cnt = self.hl_ids[r, w], self.hl_pos[r, w], self.hl_cnt[r, w:w + 1]
+                _lib.check(lib.bgl_cache_lookup_misses(h, ids.data_ptr(), cnt.data_ptr(), maxu, 0,
+                                                       self.hl_codes.data_ptr(), self.hl_src.data_ptr(),
+                                                       self.hl_counters.data_ptr(), self.hl_mpos.data_ptr(),
+                                                       self.hl_mcnt.data_ptr(), st))
+                _lib.check(lib.bgl_cache_insert(h, ids.data_ptr(), maxu, None, self.hl_counters.data_ptr(), st))
+                _lib.check(lib.bgl_host_level_codes(self.hl_codes.data_ptr(), pos.data_ptr(), cnt.data_ptr(), maxu,
+                                                    self.worker_codes[w] + r * maxu, st))
+            self.hl_done.record(self.s_hl)
+        # fold into the cache counters on the LI stream (its insert kernels update them too)
+        with torch.cuda.stream(self.s_li):
+            self.s_li.wait_event(self.hl_done)
+            _lib.check(lib.bgl_host_level_account(self.hl_counters.data_ptr(), self.counters.data_ptr(),
+                                                  _lib.stream_ptr(self.s_li)))
 
     def prime(self) -> None:
         """Prologue: S(0..2), X(0), LI(0), M(0), X(1), LI(1)."""
@@ -545,16 +639,20 @@ class ShardedPipeline:
 
     PHASES = 12            # lcm(NR, NSMP): one captured graph per step phase
 
+    def _streams(self):
+        return [x for x in (self.s_sample, self.s_li, self.s_miss, self.s_back, self.s_hl) if x is not None]
+
     def _step_body(self, k: int) -> None:
         main = torch.cuda.current_stream()
-        for x in (self.s_sample, self.s_li, self.s_miss, self.s_back):   # fork (graph capture needs it)
+        for x in self._streams():                  # fork (graph capture needs it)
             x.wait_stream(main)
         self._S(k + 3)
         self._X(k + 2)
         self._LI(k + 2)
         self._M(k + 1)
         self._B(k)
-        for x in (self.s_sample, self.s_li, self.s_miss, self.s_back):   # the step ends when all its work has
+        self._HL(k)
+        for x in self._streams():                  # the step ends when all its work has
             main.wait_stream(x)
         self.barrier()                                              # every home's pushes of round k landed
 
@@ -563,6 +661,8 @@ class ShardedPipeline:
         barriers: NCCL collectives are capturable). Cross-step event waits are
         dropped inside the graphs -- replay order already puts each step
         after the whole previous one."""
+        if self.route is not None:
+            raise ValueError("batch_devices routing runs eager steps: the captured graphs bake in the bucket order")
         self.prime()
         torch.cuda.synchronize()
         saved = self.batch_counter.clone()

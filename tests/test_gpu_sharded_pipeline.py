@@ -37,7 +37,13 @@ def _order():
     return dg_train.astype(np.int32)
 
 
-def _worker(rank, world, port, cap, where, rounds, path):
+def _route(world, rounds):
+    """batch_devices with a different permutation of the GPUs every round."""
+    rng = np.random.default_rng(world * 7 + rounds)
+    return [int(w) for _ in range(rounds) for w in rng.permutation(world)]
+
+
+def _worker(rank, world, port, cap, where, rounds, path, host=0, routed=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -52,7 +58,8 @@ def _worker(rank, world, port, cap, where, rounds, path):
     feats = synthetic_features(N, DIM, seed=8, device_resident=(where == "hbm"))
     order = torch.from_numpy(_order()).cuda()
     pipe = ShardedPipeline(rank, world, dg, FAN, B, order, SEED, cap, feats, num_batches=rounds * world,
-                           barrier=host_barrier)
+                           barrier=host_barrier, host_capacity=host,
+                           batch_devices=_route(world, rounds) if routed else None)
     out = {}
     for j in range(rounds):
         pipe.step()
@@ -77,12 +84,20 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("where,cap,world", [("host", 700, 2), ("hbm", 300, 2), ("host", 500, 3)])
-def test_sharded_pipeline_matches_reference(where, cap, world):
+@pytest.mark.parametrize("where,cap,world,host,routed", [("host", 700, 2, 0, False), ("hbm", 300, 2, 0, False),
+                                                         ("host", 500, 3, 0, False), ("host", 600, 2, 8, False),
+                                                         ("host", 400, 3, 64, False), ("host", 500, 2, 0, True),
+                                                         ("hbm", 300, 3, 64, True)])
+def test_sharded_pipeline_matches_reference(where, cap, world, host, routed):
+    """... with the shared host level on GPU 0 (host = its capacity,
+    cachesim.py:202, 330-344) and with batch_devices routing (a different GPU
+    permutation every round, cachesim.py:309) against the reference's
+    d-device simulation with the same host level and routing."""
     rounds = 6
     with tempfile.TemporaryDirectory() as td:
         path = os.path.join(td, "res")
-        mp.spawn(_worker, args=(world, _free_port(), cap, where, rounds, path), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), cap, where, rounds, path, host, routed), nprocs=world,
+                 join=True)
         res = {}
         for r in range(world):
             res.update({k + (f"_r{r}" if k == "counters" else ""): v for k, v in np.load(path + f".{r}.npz").items()})
@@ -98,13 +113,28 @@ def test_sharded_pipeline_matches_reference(where, cap, world):
     # the pipeline's lookups run two rounds ahead (LI(k+2) in step k): rounds
     # 0..rounds+1, batch indices wrapping over the epoch
     seq = [distinct[i % nb] for i in range((rounds + 2) * world)]
-    ref_cnt, ref_codes = co.FifoEngine(cap, 0, world).run(seq)
+    route = _route(world, rounds) if routed else None
+    bd = None if route is None else [route[i % nb] for i in range(len(seq))]
+    eng = co.FifoEngine(cap, host, world)
+    ref_cnt, ref_codes = eng.run(seq, bd)
     for i in range(nb):
         assert np.array_equal(res[f"ids{i}"], distinct[i]), i
         assert np.array_equal(res[f"codes{i}"], ref_codes[i]), i
         assert np.array_equal(res[f"rows{i}"], fo.synthetic_features(distinct[i], DIM, seed=8)), i
     tot = sum(res[f"counters_r{r}"] for r in range(world))
-    assert tot[:7].tolist() == np.asarray(ref_cnt).sum(axis=0)[:7].tolist()
+    ref = np.asarray(ref_cnt).sum(axis=0)
+    if host == 0:
+        assert tot[:7].tolist() == ref[:7].tolist()
+        return
+    # the device levels' lookups ran two rounds ahead, the host level (step k
+    # serves round k) did not: H, host inserts and evictions cover rounds 0..R-1
+    first = co.FifoEngine(cap, host, world)
+    cnt_r, _ = first.run(seq[:nb], None if bd is None else bd[:nb])
+    h_r = int(np.asarray(cnt_r)[:, 3].sum())
+    assert tot[:3].tolist() == ref[:3].tolist()
+    assert int(tot[3]) == h_r and int(tot[3] + tot[4]) == int(ref[3] + ref[4])
+    assert int(tot[5]) == int(ref[5]) - eng.host.insertions + first.host.insertions
+    assert int(tot[6]) == int(ref[6]) - eng.host.evictions + first.host.evictions
 
 
 def test_sharded_pipeline_graphs_single_rank_nccl():
