@@ -153,9 +153,11 @@ def build_inputs(cfg, features_where: str, graph_kind: str = "exact", shared=Non
     t1 = time.time()
     if shared is not None and features_where == "host":
         lr, lw, barrier = shared
-        feats = shared_synthetic_features(cfg["n"], cfg["dim"], GRAPH_SEED,
-                                          f"bgl_features_{os.environ.get('MASTER_PORT', '0')}", lr, lw, barrier)
+        feats, store_plan = shared_synthetic_features(cfg["n"], cfg["dim"], GRAPH_SEED,
+                                                      f"bgl_features_{os.environ.get('MASTER_PORT', '0')}", lr, lw,
+                                                      barrier)
     else:
+        store_plan = None
         feats = synthetic_features(cfg["n"], cfg["dim"], seed=GRAPH_SEED,
                                    device_resident=(features_where == "hbm"))
     torch.cuda.synchronize()
@@ -168,8 +170,11 @@ def build_inputs(cfg, features_where: str, graph_kind: str = "exact", shared=Non
         order, _ = proximity_schedule_device(dg, cfg["S"], cfg["b"], seed=RUN_SEED)
     torch.cuda.synchronize()
     t3 = time.time()
-    return dg, feats, order, {"graph_gen_s": round(t1 - t0, 3), "features_gen_s": round(t2 - t1, 3),
-                              "ordering_epoch_s": round(t3 - t2, 3)}
+    setup = {"graph_gen_s": round(t1 - t0, 3), "features_gen_s": round(t2 - t1, 3),
+             "ordering_epoch_s": round(t3 - t2, 3)}
+    if store_plan is not None:
+        setup["feature_store"] = store_plan
+    return dg, feats, order, setup
 
 
 def host_link_peak_gbs():
@@ -416,7 +421,7 @@ def dropin_e2e(args, cfg, dg, feats, order_host, max_uniq):
     scfg = SamplingConfig(fanouts=tuple(cfg["fanouts"]), batch_size=b, seed=RUN_SEED, rng=args.rng)
     ccfg = CacheConfig(device_capacity=int(cfg["cache_frac"] * cfg["n"]), feature_bytes_per_node=cfg["dim"] * 4)
     eng = FeatureCacheEngine(ccfg, feats, max_uniq)
-    simulate_epoch(dg, None, BatchSchedule(batches=sched.batches[:2], batch_size=b), scfg)   # warm the kernels
+    simulate_epoch(dg, None, BatchSchedule(batches=sched.batches[:2], batch_size=b, policy="proximity"), scfg)   # warm the kernels
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     trace, _ = simulate_epoch(dg, None, sched, scfg)

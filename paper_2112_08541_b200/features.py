@@ -42,34 +42,159 @@ def synthetic_features(num_nodes: int, dim: int, seed: int = 0, pinned: bool = T
     return out
 
 
+def numa_nodes() -> list[int]:
+    """Memory NUMA nodes of this host (/sys/devices/system/node)."""
+    base = "/sys/devices/system/node"
+    try:
+        nodes = sorted(int(d[4:]) for d in os.listdir(base) if d.startswith("node") and d[4:].isdigit())
+    except OSError:
+        return [0]
+    return nodes or [0]
+
+
+def gpu_numa_node(device_index: int) -> int:
+    """NUMA node of a GPU's PCIe root (sysfs numa_node of its bus id; 0 when
+    the platform reports none)."""
+    import subprocess
+    try:
+        bus = subprocess.run(["nvidia-smi", "-i", str(device_index), "--query-gpu=pci.bus_id",
+                              "--format=csv,noheader"], capture_output=True, text=True, timeout=20).stdout.strip()
+        dom, rest = bus.split(":", 1)
+        path = f"/sys/bus/pci/devices/{dom[-4:].lower()}:{rest.lower()}/numa_node"
+        node = int(open(path).read().strip())
+        return max(node, 0)
+    except Exception:  # noqa: BLE001 -- no nvidia-smi / sysfs entry: one node
+        return 0
+
+
+MPOL_BIND, MPOL_INTERLEAVE = 2, 3
+
+
+def mbind(addr: int, length: int, mode: int, nodes) -> bool:
+    """mbind(2) on [addr, addr + length): the memory policy new pages of the
+    range are allocated with (tmpfs mappings keep it as the shared policy of
+    the file, so pages faulted by any process follow it). False if the kernel
+    refuses (e.g. a container without the syscall)."""
+    import ctypes
+    import platform
+    nr = {"x86_64": 237, "aarch64": 235}.get(platform.machine())
+    if nr is None:
+        return False
+    nodes = list(nodes)
+    maxnode = max(nodes) + 2
+    words = (maxnode + 63) // 64
+    mask = (ctypes.c_ulong * words)()
+    for n in nodes:
+        mask[n // 64] |= 1 << (n % 64)
+    libc = ctypes.CDLL(None, use_errno=True)
+    page = os.sysconf("SC_PAGE_SIZE")
+    start = addr - addr % page
+    rc = libc.syscall(nr, ctypes.c_void_p(start), ctypes.c_ulong(length + (addr - start)), ctypes.c_int(mode),
+                      mask, ctypes.c_ulong(maxnode), ctypes.c_uint(0))
+    return rc == 0
+
+
+def feature_store_plan(nbytes: int, local_world: int, gpu_node: int, mode: str | None = None) -> dict:
+    """Where the box's shared host feature store lives (multi-GPU):
+      * one NUMA node: one /dev/shm copy, no policy;
+      * several nodes, room for one copy per GPU node in /dev/shm
+        ("replicate", the default): each GPU reads a replica bound to its own
+        node, so the N host links' miss reads do not cross the socket link;
+      * otherwise ("interleave"): one copy with its pages interleaved over all
+        nodes, so the reads spread over every socket's DRAM channels.
+    /dev/shm must hold the copies; if not, "private": every process pins its
+    own copy (when the RAM allows it; else an error naming the shortfall)."""
+    nodes = numa_nodes()
+    try:
+        st = os.statvfs("/dev/shm")
+        shm_free = st.f_bavail * st.f_frsize
+    except OSError:
+        shm_free = 0
+    mode = mode or os.environ.get("BGL_FEATURE_NUMA", "replicate")
+    plan = {"numa_nodes": len(nodes), "shm_free_gb": round(shm_free / 1e9, 1), "gpu_node": gpu_node,
+            "bytes": nbytes}
+    if len(nodes) == 1 or mode == "none":
+        plan.update(policy="single", copies=1)
+    elif mode == "replicate" and shm_free >= nbytes * len(nodes) * 1.02:
+        plan.update(policy="replicate", copies=len(nodes))
+    else:
+        plan.update(policy="interleave", copies=1)
+    if shm_free < nbytes * plan["copies"] * 1.02:
+        avail = 0
+        try:
+            for line in open("/proc/meminfo"):
+                if line.startswith("MemAvailable:"):
+                    avail = int(line.split()[1]) * 1024
+        except OSError:
+            pass
+        if avail < nbytes * local_world * 1.05:
+            raise MemoryError(f"host feature store of {nbytes / 1e9:.1f} GB: /dev/shm has {shm_free / 1e9:.1f} GB free "
+                              f"and {local_world} private copies need {nbytes * local_world / 1e9:.1f} GB of "
+                              f"{avail / 1e9:.1f} GB available")
+        plan.update(policy="private", copies=local_world)
+    return plan
+
+
 def shared_synthetic_features(num_nodes: int, dim: int, seed: int, name: str, local_rank: int, local_world: int,
-                              barrier, chunk_rows: int = 1 << 20) -> torch.Tensor:
+                              barrier, chunk_rows: int = 1 << 20, numa: str | None = None):
     """One feature store for all GPU processes of a box: a /dev/shm mapping
     (tmpfs) that every process registers as mapped pinned memory
     (bgl_host_register), so the GPUs' miss gathers read the same host copy
-    zero-copy (papers100M: 57 GB once, not once per GPU). The processes fill
-    disjoint chunks; `barrier()` is a collective over the box's processes."""
-    import os
-    path = os.path.join("/dev/shm", name)
+    zero-copy (papers100M: 57 GB once, not once per GPU) -- NUMA-aware
+    (feature_store_plan): on a multi-socket box one replica per GPU node or
+    interleaved pages. The processes fill disjoint chunks; `barrier()` is a
+    collective over the box's processes. Returns (features, plan)."""
     numel = num_nodes * dim
-    if local_rank == 0:
+    nbytes = numel * 4
+    import torch.distributed as dist
+    my_node = gpu_numa_node(torch.cuda.current_device())
+    plan = feature_store_plan(nbytes, local_world, my_node, numa)
+    multi = dist.is_initialized() and local_world > 1
+    if multi:                    # every process follows local rank 0's decision
+        plans = [None] * dist.get_world_size()
+        dist.all_gather_object(plans, plan)
+        plan = dict(plans[dist.get_rank() - local_rank], gpu_node=my_node)
+    if plan["policy"] == "private":
+        t = synthetic_features(num_nodes, dim, seed)
+        barrier()
+        barrier()
+        return t, plan
+    nodes = numa_nodes()
+    replica = nodes.index(my_node) if plan["policy"] == "replicate" and my_node in nodes else 0
+    path = os.path.join("/dev/shm", f"{name}_{replica}")
+    # which processes fill which replica: every process fills its own replica's share
+    if multi:
+        every = [None] * dist.get_world_size()
+        dist.all_gather_object(every, replica)
+        base = dist.get_rank() - local_rank
+        nodes_all = every[base:base + local_world]
+    else:
+        nodes_all = [replica]
+    fillers = [r for r in range(local_world) if nodes_all[r] == replica]
+    creator = fillers[0]
+    if local_rank == creator:
         t = torch.from_file(path, shared=True, size=numel, dtype=torch.float32)
+        if plan["policy"] == "replicate":
+            plan["mbind"] = mbind(t.data_ptr(), nbytes, MPOL_BIND, [my_node])
+        elif plan["policy"] == "interleave":
+            plan["mbind"] = mbind(t.data_ptr(), nbytes, MPOL_INTERLEAVE, nodes)
     barrier()
-    if local_rank != 0:
+    if local_rank != creator:
         t = torch.from_file(path, shared=True, size=numel, dtype=torch.float32)
     t = t.view(num_nodes, dim)
     buf = torch.empty((min(chunk_rows, num_nodes), dim), dtype=torch.float32, device="cuda")
+    me = fillers.index(local_rank)
     for ci, lo in enumerate(range(0, num_nodes, chunk_rows)):
-        if ci % local_world != local_rank:
+        if ci % len(fillers) != me:
             continue
         hi = min(num_nodes, lo + chunk_rows)
         _lib.call("bgl_synthetic_features", lo, hi - lo, dim, seed, buf.data_ptr(), _lib.stream_ptr())
         t[lo:hi].copy_(buf[: hi - lo], non_blocking=False)
     _lib.call("bgl_host_register", t.data_ptr(), numel * 4)
     barrier()
-    if local_rank == 0:
+    if local_rank == creator:
         os.unlink(path)          # every process holds its mapping; nothing leaks in /dev/shm
-    return t
+    return t, plan
 
 
 def table_pointer(features: torch.Tensor) -> int:

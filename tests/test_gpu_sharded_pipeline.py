@@ -187,7 +187,7 @@ def _shm_worker(rank, port, path):
     from paper_2112_08541_b200.features import shared_synthetic_features, table_pointer
     from paper_2112_08541_b200 import _lib
     n, dim = 50000, 24
-    t = shared_synthetic_features(n, dim, 5, f"bgl_test_{port}", rank, WORLD, dist.barrier, chunk_rows=7000)
+    t, plan = shared_synthetic_features(n, dim, 5, f"bgl_test_{port}", rank, WORLD, dist.barrier, chunk_rows=7000)
     ids = torch.from_numpy(np.random.default_rng(rank).integers(0, n, 3000).astype(np.int32)).cuda()
     pos = torch.arange(3000, dtype=torch.int32, device="cuda")
     cnt = torch.tensor([3000], dtype=torch.int64, device="cuda")
