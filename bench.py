@@ -414,9 +414,12 @@ def dropin_e2e(args, cfg, dg, feats, order_host, max_uniq):
     from paper_2112_08541_b200.cachesim import CacheConfig, simulate
     from paper_2112_08541_b200.features import FeatureCacheEngine
     from paper_2112_08541_b200.ordering import BatchSchedule
-    from paper_2112_08541_b200.sampler import SamplingConfig, simulate_epoch
+    from paper_2112_08541_b200.sampler import AccessTrace, SamplingConfig, simulate_epoch
     b, nb = cfg["b"], args.warmup + args.steps
-    sched = BatchSchedule(batches=[order_host[i * b:(i + 1) * b].astype(np.int64) for i in range(nb)],
+    epoch = -(-order_host.size // b)
+    # the pipeline's window wraps over the epoch (batch i % epoch): whole epochs, then the rest
+    parts = [min(epoch, nb - e) for e in range(0, nb, epoch)]
+    sched = BatchSchedule(batches=[order_host[i * b:(i + 1) * b].astype(np.int64) for i in range(min(nb, epoch))],
                           batch_size=b, policy="proximity")
     scfg = SamplingConfig(fanouts=tuple(cfg["fanouts"]), batch_size=b, seed=RUN_SEED, rng=args.rng)
     ccfg = CacheConfig(device_capacity=int(cfg["cache_frac"] * cfg["n"]), feature_bytes_per_node=cfg["dim"] * 4)
@@ -424,7 +427,12 @@ def dropin_e2e(args, cfg, dg, feats, order_host, max_uniq):
     simulate_epoch(dg, None, BatchSchedule(batches=sched.batches[:2], batch_size=b, policy="proximity"), scfg)   # warm the kernels
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    trace, _ = simulate_epoch(dg, None, sched, scfg)
+    rows_of = []
+    for m in parts:
+        tr, _ = simulate_epoch(dg, None, BatchSchedule(batches=sched.batches[:m], batch_size=b, policy="proximity"),
+                               scfg)
+        rows_of += tr.batches
+    trace = AccessTrace(batches=rows_of)
     t1 = time.perf_counter()
     qbytes = 0
     for i, ids in enumerate(trace.batches):
@@ -542,7 +550,8 @@ def run_bgl(args, cfg):
             g_ms.append(t[3])
         if len(hist) >= 3:                     # back(k): D + P rows of batch k (looked up two steps ago)
             ca = hist[-3]
-            hbm_bytes.append(2 * (ca[1] + ca[2]) * rb)
+            # fused HBM gather: back(k) reads + writes every row of batch k
+            hbm_bytes.append(2 * ((ca[1] + ca[2] + ca[3] + ca[4]) if pipe.fused_hbm_gather else (ca[1] + ca[2])) * rb)
             hbm_ms.append(t[4])
     # host-link peak sampled twice (before the timed region and right after
     # the stage breakdown): the link rate of the pool's boxes drifts a few GB/s
@@ -573,9 +582,14 @@ def run_bgl(args, cfg):
     else:
         hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
             if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
-        # both gathers read HBM here: misses (front) and hits (back), 2 x rows x rb each
-        alg = statistics.mean(g_bytes_host) * 2 + statistics.mean(hbm_bytes)
-        t_g = gather_ms + statistics.mean(hbm_ms)
+        # both gathers read HBM here: misses (front) and hits (back), 2 x rows x rb each; fused: one
+        # gather_v4 pass over the whole batch in back(k), timed alone (the empty miss stage is not added)
+        if pipe.fused_hbm_gather:
+            alg = statistics.mean(hbm_bytes)
+            t_g = statistics.mean(hbm_ms)
+        else:
+            alg = statistics.mean(g_bytes_host) * 2 + statistics.mean(hbm_bytes)
+            t_g = gather_ms + statistics.mean(hbm_ms)
         achieved = alg / (t_g * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 3), "traffic": None,

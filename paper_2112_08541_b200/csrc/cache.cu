@@ -462,11 +462,112 @@ __global__ void copy_rows_kernel(const int32_t* __restrict__ plan, const int64_t
     }
 }
 
+// Bulk survivor copy (TMA): the survivors of a level are ascending batch
+// positions landing in consecutive ring slots (t + j) % C (cachesim.py:101-103),
+// so the destination is one contiguous run per level (two at the ring's wrap).
+// A warp takes kCopyChunk plan entries: every lane bulk-loads its row
+// (cp.async.bulk global -> shared, completion on the warp's mbarrier), then
+// every lane that starts a run of consecutive slots issues ONE bulk store of
+// the whole run (shared -> global). The batch rows are read row by row (they
+// sit between the batch's hits), the ring is written in long contiguous
+// stores; no registers carry the bytes. Needs row_bytes % 16 == 0.
+constexpr int kCopyChunk = 16;
+constexpr int kCopyWarps = 8;
+
+__device__ __forceinline__ unsigned cache_smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__global__ void __launch_bounds__(kCopyWarps * 32)
+copy_rows_bulk_kernel(const int32_t* __restrict__ plan, const int64_t* __restrict__ plan_count, int64_t stride,
+                      int64_t C, const unsigned char* __restrict__ batch_rows, unsigned char* __restrict__ rows,
+                      int64_t rb, const int32_t* __restrict__ row_index) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[kCopyWarps];
+    const int y = blockIdx.y;
+    const int lane = lane_id(), wid = warp_id();
+    unsigned char* stage = smem + (int64_t)wid * kCopyChunk * rb;
+    const unsigned bar = cache_smem_u32(&bars[wid]);
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const int64_t cnt = plan_count[y];
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    unsigned phase = 0;
+    for (int64_t j0 = w * kCopyChunk; j0 < cnt; j0 += nw * kCopyChunk) {
+        const int m = (int)((cnt - j0) < kCopyChunk ? (cnt - j0) : kCopyChunk);
+        int32_t slot = -1;
+        int64_t src = 0;
+        if (lane < m) {
+            const int2 pe = *reinterpret_cast<const int2*>(plan + 2 * ((int64_t)y * stride + j0 + lane));
+            slot = pe.y;
+            src = row_index ? (int64_t)__ldg(row_index + pe.x) : (int64_t)pe.x;
+        }
+        // the previous chunk's stores must have read the stage before it is refilled
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"((unsigned)(m * rb))
+                         : "memory");
+        __syncwarp();
+        if (lane < m)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         :: "r"(cache_smem_u32(stage + (int64_t)lane * rb)), "l"(batch_rows + src * rb),
+                            "r"((unsigned)rb), "r"(bar) : "memory");
+        const int32_t ps = __shfl_up_sync(0xffffffffu, slot, 1);
+        const bool start = lane < m && (lane == 0 || ps + 1 != slot);
+        const unsigned sm = __ballot_sync(0xffffffffu, start);
+        const unsigned after = sm & ~((lt << 1) | 1u);
+        const int next = after ? __ffs(after) - 1 : m;
+        asm volatile("{\n.reg .pred P;\nW_%=: mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n@!P bra W_%=;\n}"
+                     :: "r"(bar), "r"(phase) : "memory");
+        phase ^= 1u;
+        if (start)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                         :: "l"(rows + ((int64_t)y * C + slot) * rb), "r"(cache_smem_u32(stage + (int64_t)lane * rb)),
+                            "r"((unsigned)((next - lane) * rb)) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 }  // namespace bgl
 
 using namespace bgl;
 
 namespace {
+
+int launch_copy_rows(const bgl_cache* c, const int32_t* plan, const int64_t* plan_count, int64_t stride,
+                     const void* batch_rows, const int32_t* row_index, cudaStream_t st) {
+    // BGL_COPY_BULK=0: the register-staged warp-per-row copy (A/B)
+    static const bool bulk_env = [] {
+        const char* e = getenv("BGL_COPY_BULK");
+        return !(e && e[0] == '0');
+    }();
+    // (row_index != NULL: the multi-GPU path reads the rows from another GPU's
+    // output over peer memory -- kept on plain loads/stores there)
+    const bool bulk = bulk_env && row_index == nullptr && (c->rb % 16) == 0 && ((uintptr_t)batch_rows % 16) == 0 &&
+                      c->rb * kCopyChunk * kCopyWarps <= 200 * 1024;
+    if (bulk) {
+        const size_t smem = (size_t)c->rb * kCopyChunk * kCopyWarps;
+        if (smem > 48 * 1024)
+            BGL_TRY(cuda_status(cudaFuncSetAttribute(copy_rows_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)smem), "cudaFuncSetAttribute(copy_rows_bulk)"));
+        unsigned gx = (unsigned)std::min<int64_t>(ceil_div(stride, (int64_t)kCopyChunk * kCopyWarps),
+                                                  (int64_t)kNumSMs * 4);
+        dim3 grid(std::max(gx, 1u), c->d);
+        copy_rows_bulk_kernel<<<grid, kCopyWarps * 32, smem, st>>>(plan, plan_count, stride, c->C,
+                                                                   (const unsigned char*)batch_rows, c->rows, c->rb,
+                                                                   row_index);
+        return launch_status("copy_rows_bulk_kernel");
+    }
+    dim3 grid(grid_for(stride * 32, 256, 8), c->d);
+    copy_rows_kernel<<<grid, 256, 0, st>>>(plan, plan_count, stride, c->C, (const unsigned char*)batch_rows, c->rows,
+                                           c->rb, row_index);
+    return launch_status("copy_rows_kernel");
+}
 
 int alloc_fill(void** p, size_t bytes, int byte, const char* what) {
     if (bytes == 0) {
@@ -690,10 +791,7 @@ int bgl_cache_copy_rows(bgl_cache_t c, const int32_t* plan, const int64_t* plan_
     BGL_CHECK_ARG(c->rb > 0, "cache was created without feature rows");
     const int64_t stride = bgl_cache_plan_stride(c, max_sorted);
     if (c->C == 0 || max_sorted <= 0) return BGL_OK;
-    dim3 grid(grid_for(stride * 32, 256, 8), c->d);
-    copy_rows_kernel<<<grid, 256, 0, as_stream(stream)>>>(plan, plan_count, stride, c->C,
-                                                          (const unsigned char*)batch_rows, c->rows, c->rb, nullptr);
-    return launch_status("copy_rows_kernel");
+    return launch_copy_rows(c, plan, plan_count, stride, batch_rows, nullptr, as_stream(stream));
 }
 
 int bgl_cache_copy_rows_indexed(bgl_cache_t c, const int32_t* plan, const int64_t* plan_count, int64_t max_sorted,
@@ -702,10 +800,7 @@ int bgl_cache_copy_rows_indexed(bgl_cache_t c, const int32_t* plan, const int64_
     BGL_CHECK_ARG(c->rb > 0, "cache was created without feature rows");
     const int64_t stride = bgl_cache_plan_stride(c, max_sorted);
     if (c->C == 0 || max_sorted <= 0) return BGL_OK;
-    dim3 grid(grid_for(stride * 32, 256, 8), c->d);
-    copy_rows_kernel<<<grid, 256, 0, as_stream(stream)>>>(plan, plan_count, stride, c->C,
-                                                          (const unsigned char*)batch_rows, c->rows, c->rb, row_index);
-    return launch_status("copy_rows_kernel");
+    return launch_copy_rows(c, plan, plan_count, stride, batch_rows, row_index, as_stream(stream));
 }
 
 int bgl_cache_level_stats(bgl_cache_t c, int64_t* out_host) {
