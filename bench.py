@@ -71,6 +71,24 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
 
 
+class L2Flush:
+    """L2 flush between timed steps (outside the events): write a buffer
+    larger than the 126 MB L2, then read another one, so the step starts with
+    a cold AND clean L2 (the write alone leaves ~126 MB of dirty lines whose
+    write-back would be charged to the step's first kernels)."""
+
+    def __init__(self, nbytes: int = 256 << 20):
+        import torch
+        self.w = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        self.r = torch.ones(nbytes // 4, dtype=torch.int32, device="cuda")
+        self.sink = torch.empty((), dtype=torch.int64, device="cuda")
+
+    def __call__(self):
+        import torch
+        self.w.zero_()
+        torch.sum(self.r, out=self.sink)
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -248,7 +266,8 @@ def bench_config(cfg, args, world, csr_entries, max_degree, nb_total):
             "sampler_rng": args.rng, "ordering": args.order,
             "parallelism": "single" if world == 1 else f"dp{world}: batch i on GPU i % {world}, node-ID-sharded "
                                                        f"FIFO cache (home of v = v % {world})",
-            "l2": "flushed between timed steps (256 MB write, outside the events)",
+            "l2": "flushed between timed steps (256 MB write, then a 256 MB read that writes the dirty lines back; "
+                  "outside the events)",
             "batches_per_epoch": int(nb_total)}
 
 
@@ -496,7 +515,7 @@ def run_bgl(args, cfg):
     pipe.capture(fed=True)
     pipe.reset()
     peak_host = host_link_peak_gbs()
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+    flush = L2Flush()
 
     pipe.prime()
     for _ in range(args.warmup):
@@ -509,7 +528,7 @@ def run_bgl(args, cfg):
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clk:
         for k in range(args.steps):
-            flush.zero_()                  # L2 flush between timed steps (outside the events)
+            flush()                  # L2 flush between timed steps (outside the events)
             ev[k][0].record()
             pipe.step()                    # graph: cache+gather of batch k || sampling of batch k+1
             ev[k][1].record()
@@ -537,7 +556,7 @@ def run_bgl(args, cfg):
     for _ in range(R):
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
         cb = pipe.counters.clone()
-        flush.zero_()
+        flush()
         pipe.step_serial(evs)                  # a(k+4) + b(k+3) | LI(k+2) | miss(k+1) | back(k)
         torch.cuda.synchronize()
         hist.append((pipe.counters - cb).cpu().tolist())
@@ -642,7 +661,7 @@ def run_bgl(args, cfg):
     h2d = 0
     cur = torch.cuda.current_stream()
     for k in range(args.warmup, args.warmup + n_e2e):
-        flush.zero_()
+        flush()
         e = eev[k - args.warmup]
         e[0].record()
         cur.wait_event(pipe.fed_ready[(k + pipe.lookahead) % len(pipe.fed_ready)])   # this step's seeds are in
@@ -757,7 +776,7 @@ def run_sharded(args, cfg):
     b, rb, dim = cfg["b"], cfg["dim"] * 4, cfg["dim"]
     cap = int(cfg["cache_frac"] * cfg["n"]) // world
     nb_total = (order.numel() + b - 1) // b
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = L2Flush()
     order_host = order.cpu().numpy().astype(np.int32)
     seeds_pinned = torch.from_numpy(order_host).pin_memory()
 
@@ -803,7 +822,7 @@ def run_sharded(args, cfg):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(dev_index) as clk:
         for k in range(args.steps):
-            flush.zero_()
+            flush()
             ev[k][0].record()
             one_round(args.warmup + k)
             ev[k][1].record()
@@ -956,7 +975,7 @@ def sharded_roofline(args, pipe, feats, rb, flush, allreduce, allgather_list, sh
     for _ in range(R):
         r = (pipe.k + 1) % pipe.NR               # step k gathers the misses of round k + 1
         c0 = pipe.counters.clone()
-        flush.zero_()
+        flush()
         pipe.step_eager()
         torch.cuda.synchronize()
         rows.append(int(pipe.own_misses(r)[1].item()))   # this rank's own misses (the worker fetches them)

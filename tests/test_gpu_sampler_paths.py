@@ -1,6 +1,6 @@
 """GPU parity for the sampler's rare paths: hubs mixed into long runs (heavy
 gaps), candidate-list overflow and the exact top-k fallback (forced with a
-tiny list), and the A/B kernels (BGL_SAMPLER=cand|fused, BGL_SEG_ILP=0) — all bit-exact
+tiny list), and the A/B kernels (BGL_SAMPLER=cand|fused) — all bit-exact
 against the oracle on the same hub graph."""
 import os
 import subprocess
@@ -31,8 +31,6 @@ def test_hubs_inside_long_runs(ref_path):
     {"BGL_SEG_CAP": "1"},                              # almost every parent takes the fallback
     {"BGL_SAMPLER": "cand"},
     {"BGL_SAMPLER": "fused", "BGL_RUNS_PER_SM": "2"},
-    {"BGL_SEG_ILP": "0"},                              # one chunk per walk iteration (the round-1 walk)
-    {"BGL_SEG_ILP": "0", "BGL_SEG_CAP": "24", "BGL_RUNS_PER_SM": "1"},
 ])
 def test_rare_paths_under_env(env, ref_path):
     e = dict(os.environ, **env)
