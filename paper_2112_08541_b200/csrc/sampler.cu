@@ -499,7 +499,6 @@ sample_cand_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
 // its own range only. A parent with fewer than k candidates (or whose range
 // overflowed the list) is redone exactly with a warp top-k over all its draws.
 constexpr int kSegCap = 512;
-constexpr int kOutG = 4;   // candidate chunks whose col loads are batched (output phase)
 
 struct SegWarp {
     uint64_t cand[kSegCap];
@@ -568,6 +567,62 @@ __device__ __forceinline__ int seg_walk(SegWarp& sw, const PcgTable T, U128 A32,
     return L;
 }
 
+// The same walk two chunks per iteration: the states of walk positions w + 32
+// and w + 64 are both one affine map away from w's (A32 / A64), so the two
+// 16-mad carry chains of an iteration are independent (ILP 2) instead of one
+// chain per chunk; the chunks are still appended in walk order.
+template <bool kGaps>
+__device__ __forceinline__ int seg_walk2(SegWarp& sw, const PcgTable T, U128 A32, U128 C32, U128 A64, U128 C64,
+                                         int64_t d_run, int32_t Wtot, int lane, unsigned lt, int cap) {
+    int j = 0;
+    while (lane >= sw.wend[j]) ++j;
+    int nb = sw.wend[j], ws = sw.wst[j];
+    uint64_t th = sw.thr[j];
+    int64_t g = kGaps ? sw.gap[j] : 0;
+    U128 s = T.at((uint64_t)(d_run + lane + g + 1));
+    int L = 0;
+    for (int W = 0; W < Wtot; W += 64) {
+        U128 s2 = affine_mad(A32, C32, s);
+        U128 sn = affine_mad(A64, C64, s);
+        const int w = W + lane;
+        if (w >= nb) {
+            seg_take(sw, w, j, nb, th, ws);
+            if (kGaps) {
+                const int64_t gj = sw.gap[j];
+                if (gj != g && w < Wtot) {          // heavy parents' draws lie between
+                    const uint64_t dlt = (uint64_t)(gj - g);
+                    s = T.adv(s, dlt);
+                    s2 = T.adv(s2, dlt);
+                    sn = T.adv(sn, dlt);
+                    g = gj;
+                }
+            }
+        }
+        const uint64_t out = xsl_rr_fs(s);
+        seg_append(sw, out < th, (out & ~2047ull) | (uint64_t)(w - ws), j, L, lt, cap);
+        if (W + 32 < Wtot) {                        // warp-uniform
+            const int w2 = w + 32;
+            if (w2 >= nb) {
+                seg_take(sw, w2, j, nb, th, ws);
+                if (kGaps) {
+                    const int64_t gj = sw.gap[j];
+                    if (gj != g && w2 < Wtot) {
+                        const uint64_t dlt = (uint64_t)(gj - g);
+                        s2 = T.adv(s2, dlt);
+                        sn = T.adv(sn, dlt);
+                        g = gj;
+                    }
+                }
+            }
+            const uint64_t out2 = xsl_rr_fs(s2);
+            seg_append(sw, out2 < th, (out2 & ~2047ull) | (uint64_t)(w2 - ws), j, L, lt, cap);
+        }
+        s = sn;
+    }
+    return L;
+}
+
+template <bool kIlp2>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4)
 sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                   const int32_t* __restrict__ parents, const int64_t* __restrict__ num_parents_dev,
@@ -649,8 +704,16 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
         }
         __syncwarp();
         int L = 0;
-        if (Wtot > 0) L = hm ? seg_walk<true>(sw, T, A32, C32, D0 + pre_d, Wtot, lane, lt, cap)
-                             : seg_walk<false>(sw, T, A32, C32, D0 + pre_d, Wtot, lane, lt, cap);
+        if (Wtot > 0) {
+            if (kIlp2) {
+                const U128 A64 = T.A(6), C64 = T.C(6);
+                L = hm ? seg_walk2<true>(sw, T, A32, C32, A64, C64, D0 + pre_d, Wtot, lane, lt, cap)
+                       : seg_walk2<false>(sw, T, A32, C32, A64, C64, D0 + pre_d, Wtot, lane, lt, cap);
+            } else {
+                L = hm ? seg_walk<true>(sw, T, A32, C32, D0 + pre_d, Wtot, lane, lt, cap)
+                       : seg_walk<false>(sw, T, A32, C32, D0 + pre_d, Wtot, lane, lt, cap);
+            }
+        }
         __syncwarp();
         // each parent's candidates are one range of the (parent-ordered) list
         const int Ls = L < cap ? L : cap;
@@ -667,43 +730,25 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
         sw.cst[lane] = c_st;
         const bool fb = light && (c_own < (int)k || cut);
         __syncwarp();
-        // kOutG candidate chunks per round: their neighbour-ID loads (random
-        // reads of col) are all in flight before the first result is stored
-        for (int b0 = 0; b0 < Ls; b0 += 32 * kOutG) {
-            int32_t vv[kOutG];
-            int64_t dst[kOutG];
-            int32_t pj[kOutG];
-#pragma unroll
-            for (int g = 0; g < kOutG; ++g) {
-                const int i = b0 + g * 32 + lane;
-                const bool has = i < Ls;
-                const uint64_t key = has ? sw.cand[i] : ~0ull;
-                const int j = has ? (int)sw.cj[i] : 0;
-                const int kj = __shfl_sync(FULL, (int)k, j);
-                const int64_t offj = __shfl_sync(FULL, off, j);
-                const int64_t oij = __shfl_sync(FULL, ex_k, j);
-                const bool fbj = __shfl_sync(FULL, (int)fb, j) != 0;
-                const int e = __shfl_sync(FULL, c_st + c_own, j);
-                dst[g] = -1;
-                vv[g] = 0;
-                pj[g] = 0;
-                if (has && !fbj) {
-                    const int st = sw.cst[j];
-                    int rk = 0;
-                    for (int x = st; x < e; ++x) rk += sw.cand[x] < key;
-                    if (rk < kj) {
-                        vv[g] = __ldg(indices + offj + (int64_t)(key & 2047u));
-                        dst[g] = oij + rk;
-                        pj[g] = (int32_t)(r * run + j);
-                    }
-                }
-            }
-#pragma unroll
-            for (int g = 0; g < kOutG; ++g) {
-                if (dst[g] >= 0) {
-                    if (out_ids) out_ids[dst[g]] = vv[g];
-                    if (out_pidx) out_pidx[dst[g]] = pj[g];
-                    if (bitmap) mark_bit(bitmap, vv[g]);
+        for (int b0 = 0; b0 < Ls; b0 += 32) {
+            const int i = b0 + lane;
+            const bool has = i < Ls;
+            const uint64_t key = has ? sw.cand[i] : ~0ull;
+            const int j = has ? (int)sw.cj[i] : 0;
+            const int kj = __shfl_sync(FULL, (int)k, j);
+            const int64_t offj = __shfl_sync(FULL, off, j);
+            const int64_t oij = __shfl_sync(FULL, ex_k, j);
+            const bool fbj = __shfl_sync(FULL, (int)fb, j) != 0;
+            const int e = __shfl_sync(FULL, c_st + c_own, j);
+            if (has && !fbj) {
+                const int st = sw.cst[j];
+                int rk = 0;
+                for (int x = st; x < e; ++x) rk += sw.cand[x] < key;
+                if (rk < kj) {
+                    const int32_t v = indices[offj + (int64_t)(key & 2047u)];
+                    if (out_ids) out_ids[oij + rk] = v;
+                    if (out_pidx) out_pidx[oij + rk] = (int32_t)(r * run + j);
+                    if (bitmap) mark_bit(bitmap, v);
                 }
             }
         }
@@ -920,8 +965,14 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     const unsigned cap_blocks = (unsigned)kNumSMs * 8;
     if (blocks > cap_blocks) blocks = cap_blocks;               // runs are claimed dynamically
     if (max_ctas > 0 && blocks > (unsigned)max_ctas) blocks = (unsigned)max_ctas;
+    // BGL_SEG_ILP=0: one chunk per walk iteration (the round-1 kernel, A/B)
+    static const bool ilp2 = [] {
+        const char* e = getenv("BGL_SEG_ILP");
+        return !(e && e[0] == '0');
+    }();
     if (mode == 2) {
-        sample_seg_kernel<<<blocks, kWarpsPerBlock * 32, 0, st>>>(
+        auto kern = ilp2 ? sample_seg_kernel<true> : sample_seg_kernel<false>;
+        kern<<<blocks, kWarpsPerBlock * 32, 0, st>>>(
             indptr, indices, parents, num_parents_dev, fanout, table, draw_base, ss, w.deg_prefix, w.k_prefix,
             w.heavy, w.heavy_count, out_ids, out_parent_idx, num_out_dev, bm, (int32_t)run, heavy_deg, mar[0], mar[1],
             seg_cap);
