@@ -567,62 +567,6 @@ __device__ __forceinline__ int seg_walk(SegWarp& sw, const PcgTable T, U128 A32,
     return L;
 }
 
-// The same walk two chunks per iteration: the states of walk positions w + 32
-// and w + 64 are both one affine map away from w's (A32 / A64), so the two
-// 16-mad carry chains of an iteration are independent (ILP 2) instead of one
-// chain per chunk; the chunks are still appended in walk order.
-template <bool kGaps>
-__device__ __forceinline__ int seg_walk2(SegWarp& sw, const PcgTable T, U128 A32, U128 C32, U128 A64, U128 C64,
-                                         int64_t d_run, int32_t Wtot, int lane, unsigned lt, int cap) {
-    int j = 0;
-    while (lane >= sw.wend[j]) ++j;
-    int nb = sw.wend[j], ws = sw.wst[j];
-    uint64_t th = sw.thr[j];
-    int64_t g = kGaps ? sw.gap[j] : 0;
-    U128 s = T.at((uint64_t)(d_run + lane + g + 1));
-    int L = 0;
-    for (int W = 0; W < Wtot; W += 64) {
-        U128 s2 = affine_mad(A32, C32, s);
-        U128 sn = affine_mad(A64, C64, s);
-        const int w = W + lane;
-        if (w >= nb) {
-            seg_take(sw, w, j, nb, th, ws);
-            if (kGaps) {
-                const int64_t gj = sw.gap[j];
-                if (gj != g && w < Wtot) {          // heavy parents' draws lie between
-                    const uint64_t dlt = (uint64_t)(gj - g);
-                    s = T.adv(s, dlt);
-                    s2 = T.adv(s2, dlt);
-                    sn = T.adv(sn, dlt);
-                    g = gj;
-                }
-            }
-        }
-        const uint64_t out = xsl_rr_fs(s);
-        seg_append(sw, out < th, (out & ~2047ull) | (uint64_t)(w - ws), j, L, lt, cap);
-        if (W + 32 < Wtot) {                        // warp-uniform
-            const int w2 = w + 32;
-            if (w2 >= nb) {
-                seg_take(sw, w2, j, nb, th, ws);
-                if (kGaps) {
-                    const int64_t gj = sw.gap[j];
-                    if (gj != g && w2 < Wtot) {
-                        const uint64_t dlt = (uint64_t)(gj - g);
-                        s2 = T.adv(s2, dlt);
-                        sn = T.adv(sn, dlt);
-                        g = gj;
-                    }
-                }
-            }
-            const uint64_t out2 = xsl_rr_fs(s2);
-            seg_append(sw, out2 < th, (out2 & ~2047ull) | (uint64_t)(w2 - ws), j, L, lt, cap);
-        }
-        s = sn;
-    }
-    return L;
-}
-
-template <bool kIlp2>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4)
 sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                   const int32_t* __restrict__ parents, const int64_t* __restrict__ num_parents_dev,
@@ -704,16 +648,8 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
         }
         __syncwarp();
         int L = 0;
-        if (Wtot > 0) {
-            if (kIlp2) {
-                const U128 A64 = T.A(6), C64 = T.C(6);
-                L = hm ? seg_walk2<true>(sw, T, A32, C32, A64, C64, D0 + pre_d, Wtot, lane, lt, cap)
-                       : seg_walk2<false>(sw, T, A32, C32, A64, C64, D0 + pre_d, Wtot, lane, lt, cap);
-            } else {
-                L = hm ? seg_walk<true>(sw, T, A32, C32, D0 + pre_d, Wtot, lane, lt, cap)
-                       : seg_walk<false>(sw, T, A32, C32, D0 + pre_d, Wtot, lane, lt, cap);
-            }
-        }
+        if (Wtot > 0) L = hm ? seg_walk<true>(sw, T, A32, C32, D0 + pre_d, Wtot, lane, lt, cap)
+                             : seg_walk<false>(sw, T, A32, C32, D0 + pre_d, Wtot, lane, lt, cap);
         __syncwarp();
         // each parent's candidates are one range of the (parent-ordered) list
         const int Ls = L < cap ? L : cap;
@@ -965,14 +901,8 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     const unsigned cap_blocks = (unsigned)kNumSMs * 8;
     if (blocks > cap_blocks) blocks = cap_blocks;               // runs are claimed dynamically
     if (max_ctas > 0 && blocks > (unsigned)max_ctas) blocks = (unsigned)max_ctas;
-    // BGL_SEG_ILP=0: one chunk per walk iteration (the round-1 kernel, A/B)
-    static const bool ilp2 = [] {
-        const char* e = getenv("BGL_SEG_ILP");
-        return !(e && e[0] == '0');
-    }();
     if (mode == 2) {
-        auto kern = ilp2 ? sample_seg_kernel<true> : sample_seg_kernel<false>;
-        kern<<<blocks, kWarpsPerBlock * 32, 0, st>>>(
+        sample_seg_kernel<<<blocks, kWarpsPerBlock * 32, 0, st>>>(
             indptr, indices, parents, num_parents_dev, fanout, table, draw_base, ss, w.deg_prefix, w.k_prefix,
             w.heavy, w.heavy_count, out_ids, out_parent_idx, num_out_dev, bm, (int32_t)run, heavy_deg, mar[0], mar[1],
             seg_cap);
