@@ -567,7 +567,11 @@ __device__ __forceinline__ int seg_walk(SegWarp& sw, const PcgTable T, U128 A32,
     return L;
 }
 
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4)
+// WPB warps per CTA, MINB CTAs per SM: (8, 4) = 32 resident warps per SM
+// (64 registers); (6, 6) = 36 (56 registers), enough for the largest hop's
+// runs to start in one wave (153.6K parents / 32 = 4800 runs vs 4736 / 5328).
+template <int WPB, int MINB>
+__global__ void __launch_bounds__(WPB * 32, MINB)
 sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                   const int32_t* __restrict__ parents, const int64_t* __restrict__ num_parents_dev,
                   int32_t fanout, const uint64_t* __restrict__ table, int64_t* __restrict__ draw_base,
@@ -575,7 +579,7 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
                   int32_t* __restrict__ heavy, int64_t* __restrict__ heavy_count,
                   int32_t* __restrict__ out_ids, int32_t* __restrict__ out_pidx, int64_t* __restrict__ num_out,
                   uint32_t* __restrict__ bitmap, int32_t run, int64_t heavy_deg, float ma, float mb, int cap) {
-    __shared__ SegWarp s_seg[kWarpsPerBlock];
+    __shared__ SegWarp s_seg[WPB];
     SegWarp& sw = s_seg[warp_id()];
     const int64_t n = *num_parents_dev;
     const int64_t nruns = n > 0 ? ceil_div(n, run) : 1;
@@ -897,12 +901,19 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     // for the small hops were measured slower: the CTA kernel runs after it)
     const int64_t heavy_deg = kNarrowMaxDeg;
     ScanState ss = make_scan_state(w.scan, 2, w.max_tiles);
-    unsigned blocks = (unsigned)ceil_div(runs, kWarpsPerBlock);
+    // BGL_SEG_OCC=8x4 (default) | 6x6: warps per CTA x CTAs per SM of the segmented walk
+    static const int seg_wpb = [] {
+        const char* e = getenv("BGL_SEG_OCC");
+        return (e && std::string(e) == "6x6") ? 6 : 8;
+    }();
+    const int wpb = mode == 2 ? seg_wpb : kWarpsPerBlock;
+    unsigned blocks = (unsigned)ceil_div(runs, wpb);
     const unsigned cap_blocks = (unsigned)kNumSMs * 8;
     if (blocks > cap_blocks) blocks = cap_blocks;               // runs are claimed dynamically
     if (max_ctas > 0 && blocks > (unsigned)max_ctas) blocks = (unsigned)max_ctas;
     if (mode == 2) {
-        sample_seg_kernel<<<blocks, kWarpsPerBlock * 32, 0, st>>>(
+        auto kern = wpb == 6 ? sample_seg_kernel<6, 6> : sample_seg_kernel<8, 4>;
+        kern<<<blocks, wpb * 32, 0, st>>>(
             indptr, indices, parents, num_parents_dev, fanout, table, draw_base, ss, w.deg_prefix, w.k_prefix,
             w.heavy, w.heavy_count, out_ids, out_parent_idx, num_out_dev, bm, (int32_t)run, heavy_deg, mar[0], mar[1],
             seg_cap);

@@ -31,6 +31,8 @@ def test_hubs_inside_long_runs(ref_path):
     {"BGL_SEG_CAP": "1"},                              # almost every parent takes the fallback
     {"BGL_SAMPLER": "cand"},
     {"BGL_SAMPLER": "fused", "BGL_RUNS_PER_SM": "2"},
+    {"BGL_SEG_OCC": "6x6"},                            # 6 warps x 6 CTAs per SM walk
+    {"BGL_SEG_OCC": "6x6", "BGL_SEG_CAP": "24", "BGL_RUNS_PER_SM": "1"},
 ])
 def test_rare_paths_under_env(env, ref_path):
     e = dict(os.environ, **env)
