@@ -136,6 +136,22 @@ int bgl_relabel(const int32_t* keys, int32_t nseg, const int64_t* seg_off,
 int bgl_unique_reset(void* workspace, int64_t num_nodes, const int32_t* uniq,
                      const int64_t* num_uniq_dev, int64_t max_uniq, void* stream);
 
+/* Sparse int64 node IDs (IDs not dense in [0, 2^31)): np.unique(keys,
+ * return_inverse=True) with a GPU open-addressing hash table (linear probing,
+ * 64-bit atomicCAS claim) + an LSD radix sort of the distinct keys. Replaces
+ * the same np.unique (gnnio/sampler.py:115,157) where gnnio's dict-based FIFO
+ * (cachesim.py:81-107, simulate :275-363) accepts any int64 node ID.
+ * keys: int64[n], every key in [0, 2^key_bits) (key_bits 0 = 64; keys must be
+ * >= 0). Writes the ascending distinct keys to uniq_out[0..U) (may be NULL),
+ * U to *num_uniq_dev and rank_out[i] = rank of keys[i] (may be NULL). */
+size_t bgl_hash_unique_workspace(int64_t max_n);
+int bgl_hash_unique(const int64_t* keys, int64_t n, int32_t key_bits, void* workspace,
+                    int64_t* uniq_out, int64_t* num_uniq_dev, int32_t* rank_out, void* stream);
+/* home[i] = keys[i] % num_shards (cachesim.py:320) for i < *n_dev (n_dev may be
+ * NULL: max_n keys). */
+int bgl_key_home(const int64_t* keys, const int64_t* n_dev, int64_t max_n, int32_t num_shards,
+                 uint8_t* home, void* stream);
+
 /* ---------------------------------------------------------------- FIFO cache
  * BGL's dynamic FIFO feature cache (gnnio.cachesim FifoLevel, cachesim.py:
  * 81-107, engine cachesim.py:190-203, simulate cachesim.py:275-363).
@@ -158,6 +174,14 @@ int bgl_cache_reserve_batch(bgl_cache_t cache, int64_t max_batch);
  * cachesim.py:319-320); lookups code a hit D when worker == shard_index,
  * else P. Single-process handles keep the default (0 of num_shards). */
 int bgl_cache_set_shard(bgl_cache_t cache, int32_t shard_index, int32_t num_global_shards);
+/* Sparse node IDs: the cache runs on dense ranks (bgl_hash_unique) and the
+ * shard of rank r is home_of[r] (= the sparse ID % num_shards) instead of
+ * r % num_shards. home_of is caller-owned device memory that must outlive its
+ * use; NULL restores v % num_shards. */
+int bgl_cache_set_home_map(bgl_cache_t cache, const uint8_t* home_of);
+/* Rename every resident rank v to old_to_new[v] (NULL: keep) and rebuild the
+ * indices for a node space of new_num_nodes (the key set grew: ranks move). */
+int bgl_cache_remap(bgl_cache_t cache, const int32_t* old_to_new, int64_t new_num_nodes, void* stream);
 /* Device pointers of the ring feature rows ([num_shards*shard_capacity][row_bytes]). */
 void* bgl_cache_rows(bgl_cache_t cache);
 /* Classify every query against the pre-batch state (cachesim.py:318-339):

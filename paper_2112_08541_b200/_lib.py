@@ -43,6 +43,9 @@ PROTOTYPES = {
     "bgl_unique_sorted": (ctypes.c_int, [c_vp, c_i32, p_i64, c_vp, p_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "bgl_relabel": (ctypes.c_int, [c_vp, c_i32, p_i64, c_vp, p_i64, c_i64, c_vp, c_vp, c_vp]),
     "bgl_unique_reset": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_i64, c_vp]),
+    "bgl_hash_unique_workspace": (c_sz, [c_i64]),
+    "bgl_hash_unique": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "bgl_key_home": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
     "bgl_cache_create": (ctypes.c_int, [c_i64, c_i32, c_i64, c_i64, c_i64, ctypes.POINTER(c_vp)]),
     "bgl_cache_destroy": (ctypes.c_int, [c_vp]),
     "bgl_cache_reserve_nodes": (ctypes.c_int, [c_vp, c_i64, c_vp]),
@@ -50,6 +53,8 @@ PROTOTYPES = {
     "bgl_cache_reserve_batch": (ctypes.c_int, [c_vp, c_i64]),
     "bgl_cache_rows": (c_vp, [c_vp]),
     "bgl_cache_set_shard": (ctypes.c_int, [c_vp, c_i32, c_i32]),
+    "bgl_cache_set_home_map": (ctypes.c_int, [c_vp, c_vp]),
+    "bgl_cache_remap": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp]),
     "bgl_cache_lookup": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "bgl_cache_lookup_misses": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "bgl_cache_insert": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),

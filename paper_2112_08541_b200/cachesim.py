@@ -68,6 +68,8 @@ class FifoCacheDevice:
                                                 cfg.host_capacity, self.row_bytes, _lib.ctypes.byref(h)))
         self.handle = h.value
         self.max_batch = 0
+        self.keys = None     # sparse IDs: sorted int64 key of every dense rank (device)
+        self.home = None     # sparse IDs: uint8 shard of every dense rank (device)
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -86,6 +88,42 @@ class FifoCacheDevice:
         if max_batch > self.max_batch:
             _lib.check(lib.bgl_cache_reserve_batch(self.handle, int(max_batch)))
             self.max_batch = int(max_batch)
+
+    def adopt_keys(self, flat: np.ndarray) -> tuple[torch.Tensor, int]:
+        """Sparse node IDs (gnnio's FifoLevel is a dict, cachesim.py:81-107, so
+        any int64 ID is valid): run the rings on dense ranks. The key set
+        (resident keys + this trace) is deduplicated and sorted on the device by
+        the open-addressing hash table (`bgl_hash_unique`); ranks keep the ID
+        order, so every ascending insert list is the reference's; resident
+        ranks are renamed to their new ranks (`bgl_cache_remap`) and each
+        rank's shard is its ID % d (`bgl_cache_set_home_map`). Returns the
+        trace's ranks (int32, device) and the dense node-space size."""
+        lib = _lib.load()
+        st = _lib.stream_ptr()
+        new = torch.from_numpy(np.ascontiguousarray(flat, dtype=np.int64)).cuda()
+        if self.keys is not None:
+            old = self.keys
+            old_max = int(self.keys[-1].item()) if self.keys.numel() else 0
+        else:                                   # dense ranks so far: their IDs are 0..n-1
+            old = torch.arange(self.num_nodes, dtype=torch.int64, device="cuda")
+            old_max = self.num_nodes - 1
+        allk = torch.cat([old, new])
+        n = int(allk.numel())
+        key_bits = max(old_max, int(flat.max()) if flat.size else 0).bit_length()
+        ws = torch.empty(int(lib.bgl_hash_unique_workspace(n)), dtype=torch.uint8, device="cuda")
+        uniq = torch.empty(n, dtype=torch.int64, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        rank = torch.empty(n, dtype=torch.int32, device="cuda")
+        _lib.check(lib.bgl_hash_unique(allk.data_ptr(), n, key_bits, ws.data_ptr(), uniq.data_ptr(), cnt.data_ptr(),
+                                       rank.data_ptr(), st))
+        U = int(cnt.item())
+        _lib.check(lib.bgl_cache_remap(self.handle, rank.data_ptr(), max(U, 1), st))
+        self.num_nodes = max(self.num_nodes, U)
+        self.keys = uniq[:U].clone()
+        self.home = torch.empty(max(U, 1), dtype=torch.uint8, device="cuda")
+        _lib.check(lib.bgl_key_home(self.keys.data_ptr(), None, U, self.cfg.num_devices, self.home.data_ptr(), st))
+        _lib.check(lib.bgl_cache_set_home_map(self.handle, self.home.data_ptr()))
+        return rank[old.numel():], self.num_nodes
 
     def rows_ptr(self) -> int:
         return _lib.load().bgl_cache_rows(self.handle) or 0
@@ -106,6 +144,11 @@ class FifoCacheDevice:
         host_tail = np.zeros(1, dtype=np.int64)
         _lib.check(_lib.load().bgl_cache_export(self.handle, dev_slots.ctypes.data, dev_tails.ctypes.data,
                                                 host_slots.ctypes.data, host_tail.ctypes.data))
+        if self.keys is not None:               # dense ranks -> the sparse IDs
+            keys = self.keys.cpu().numpy()
+            for a in (dev_slots, host_slots):
+                m = a >= 0
+                a[m] = keys[a[m]]
         return dev_slots, dev_tails, host_slots, int(host_tail[0])
 
 
@@ -350,6 +393,15 @@ class _UniqueScratch:
         self.count = torch.zeros(1, dtype=torch.int64, device="cuda")
 
 
+# dense node-ID space of the direct-address index: beyond it (IDs >= 2^31, or
+# an ID space far larger than the trace) the rings run on hash-deduplicated ranks
+_DENSE_LIMIT = (1 << 31) - 1
+
+
+def _sparse_ids(num_nodes: int, total: int) -> bool:
+    return num_nodes > _DENSE_LIMIT or num_nodes > max(1 << 26, 16 * total)
+
+
 def simulate(trace, cfg: CacheConfig, g=None, batch_devices=None, state: CacheEngineState | None = None,
              record_outcomes: bool = False) -> CacheSimReport:
     """Replay an access trace through the two-level multi-device cache
@@ -375,10 +427,14 @@ def simulate(trace, cfg: CacheConfig, g=None, batch_devices=None, state: CacheEn
     if flat.size and flat.min() < 0:
         raise ValueError("node IDs must be >= 0")
     num_nodes = int(flat.max()) + 1 if flat.size else 1
+    sparse = (state is not None and state.engine.keys is not None) or _sparse_ids(num_nodes, flat.size)
     if state is None:
-        state = cold_state(cfg, num_nodes)
+        state = cold_state(cfg, 1 if sparse else num_nodes)
     eng = state.engine
     maxb = int(sizes.max()) if nb else 0
+    ids = None
+    if sparse and flat.size:
+        ids, num_nodes = eng.adopt_keys(flat)
     eng.reserve(num_nodes, maxb)
     counters = torch.zeros((max(nb, 1), 8), dtype=torch.int64, device="cuda")
     if nb == 0:
@@ -386,7 +442,8 @@ def simulate(trace, cfg: CacheConfig, g=None, batch_devices=None, state: CacheEn
 
     lib = _lib.load()
     st = _lib.stream_ptr()
-    ids = torch.from_numpy(flat.astype(np.int32)).cuda()
+    if ids is None:
+        ids = torch.from_numpy(flat.astype(np.int32)).cuda()
     offs = np.concatenate([[0], np.cumsum(sizes)])
     # device-side batch lengths (the ABI takes counts on the device)
     lens = torch.from_numpy(sizes).cuda()

@@ -41,6 +41,7 @@ struct bgl_cache {
     int32_t shard_index = 0;     // global shard of this handle (multi-GPU: rank)
     int32_t global_shards = 0;   // 0 = d (single process)
     int64_t* level_stats = nullptr;   // [d+1][2] insertions, evictions per level (_Level counters, cachesim.py:45-49)
+    const uint8_t* home_of = nullptr; // sparse IDs: shard of each dense rank (caller-owned); null = v % d
 };
 
 namespace bgl {
@@ -55,12 +56,13 @@ enum : uint8_t { kD = 0, kP = 1, kH = 2, kM = 3 };
 __global__ void lookup_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ n_dev, int32_t worker,
                               int32_t shard, int32_t d, int64_t C, const int32_t* __restrict__ slot_of,
                               const int32_t* __restrict__ hslot_of, uint8_t* __restrict__ codes,
-                              int64_t* __restrict__ src_row, int64_t* __restrict__ counters) {
+                              int64_t* __restrict__ src_row, int64_t* __restrict__ counters,
+                              const uint8_t* __restrict__ home_of) {
     const int64_t n = *n_dev;
     int64_t c[4] = {0, 0, 0, 0};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = ids[i];
-        const int32_t h = v % d;
+        const int32_t h = home_of ? (int32_t)home_of[v] : v % d;
         const int32_t s = slot_of[v];
         uint8_t code;
         int64_t src = -1;
@@ -94,11 +96,11 @@ __global__ void lookup_kernel(const int32_t* __restrict__ ids, const int64_t* __
 
 // level of a sorted id: shard (dev-missed) and whether it is a full miss
 __device__ __forceinline__ void classify(int32_t v, int32_t d, const int32_t* slot_of, const int32_t* hslot_of,
-                                         int* shard, bool* full) {
+                                         const uint8_t* home_of, int* shard, bool* full) {
     *shard = -1;
     *full = false;
     if (slot_of[v] < 0) {
-        *shard = v % d;
+        *shard = home_of ? (int)home_of[v] : v % d;
         *full = (hslot_of == nullptr) || (hslot_of[v] < 0);
     }
 }
@@ -106,7 +108,7 @@ __device__ __forceinline__ void classify(int32_t v, int32_t d, const int32_t* sl
 __global__ void __launch_bounds__(kCThreads)
 miss_count_kernel(const int32_t* __restrict__ sorted_ids, const int64_t* __restrict__ n_dev, int32_t d,
                   const int32_t* __restrict__ slot_of, const int32_t* __restrict__ hslot_of,
-                  int64_t* __restrict__ tile_counts) {
+                  int64_t* __restrict__ tile_counts, const uint8_t* __restrict__ home_of) {
     __shared__ int64_t s_cnt[kMaxLevels];
     const int64_t n = *n_dev;
     const int64_t tile = blockIdx.x;
@@ -118,7 +120,7 @@ miss_count_kernel(const int32_t* __restrict__ sorted_ids, const int64_t* __restr
             if (e < n) {
                 int sh;
                 bool full;
-                classify(sorted_ids[e], d, slot_of, hslot_of, &sh, &full);
+                classify(sorted_ids[e], d, slot_of, hslot_of, home_of, &sh, &full);
                 if (sh >= 0) atomicAdd((unsigned long long*)&s_cnt[sh], 1ull);
                 if (full) atomicAdd((unsigned long long*)&s_cnt[d], 1ull);
             }
@@ -149,7 +151,8 @@ __global__ void miss_scan_kernel(int64_t* __restrict__ tile_counts, int64_t ntil
 __global__ void __launch_bounds__(kCThreads)
 miss_scatter_kernel(const int32_t* __restrict__ sorted_ids, const int64_t* __restrict__ n_dev, int32_t d,
                     const int32_t* __restrict__ slot_of, const int32_t* __restrict__ hslot_of,
-                    const int64_t* __restrict__ tile_off, int32_t* __restrict__ lists, int64_t list_cap) {
+                    const int64_t* __restrict__ tile_off, int32_t* __restrict__ lists, int64_t list_cap,
+                    const uint8_t* __restrict__ home_of) {
     constexpr int NW = kCThreads / 32;
     __shared__ int32_t s_w[NW][kMaxLevels];
     __shared__ int64_t s_run[kMaxLevels];
@@ -164,7 +167,7 @@ miss_scatter_kernel(const int32_t* __restrict__ sorted_ids, const int64_t* __res
         int64_t e = tile * kCTile + r * kCThreads + threadIdx.x;
         int sh = -1;
         bool full = false;
-        if (e < n) classify(sorted_ids[e], d, slot_of, hslot_of, &sh, &full);
+        if (e < n) classify(sorted_ids[e], d, slot_of, hslot_of, home_of, &sh, &full);
         int my_rank_sh = 0, my_rank_h = 0;
         for (int y = 0; y < d; ++y) {
             unsigned m = __ballot_sync(0xffffffffu, sh == y);
@@ -710,17 +713,18 @@ int bgl_cache_lookup(bgl_cache_t c, const int32_t* ids, const int64_t* n_dev, in
     }
     if (max_n > 0) {
         lookup_kernel<<<grid_for(max_n, 256), 256, 0, st>>>(ids, n_dev, worker, c->shard_index, c->d, c->C, c->slot_of, c->hslot_of,
-                                                            codes, src_row, counters);
+                                                            codes, src_row, counters, c->home_of);
         BGL_TRY(launch_status("lookup_kernel"));
     }
     const int64_t ntiles = std::max<int64_t>(1, ceil_div(max_sorted, kCTile));
     miss_count_kernel<<<(unsigned)ntiles, kCThreads, 0, st>>>(sorted_ids, n_sorted_dev, c->d, c->slot_of,
-                                                              c->hslot_of, c->tile_counts);
+                                                              c->hslot_of, c->tile_counts, c->home_of);
     BGL_TRY(launch_status("miss_count_kernel"));
     miss_scan_kernel<<<1, kCThreads, 0, st>>>(c->tile_counts, ntiles, c->d, c->mcount);
     BGL_TRY(launch_status("miss_scan_kernel"));
     miss_scatter_kernel<<<(unsigned)ntiles, kCThreads, 0, st>>>(sorted_ids, n_sorted_dev, c->d, c->slot_of,
-                                                                c->hslot_of, c->tile_counts, c->lists, c->list_cap);
+                                                                c->hslot_of, c->tile_counts, c->lists, c->list_cap,
+                                                                c->home_of);
     return launch_status("miss_scatter_kernel");
 }
 
@@ -877,6 +881,65 @@ extern "C" int bgl_cache_warm(bgl_cache_t c, const int32_t* dev_nodes, const int
     if (n_host > 0) {
         warm_kernel<<<grid_for(n_host, 256), 256, 0, st>>>(host_nodes, n_host, c->hring, c->hslot_of);
         BGL_TRY(launch_status("warm_kernel"));
+    }
+    return BGL_OK;
+}
+
+// ---------------------------------------------------------------- sparse node IDs
+// Traces whose node IDs are sparse int64 run on dense ranks (bgl_hash_unique:
+// the rank order is the ID order, so every ascending insert list is the
+// reference's); the shard of a rank is then home_of[rank] = ID % d instead of
+// rank % d, and a growing key set remaps the rings' ranks and rebuilds the
+// index from them.
+namespace bgl {
+__global__ void remap_ring_kernel(int32_t* __restrict__ ring, int64_t len, const int32_t* __restrict__ old_to_new,
+                                  int32_t* __restrict__ index) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < len; s += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = ring[s];
+        if (v < 0) continue;
+        const int32_t w = old_to_new ? old_to_new[v] : v;
+        ring[s] = w;
+        index[w] = (int32_t)s;
+    }
+}
+}  // namespace bgl
+
+extern "C" int bgl_cache_set_home_map(bgl_cache_t c, const uint8_t* home_of) {
+    BGL_CHECK_ARG(c, "null cache");
+    BGL_CHECK_ARG(home_of == nullptr || c->d <= 255, "home map needs num_devices <= 255");
+    c->home_of = home_of;
+    return BGL_OK;
+}
+
+extern "C" int bgl_cache_remap(bgl_cache_t c, const int32_t* old_to_new, int64_t new_num_nodes, void* stream) {
+    BGL_CHECK_ARG(c, "null cache");
+    BGL_CHECK_ARG(new_num_nodes >= 1 && new_num_nodes < (1ll << 31), "num_nodes must be in [1, 2^31)");
+    cudaStream_t st = as_stream(stream);
+    if (new_num_nodes > c->n) {
+        BGL_TRY(cuda_status(cudaStreamSynchronize(st), "remap sync"));
+        int32_t* arrs[2] = {c->slot_of, c->hslot_of};
+        for (int a = 0; a < 2; ++a) {
+            if (!arrs[a]) continue;
+            cudaFree(arrs[a]);
+            arrs[a] = nullptr;
+            BGL_TRY(alloc_fill((void**)&arrs[a], new_num_nodes * 4, 0xFF, "cache index remap"));
+        }
+        c->slot_of = arrs[0];
+        c->hslot_of = arrs[1];
+        c->n = new_num_nodes;
+    } else {
+        BGL_TRY(cuda_status(cudaMemsetAsync(c->slot_of, 0xFF, c->n * 4, st), "remap reset"));
+        if (c->hslot_of) BGL_TRY(cuda_status(cudaMemsetAsync(c->hslot_of, 0xFF, c->n * 4, st), "remap reset"));
+    }
+    for (int y = 0; y < c->d; ++y) {
+        if (c->C == 0) break;
+        remap_ring_kernel<<<grid_for(c->C, 256), 256, 0, st>>>(c->rings + (int64_t)y * c->C, c->C, old_to_new,
+                                                               c->slot_of);
+        BGL_TRY(launch_status("remap_ring_kernel"));
+    }
+    if (c->Ch > 0) {
+        remap_ring_kernel<<<grid_for(c->Ch, 256), 256, 0, st>>>(c->hring, c->Ch, old_to_new, c->hslot_of);
+        BGL_TRY(launch_status("remap_ring_kernel"));
     }
     return BGL_OK;
 }

@@ -480,13 +480,77 @@ def make_c2_window(nbatches: int = 25, procs: int = 0):
     np.savez_compressed(os.path.join(HERE, "c2_window.npz"), **out)
 
 
+def make_sparse():
+    """Sparse / >= 2^31 int64 node IDs through gnnio's dict-based FIFO
+    (cachesim.py:81-107, 275-363): each case draws its universe from a
+    different ID range (just above 2^31, up to 2^40, up to 2^62, or dense IDs
+    spread by a large stride), replays it batch by batch with a persistent
+    state (every call grows the key set) and records codes, counters and the
+    rings after every batch, plus the whole-trace call's counters."""
+    rng = np.random.default_rng(7)
+    out = {}
+    specs, all_batches, all_codes, all_counters = [], [], [], []
+    dev_slots, dev_tails, host_slots, host_tails, whole = [], [], [], [], []
+    kinds = ["sorted", "unsorted", "dups"]
+    ranges = [("above31", 2**31, 2**31 + 5000), ("p40", 0, 2**40), ("p62", 0, 2**62), ("stride", 0, 0)]
+    for ci in range(16):
+        kind = kinds[ci % 3]
+        rname, lo, hi = ranges[ci % 4]
+        usize = int(rng.integers(8, 300))
+        if rname == "stride":
+            universe = np.arange(usize, dtype=np.int64) * int(rng.integers(2**27, 2**29)) + int(rng.integers(0, 7))
+        else:
+            universe = np.unique(rng.integers(lo, hi, size=usize, dtype=np.int64))
+        idx_batches = cache_case_batches(np.random.default_rng(1000 + ci), kind)
+        batches = [universe[np.asarray(b) % universe.size] for b in idx_batches]
+        if kind == "sorted":
+            batches = [np.unique(b) for b in batches]
+        d = int(rng.choice([1, 2, 3, 4, 8]))
+        cap = int(rng.integers(0, 65))
+        hcap = int(rng.choice([0, 1, 8, 64]))
+        use_bd = ci % 4 == 3
+        bd = [int(x) for x in rng.integers(d, size=len(batches))] if use_bd else None
+        cfg = cs.CacheConfig(device_capacity=cap, host_capacity=hcap, num_devices=d, policy="fifo",
+                             feature_bytes_per_node=512)
+        state = cs.cold_state(cfg)
+        for i, b in enumerate(batches):
+            rep = cs.simulate(AccessTrace(batches=[np.asarray(b, dtype=np.int64)]), cfg,
+                              batch_devices=[bd[i] if bd else i % d], state=state, record_outcomes=True)
+            all_codes.append(np.array(["DPHM".index(c) for c in rep.outcomes[0]], dtype=np.int64))
+            all_counters.append([rep.batch_queries[0], rep.batch_own_hits[0], rep.batch_peer_hits[0],
+                                 rep.batch_host_hits[0], rep.batch_misses[0], rep.batch_insertions[0],
+                                 rep.batch_evictions[0], rep.batch_metadata_updates[0]])
+            dev_slots.append(np.stack([lv.slots for lv in state.devices]).ravel())
+            dev_tails.append([lv.tail for lv in state.devices])
+            host_slots.append(state.host.slots.copy())
+            host_tails.append([state.host.tail])
+        rep = cs.simulate(AccessTrace(batches=[np.asarray(b, dtype=np.int64) for b in batches]), cfg,
+                          batch_devices=bd)
+        whole.append([sum(rep.batch_own_hits), sum(rep.batch_peer_hits), sum(rep.batch_host_hits),
+                      sum(rep.batch_misses), sum(rep.batch_insertions), sum(rep.batch_evictions)])
+        specs.append((d, cap, hcap, len(batches), int(use_bd), kinds.index(kind)))
+        all_batches.extend(batches)
+        out[f"bd_{ci}"] = np.array(bd if bd else [], dtype=np.int64)
+    out["specs"] = np.array(specs, dtype=np.int64)
+    out["whole"] = np.array(whole, dtype=np.int64)
+    put(out, "batches", all_batches)
+    put(out, "codes", all_codes, np.int8)
+    out["counters"] = np.array(all_counters, dtype=np.int64)
+    put(out, "dev_slots", dev_slots)
+    put(out, "dev_tails", dev_tails)
+    put(out, "host_slots", host_slots)
+    put(out, "host_tails", host_tails)
+    np.savez_compressed(os.path.join(HERE, "sparse.npz"), **out)
+
+
 if __name__ == "__main__":
     parts = sys.argv[1:] or ["sampler", "cache", "ordering", "static", "shuffle", "graphgen", "c1", "c2", "policies",
-                             "c2_window"]
+                             "c2_window", "sparse"]
     gs = graphs()
     makers = {"sampler": lambda: make_sampler(gs), "cache": make_cache, "ordering": lambda: make_ordering(gs),
               "static": lambda: make_static(gs), "shuffle": lambda: make_shuffle(gs), "graphgen": make_graphgen,
-              "c1": make_c1, "c2": make_c2, "policies": lambda: make_policies(gs), "c2_window": make_c2_window}
+              "c1": make_c1, "c2": make_c2, "policies": lambda: make_policies(gs), "c2_window": make_c2_window,
+              "sparse": make_sparse}
     for part in parts:
         makers[part]()
         f = part + ".npz"

@@ -131,6 +131,21 @@ def test_fifo_batched_oracle_matches_reference(golden):
             assert state[3] == htl[i]
 
 
+def test_fifo_sparse_ids_oracle_matches_reference(golden):
+    """Sparse / >= 2^31 int64 IDs (tests/golden/sparse.npz, gnnio's dict FIFO):
+    the sequential oracle restates them exactly, so the GPU tests can use it."""
+    npz = golden("sparse")
+    for d, cap, hcap, bd, batches, codes, cnt, dsl, dtl, hsl, htl, _ in _cache_cases(npz):
+        eng = co.FifoEngine(cap, hcap, d)
+        for i, b in enumerate(batches):
+            c, cd = eng.run([b], [bd[i] if bd else i % d])
+            assert np.array_equal(cd[0], codes[i])
+            assert np.array_equal(c[0], cnt[i][:7])
+            assert np.array_equal(np.concatenate([r.slots for r in eng.devices]) if cap else np.empty(0), dsl[i])
+            assert np.array_equal(eng.host.slots, hsl[i])
+    assert npz["batches__data"].max() >= 2**40 and npz["batches__data"].min() >= 0
+
+
 def test_fifo_real_trace(golden):
     npz = golden("cache")
     trace = get(npz, "real_trace")
