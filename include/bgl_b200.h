@@ -79,6 +79,11 @@ int bgl_pcg64_draws(const uint64_t* table, int64_t first, int64_t n, uint64_t* o
  * CTAs of the sampling kernels (grid-stride loops cover the rest), leaving
  * SMs to a concurrently running gather; 0 = fill the GPU. */
 size_t bgl_sample_hop_workspace(int64_t max_parents);
+/* Diagnostics (tools/seg_timeline.py): buf (device, zeroed by the caller)
+ * receives one {num_parents, run, smid, walk draws, t_claim, t_walk, t_post,
+ * t_end} record (8 u64, globaltimer ns) per run of the segmented walk,
+ * buf[0] = record count; NULL turns it off. */
+int bgl_debug_seg_trace(void* buf);
 int bgl_sample_hop(const int64_t* indptr, const int32_t* indices,
                    const int32_t* parents, const int64_t* num_parents_dev, int64_t max_parents,
                    int32_t fanout, const uint64_t* table, int64_t* draw_base,

@@ -30,6 +30,7 @@ PROTOTYPES = {
     "bgl_pcg64_tables": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp]),
     "bgl_pcg64_draws": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp]),
     "bgl_sample_hop_workspace": (c_sz, [c_i64]),
+    "bgl_debug_seg_trace": (ctypes.c_int, [c_vp]),
     "bgl_sample_hop": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                        c_i32, c_vp]),
     "bgl_sample_hop_counter_workspace": (c_sz, [c_i64]),

@@ -500,6 +500,31 @@ sample_cand_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
 // overflowed the list) is redone exactly with a warp top-k over all its draws.
 constexpr int kSegCap = 512;
 
+// Diagnostics (tools/seg_timeline.py, bgl_debug_seg_trace): when set, lane 0
+// of every run appends {n, r, smid, Wtot, t_claim, t_walk, t_post, t_end}
+// (globaltimer ns) -- the per-run timeline behind DESIGN.md's sampler notes.
+__device__ unsigned long long* g_seg_trace = nullptr;
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __noinline__ void seg_trace_record(unsigned long long* trace, int64_t n, int64_t r, int32_t Wtot,
+                                              uint64_t t_claim, uint64_t t_walk, uint64_t t_post) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    const unsigned long long slot = atomicAdd(trace, 1ull);
+    unsigned long long* rec = trace + 8 + 8 * slot;
+    rec[0] = (unsigned long long)n;
+    rec[1] = (unsigned long long)r;
+    rec[2] = sm;
+    rec[3] = (unsigned long long)Wtot;
+    rec[4] = t_claim;
+    rec[5] = t_walk;
+    rec[6] = t_post;
+    rec[7] = gtimer();
+}
+
 struct SegWarp {
     uint64_t cand[kSegCap];
     uint64_t thr[33];    // [32]: sentinel 0 (lanes past the run's draws never pass)
@@ -589,11 +614,14 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
     const PcgTable T{table};
     const U128 A32 = T.A(5), C32 = T.C(5);
     const int64_t D0 = draw_base[0];
+    unsigned long long* trace = g_seg_trace;
     while (true) {
         int64_t r = 0;
         if (lane == 0) r = (int64_t)atomicAdd(ss.ticket, 1u);
         r = __shfl_sync(FULL, r, 0);
         if (r >= nruns) break;
+        uint64_t t_claim = 0, t_walk = 0, t_post = 0;
+        if (trace) t_claim = gtimer();
         const int64_t q = r * run + lane;
         const bool valid = lane < run && q < n;
         const int32_t p = valid ? parents[q] : 0;
@@ -652,9 +680,11 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
         }
         __syncwarp();
         int L = 0;
+        if (trace) t_walk = gtimer();
         if (Wtot > 0) L = hm ? seg_walk<true>(sw, T, A32, C32, D0 + pre_d, Wtot, lane, lt, cap)
                              : seg_walk<false>(sw, T, A32, C32, D0 + pre_d, Wtot, lane, lt, cap);
         __syncwarp();
+        if (trace) t_post = gtimer();
         // each parent's candidates are one range of the (parent-ordered) list
         const int Ls = L < cap ? L : cap;
         int lo = 0, hi = Ls;                    // first index with cj >= lane
@@ -723,6 +753,7 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
             }
         }
         __syncwarp();
+        if (trace && lane == 0) seg_trace_record(trace, n, r, Wtot, t_claim, t_walk, t_post);
     }
 }
 
@@ -836,6 +867,13 @@ sample_heavy_kernel(const int64_t* __restrict__ indptr, const int32_t* __restric
 using namespace bgl;
 
 extern "C" {
+
+// Diagnostics only: route the segmented walk's per-run timeline into buf
+// (device; buf[0] = record count, records of 8 u64 from buf + 8); NULL = off.
+int bgl_debug_seg_trace(void* buf) {
+    unsigned long long* p = reinterpret_cast<unsigned long long*>(buf);
+    return cuda_status(cudaMemcpyToSymbol(g_seg_trace, &p, sizeof(p)), "bgl_debug_seg_trace");
+}
 
 size_t bgl_sample_hop_workspace(int64_t max_parents) {
     int64_t m = max_parents > 0 ? max_parents : 1;
