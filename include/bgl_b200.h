@@ -187,6 +187,23 @@ int bgl_cache_set_home_map(bgl_cache_t cache, const uint8_t* home_of);
 /* Rename every resident rank v to old_to_new[v] (NULL: keep) and rebuild the
  * indices for a node space of new_num_nodes (the key set grew: ranks move). */
 int bgl_cache_remap(bgl_cache_t cache, const int32_t* old_to_new, int64_t new_num_nodes, void* stream);
+/* LRU / LFU levels (gnnio LruLevel cachesim.py:110-133, LfuLevel :136-175),
+ * set once on a fresh handle without feature rows: policy 1 = LRU, 2 = LFU
+ * (0 = FIFO, the default). The batch's lookup is bgl_cache_lookup (codes
+ * required); bgl_cache_update_ordered then applies the batch to every level
+ * in closed form (ordered.cu): LRU hits move to the recency end in the
+ * order of their last hit, LFU hits add to the frequency; inserts of the
+ * ascending miss lists evict per the policy. counters[5..7] += insertions,
+ * evictions, metadata updates (cachesim.py:346-361). */
+int bgl_cache_set_policy(bgl_cache_t cache, int32_t policy);
+int bgl_cache_update_ordered(bgl_cache_t cache, const int32_t* ids, const int64_t* n_dev, int64_t max_n,
+                             const uint8_t* codes, const int32_t* sorted_ids, int64_t* counters, void* stream);
+/* Host copy of one level (level == num_shards: the host level): its residents
+ * in eviction order (LRU: least recent first; LFU: insertion-tick order),
+ * their LFU freq / tick (may be NULL), the level's tick counter and metadata
+ * updates (may be NULL). list_host holds the level's capacity. */
+int bgl_cache_export_ordered(bgl_cache_t cache, int32_t level, int64_t* list_host, int64_t* len_host,
+                             int64_t* freq_host, int64_t* tick_host, int64_t* level_tick_host, int64_t* md_host);
 /* Device pointers of the ring feature rows ([num_shards*shard_capacity][row_bytes]). */
 void* bgl_cache_rows(bgl_cache_t cache);
 /* Classify every query against the pre-batch state (cachesim.py:318-339):

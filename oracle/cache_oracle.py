@@ -201,3 +201,122 @@ def static_run(batches, dev_sets, host_set, num_devices, batch_devices=None):
         counters[i] = (len(batch), c[0], c[1], c[2], c[3], 0, 0)
         codes_all.append(codes)
     return counters, codes_all
+
+
+# -- LRU / LFU levels (cachesim.py:110-175): batch-parallel closed forms -------------
+#
+# Within a batch the residency is the pre-batch one (inserts come after the
+# batch, cachesim.py:341-344); hits only reorder (LRU move_to_end) or count
+# (LFU freq += 1). With the level kept as an ordered resident list `log`:
+#   LRU: log in recency order. S = [residents not hit] ++ [hit nodes by their
+#        LAST hit in the batch] ++ [inserts, ascending]; every insert evicts
+#        the front when full, so e = max(0, len0 + M - C) and the new log is
+#        S[e:] (a queue keeps its last C entries).
+#   LFU: log in insertion-tick order; eviction takes the min (freq, tick).
+#        Inserts have key (1, T + j): above every resident with freq 1 (older
+#        ticks) and below every resident with freq >= 2, so with A = the
+#        freq-1 residents (tick order) the evictions are the first e of
+#        A ++ inserts -- except when the level is full at the first insert and
+#        holds no freq-1 node: then the first eviction is the global min
+#        (freq, tick) resident and the next e - 1 are inserts.
+# Counters per level: insertions += M, evictions += e, metadata_updates +=
+# hits + M (C == 0: inserts are no-ops, :122, :156).
+
+class OrderedLevel:
+    """One LRU or LFU level as the batch-parallel engine keeps it."""
+
+    def __init__(self, policy: str, capacity: int):
+        self.policy = policy
+        self.capacity = int(capacity)
+        self.log: list[int] = []          # LRU: recency order; LFU: tick order
+        self.freq: dict[int, int] = {}    # LFU
+        self.tick_of: dict[int, int] = {}
+        self.tick = 0
+        self.insertions = self.evictions = self.metadata_updates = 0
+
+    def __contains__(self, node):
+        return node in self.freq if self.policy == "lfu" else node in self._set()
+
+    def _set(self):
+        return set(self.log)
+
+    def apply(self, hits_in_order: list[int], inserts_sorted: list[int]):
+        C = self.capacity
+        self.metadata_updates += len(hits_in_order)
+        M = len(inserts_sorted) if C > 0 else 0
+        len0 = len(self.log)
+        e = max(0, len0 + M - C) if C > 0 else 0
+        if self.policy == "lru":
+            last = {}
+            for i, v in enumerate(hits_in_order):
+                last[v] = i
+            hit_nodes = [v for v, _ in sorted(last.items(), key=lambda x: x[1])]
+            kept = [v for v in self.log if v not in last]
+            S = kept + hit_nodes + (list(inserts_sorted) if C > 0 else [])
+            self.log = S[e:]
+        else:
+            for v in hits_in_order:
+                self.freq[v] += 1
+            if C > 0 and M:
+                k0 = max(0, C - len0)
+                A = [v for v in self.log if self.freq[v] == 1]
+                X = list(inserts_sorted)
+                if e >= 1 and k0 == 0 and not A:
+                    victim = min(self.log, key=lambda v: (self.freq[v], self.tick_of[v]))
+                    gone = {victim} | set(X[:e - 1])
+                else:
+                    gone = set((A + X)[:e])
+                for j, x in enumerate(X):
+                    self.freq[x] = 1
+                    self.tick_of[x] = self.tick + 1 + j
+                self.tick += M
+                self.log = [v for v in self.log + X if v not in gone]
+                for v in gone:
+                    del self.freq[v]
+                    del self.tick_of[v]
+        self.insertions += M
+        self.evictions += e
+        self.metadata_updates += M
+
+
+def simulate_ordered(policy, batches, device_capacity, host_capacity, num_devices, batch_devices=None,
+                     state=None):
+    """LRU / LFU engine in the batch-parallel form above; same outputs as the
+    reference simulate (counters [nb, 8] incl. metadata updates, codes)."""
+    d = num_devices
+    if state is None:
+        state = ([OrderedLevel(policy, device_capacity) for _ in range(d)], OrderedLevel(policy, host_capacity))
+    devs, host = state
+    counters = np.zeros((len(batches), 8), dtype=np.int64)
+    codes_all = []
+    tot = lambda a: sum(getattr(lv, a) for lv in devs) + getattr(host, a)  # noqa: E731
+    for i, batch in enumerate(batches):
+        worker = batch_devices[i] if batch_devices is not None else i % d
+        b0 = (tot("insertions"), tot("evictions"), tot("metadata_updates"))
+        sets = [set(lv.log) for lv in devs]
+        hset = set(host.log)
+        codes = np.empty(len(batch), dtype=np.uint8)
+        dev_hits = [[] for _ in range(d)]
+        host_hits, dm, fm = [], set(), set()
+        for j, v in enumerate(batch):
+            v = int(v)
+            h = v % d
+            if v in sets[h]:
+                codes[j] = CODE_D if h == worker else CODE_P
+                dev_hits[h].append(v)
+            elif v in hset:
+                codes[j] = CODE_H
+                host_hits.append(v)
+                dm.add(v)
+            else:
+                codes[j] = CODE_M
+                dm.add(v)
+                fm.add(v)
+        for h in range(d):
+            devs[h].apply(dev_hits[h], sorted(x for x in dm if x % d == h))
+        host.apply(host_hits, sorted(fm))
+        c = np.bincount(codes, minlength=4)
+        b1 = (tot("insertions"), tot("evictions"), tot("metadata_updates"))
+        counters[i] = (len(batch), c[0], c[1], c[2], c[3], b1[0] - b0[0], b1[1] - b0[1], b1[2] - b0[2])
+        codes_all.append(codes)
+    return counters, codes_all, state

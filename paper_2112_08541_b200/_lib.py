@@ -56,6 +56,9 @@ PROTOTYPES = {
     "bgl_cache_set_shard": (ctypes.c_int, [c_vp, c_i32, c_i32]),
     "bgl_cache_set_home_map": (ctypes.c_int, [c_vp, c_vp]),
     "bgl_cache_remap": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp]),
+    "bgl_cache_set_policy": (ctypes.c_int, [c_vp, c_i32]),
+    "bgl_cache_update_ordered": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "bgl_cache_export_ordered": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "bgl_cache_lookup": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "bgl_cache_lookup_misses": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "bgl_cache_insert": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),

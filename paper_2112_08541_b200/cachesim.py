@@ -17,8 +17,12 @@ The static-degree policy -- the paper's comparison baseline (SURVEY.md §8f
 "next" #1) -- also runs on the device: `warm_static` selects each shard's
 top-degree nodes with a sort-free histogram + ascending compaction and fills
 the same rings, lookups use the same kernel and nothing is inserted.
-LRU/LFU are not BGL's path (the paper rejects them): they
-raise NotImplementedError -- there is no CPU fallback.
+LRU and LFU (the policies the paper compares against and rejects,
+PAPER.md:187,333; LruLevel / LfuLevel cachesim.py:110-175) run on the device
+too: the same lookup, then one closed-form update per level
+(`bgl_cache_update_ordered`, csrc/ordered.cu), bit-exact with the
+reference's sequential levels -- so `compare_policies` sweeps all of
+`POLICIES` on the GPU. There is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -32,6 +36,7 @@ from . import _lib
 
 POLICIES = ("static-degree", "fifo", "lru", "lfu")
 CODE_CHARS = "DPHM"
+_POLICY_CODE = {"fifo": 0, "lru": 1, "lfu": 2}
 
 
 @dataclass
@@ -128,6 +133,26 @@ class FifoCacheDevice:
     def rows_ptr(self) -> int:
         return _lib.load().bgl_cache_rows(self.handle) or 0
 
+    def ordered_level(self, level: int):
+        """LRU / LFU level `level` (d = the host level): residents in eviction
+        order, their LFU freq and tick, the level's tick counter."""
+        c = self.cfg
+        cap = c.host_capacity if level == c.num_devices else c.device_capacity
+        lst = np.zeros(max(cap, 1), dtype=np.int64)
+        fq = np.zeros(max(cap, 1), dtype=np.int64)
+        tk = np.zeros(max(cap, 1), dtype=np.int64)
+        ln = np.zeros(1, dtype=np.int64)
+        lt = np.zeros(1, dtype=np.int64)
+        md = np.zeros(1, dtype=np.int64)
+        _lib.check(_lib.load().bgl_cache_export_ordered(self.handle, level, lst.ctypes.data, ln.ctypes.data,
+                                                        fq.ctypes.data, tk.ctypes.data, lt.ctypes.data,
+                                                        md.ctypes.data))
+        n = int(ln[0])
+        lst, fq, tk = lst[:n], fq[:n], tk[:n]
+        if self.keys is not None:
+            lst = self.keys.cpu().numpy()[lst]
+        return lst, fq, tk, int(lt[0]), int(md[0])
+
     def level_stats(self) -> np.ndarray:
         """int64 [d+1, 2]: cumulative (insertions, evictions) per level, the
         host level last (_Level counters, cachesim.py:45-49)."""
@@ -198,8 +223,38 @@ class FifoLevelView:
     @property
     def metadata_updates(self) -> int:
         """_Level.metadata_updates (cachesim.py:49): FIFO and static levels
-        never update metadata (only LRU/LFU do, :118-131, :150-174)."""
-        return 0
+        never update metadata; LRU / LFU count every hit and insert
+        (:118-131, :150-174)."""
+        if self._state.policy not in ("lru", "lfu"):
+            return 0
+        return self._ordered()[4]
+
+    def _ordered(self):
+        y = self._state.cfg.num_devices if self._level < 0 else self._level
+        return self._state.engine.ordered_level(y)
+
+    @property
+    def entries(self):
+        """LruLevel.entries (cachesim.py:113): residents, least recent first."""
+        from collections import OrderedDict
+        return OrderedDict((int(v), None) for v in self._ordered()[0])
+
+    @property
+    def freq(self) -> dict[int, int]:
+        """LfuLevel.freq (cachesim.py:141)."""
+        lst, fq, _, _, _ = self._ordered()
+        return {int(v): int(f) for v, f in zip(lst, fq)}
+
+    @property
+    def tick_of(self) -> dict[int, int]:
+        """LfuLevel.tick_of (cachesim.py:142)."""
+        lst, _, tk, _, _ = self._ordered()
+        return {int(v): int(t) for v, t in zip(lst, tk)}
+
+    @property
+    def tick(self) -> int:
+        """LfuLevel.tick (cachesim.py:144): ticks handed out so far."""
+        return self._ordered()[3]
 
     @property
     def resident(self) -> frozenset:
@@ -213,9 +268,13 @@ class FifoLevelView:
         return {int(v): i for i, v in enumerate(s) if v >= 0}
 
     def __contains__(self, node) -> bool:
+        if self._state.policy in ("lru", "lfu"):
+            return bool(np.any(self._ordered()[0] == int(node)))
         return bool(np.any(self.slots == int(node)))
 
     def __len__(self) -> int:
+        if self._state.policy in ("lru", "lfu"):
+            return int(self._ordered()[0].size)
         return int(np.count_nonzero(self.slots >= 0))
 
 
@@ -241,9 +300,12 @@ def cold_state(cfg: CacheConfig, num_nodes: int = 1, row_bytes: int = 0) -> Cach
     """Empty caches (cachesim.py:197-203). The index grows on demand."""
     if cfg.policy == "static-degree":
         raise ValueError("static policy requires warm_static(g, cfg)")
-    if cfg.policy != "fifo":
+    if cfg.policy not in _POLICY_CODE:
         raise _not_on_device(cfg.policy)
-    return CacheEngineState(cfg=cfg, engine=FifoCacheDevice(cfg, num_nodes, row_bytes), policy="fifo")
+    eng = FifoCacheDevice(cfg, num_nodes, row_bytes)
+    if cfg.policy != "fifo":
+        _lib.check(_lib.load().bgl_cache_set_policy(eng.handle, _POLICY_CODE[cfg.policy]))
+    return CacheEngineState(cfg=cfg, engine=eng, policy=cfg.policy)
 
 
 def _top_degree(dg, num_shards: int, capacity: int, exclude: torch.Tensor | None):
@@ -416,8 +478,9 @@ def simulate(trace, cfg: CacheConfig, g=None, batch_devices=None, state: CacheEn
             raise ValueError("state/policy mismatch")
     elif state is not None and state.policy != cfg.policy:
         raise ValueError("state/policy mismatch")
-    if cfg.policy not in ("fifo", "static-degree"):
+    if cfg.policy not in POLICIES:
         raise _not_on_device(cfg.policy)
+    ordered = cfg.policy in ("lru", "lfu")
 
     batches = [np.asarray(b, dtype=np.int64).ravel() for b in trace.batches]
     nb = len(batches)
@@ -447,7 +510,7 @@ def simulate(trace, cfg: CacheConfig, g=None, batch_devices=None, state: CacheEn
     offs = np.concatenate([[0], np.cumsum(sizes)])
     # device-side batch lengths (the ABI takes counts on the device)
     lens = torch.from_numpy(sizes).cuda()
-    codes = torch.empty(max(flat.size, 1), dtype=torch.uint8, device="cuda") if record_outcomes else None
+    codes = torch.empty(max(flat.size, 1), dtype=torch.uint8, device="cuda") if record_outcomes or ordered else None
     scratch = _UniqueScratch(eng.num_nodes, maxb)
     seg_off = _lib.c_i64 * 1
     c_off = seg_off(0)
@@ -483,7 +546,10 @@ def simulate(trace, cfg: CacheConfig, g=None, batch_devices=None, state: CacheEn
         _lib.check(lib.bgl_cache_lookup(eng.handle, bptr, nptr, n, worker, sptr, scnt, n,
                                         None if codes is None else codes.data_ptr() + int(offs[i]),
                                         None, cptr, st))
-        if not static:                         # static levels never change (StaticLevel.insert, cachesim.py:74-75)
+        if ordered:                            # LRU / LFU: hits reorder / count, then the policy's inserts
+            _lib.check(lib.bgl_cache_update_ordered(eng.handle, bptr, nptr, n, codes.data_ptr() + int(offs[i]),
+                                                    sptr, cptr, st))
+        elif not static:                       # static levels never change (StaticLevel.insert, cachesim.py:74-75)
             _lib.check(lib.bgl_cache_insert(eng.handle, sptr, n, None, cptr, st))
         if unsorted[i]:
             _lib.check(lib.bgl_unique_reset(scratch.ws.data_ptr(), eng.num_nodes, scratch.uniq.data_ptr(),
@@ -507,10 +573,10 @@ def amortized_update_ops(report: CacheSimReport) -> dict[str, float]:
     }
 
 
-def compare_policies(g, trace, capacities, policies=("static-degree", "fifo"), num_devices: int = 1, host_capacity: int = 0,
+def compare_policies(g, trace, capacities, policies=POLICIES, num_devices: int = 1, host_capacity: int = 0,
                      feature_bytes_per_node: int = 512) -> list[dict]:
-    """Hit-ratio table over a (policy x capacity) sweep (cachesim.py:378-409).
-    The device runs the static-degree and FIFO cells (the default sweep)."""
+    """Hit-ratio table over a (policy x capacity) sweep (cachesim.py:378-409);
+    every cell runs on the device."""
     rows = []
     for policy in policies:
         for cap in capacities:

@@ -20,29 +20,9 @@
 #include <algorithm>
 #include <vector>
 
+#include "cache.cuh"
 #include "common.cuh"
 #include "scan.cuh"
-
-struct bgl_cache {
-    int64_t n = 0;          // node-ID space of the index
-    int32_t d = 1;
-    int64_t C = 0, Ch = 0, rb = 0;
-    int32_t* slot_of = nullptr;
-    int32_t* hslot_of = nullptr;
-    int32_t* rings = nullptr;
-    int32_t* hring = nullptr;
-    int64_t* tails = nullptr;     // [d+1]
-    int64_t* mcount = nullptr;    // [d+1] misses per level in the current batch
-    unsigned char* rows = nullptr;
-    int32_t* lists = nullptr;     // [(d+1)][list_cap] positions into sorted_ids
-    int64_t list_cap = 0;
-    int64_t* tile_counts = nullptr;   // [max_tiles][d+1] (exclusive offsets after scan)
-    int64_t max_tiles = 0;
-    int32_t shard_index = 0;     // global shard of this handle (multi-GPU: rank)
-    int32_t global_shards = 0;   // 0 = d (single process)
-    int64_t* level_stats = nullptr;   // [d+1][2] insertions, evictions per level (_Level counters, cachesim.py:45-49)
-    const uint8_t* home_of = nullptr; // sparse IDs: shard of each dense rank (caller-owned); null = v % d
-};
 
 namespace bgl {
 
@@ -51,7 +31,6 @@ constexpr int kCRounds = 4;
 constexpr int kCTile = kCThreads * kCRounds;
 constexpr int kMaxLevels = 65;   // d <= 64 plus the host level
 
-enum : uint8_t { kD = 0, kP = 1, kH = 2, kM = 3 };
 
 __global__ void lookup_kernel(const int32_t* __restrict__ ids, const int64_t* __restrict__ n_dev, int32_t worker,
                               int32_t shard, int32_t d, int64_t C, const int32_t* __restrict__ slot_of,
@@ -536,6 +515,15 @@ copy_rows_bulk_kernel(const int32_t* __restrict__ plan, const int64_t* __restric
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+int alloc_fill(void** p, size_t bytes, int byte, const char* what) {
+    if (bytes == 0) {
+        *p = nullptr;
+        return BGL_OK;
+    }
+    BGL_TRY(cuda_status(cudaMalloc(p, bytes), what));
+    return cuda_status(cudaMemset(*p, byte, bytes), what);
+}
+
 }  // namespace bgl
 
 using namespace bgl;
@@ -572,15 +560,6 @@ int launch_copy_rows(const bgl_cache* c, const int32_t* plan, const int64_t* pla
     return launch_status("copy_rows_kernel");
 }
 
-int alloc_fill(void** p, size_t bytes, int byte, const char* what) {
-    if (bytes == 0) {
-        *p = nullptr;
-        return BGL_OK;
-    }
-    BGL_TRY(cuda_status(cudaMalloc(p, bytes), what));
-    return cuda_status(cudaMemset(*p, byte, bytes), what);
-}
-
 void free_cache(bgl_cache* c) {
     cudaFree(c->slot_of);
     cudaFree(c->hslot_of);
@@ -592,6 +571,11 @@ void free_cache(bgl_cache* c) {
     cudaFree(c->lists);
     cudaFree(c->tile_counts);
     cudaFree(c->level_stats);
+    cudaFree(c->lastq);
+    cudaFree(c->freq);
+    cudaFree(c->tick);
+    cudaFree(c->level_tick);
+    cudaFree(c->md_stats);
 }
 
 }  // namespace
@@ -662,6 +646,7 @@ int bgl_cache_reserve_nodes(bgl_cache_t c, int64_t num_nodes, void* stream) {
     }
     c->slot_of = arrs[0];
     c->hslot_of = arrs[1];
+    BGL_TRY(bgl_cache_ordered_resize(c, num_nodes, nullptr, st));
     c->n = num_nodes;
     return BGL_OK;
 }
@@ -915,6 +900,8 @@ extern "C" int bgl_cache_remap(bgl_cache_t c, const int32_t* old_to_new, int64_t
     BGL_CHECK_ARG(c, "null cache");
     BGL_CHECK_ARG(new_num_nodes >= 1 && new_num_nodes < (1ll << 31), "num_nodes must be in [1, 2^31)");
     cudaStream_t st = as_stream(stream);
+    // LRU / LFU per-node state follows its residents to their new ranks
+    BGL_TRY(bgl_cache_ordered_resize(c, std::max(new_num_nodes, c->n), old_to_new, st));
     if (new_num_nodes > c->n) {
         BGL_TRY(cuda_status(cudaStreamSynchronize(st), "remap sync"));
         int32_t* arrs[2] = {c->slot_of, c->hslot_of};

@@ -386,21 +386,23 @@ def make_c1():
 
 
 def make_policies(gs):
-    """compare_policies (cachesim.py:378-409) + amortized_update_ops
-    (:366-375) over the device-run policies on a sampled trace of the planted
+    """compare_policies (cachesim.py:378-409) with its default policy set
+    (POLICIES: static-degree, FIFO, LRU, LFU) + amortized_update_ops
+    (:366-375) for the dynamic policies, on a sampled trace of the planted
     graph, d = 2 devices with a host level."""
     g = gs["dense"]
     sched = od.proximity_schedule(g, 2, 128, seed=3)
     trace, _ = sp.simulate_epoch(g, random_partition(g, 1), sched, sp.SamplingConfig(fanouts=(5, 3), seed=2))
-    rows = cs.compare_policies(g, trace, [40, 150, 600], policies=("static-degree", "fifo"), num_devices=2,
-                               host_capacity=100)
-    amort = cs.amortized_update_ops(cs.simulate(trace, cs.CacheConfig(device_capacity=150, host_capacity=100,
-                                                                       num_devices=2)))
-    out = {"rows": np.array([[["static-degree", "fifo"].index(r["policy"]), r["capacity"], r["device_hits"],
+    rows = cs.compare_policies(g, trace, [40, 150, 600], num_devices=2, host_capacity=100)
+    amort = [cs.amortized_update_ops(cs.simulate(trace, cs.CacheConfig(device_capacity=150, host_capacity=100,
+                                                                        num_devices=2, policy=p)))
+             for p in ("fifo", "lru", "lfu")]
+    out = {"rows": np.array([[list(cs.POLICIES).index(r["policy"]), r["capacity"], r["device_hits"],
                               r["host_hits"], r["misses"]] for r in rows], dtype=np.int64),
            "hit_ratio": np.array([r["hit_ratio"] for r in rows], dtype=np.float64),
-           "amortized": np.array([amort[k] for k in ("lookups_per_batch", "insertions_per_batch",
-                                                     "evictions_per_batch", "metadata_updates_per_batch")])}
+           "amortized": np.array([[a[k] for k in ("lookups_per_batch", "insertions_per_batch",
+                                                  "evictions_per_batch", "metadata_updates_per_batch")]
+                                  for a in amort])}
     put(out, "trace", trace.batches, np.int32)
     np.savez_compressed(os.path.join(HERE, "policies.npz"), **out)
 
@@ -543,14 +545,84 @@ def make_sparse():
     np.savez_compressed(os.path.join(HERE, "sparse.npz"), **out)
 
 
+def make_ordered():
+    """gnnio's LRU and LFU levels (cachesim.py:110-175) through simulate
+    (cachesim.py:275-363), batch by batch on a persistent state: counters,
+    codes, and every level after every batch -- LRU: `entries` in recency
+    order; LFU: the residents in tick order with their `freq`, `tick_of` and
+    the level's `tick`. Plus whole-trace counters of the desk-scale sampler
+    trace for d = 1, 2, 4."""
+    rng = np.random.default_rng(11)
+    out = {}
+    specs, all_batches, all_codes, all_counters = [], [], [], []
+    logs, freqs, ticks, level_ticks = [], [], [], []
+    kinds = ["sorted", "unsorted", "dups"]
+    for ci in range(48):
+        policy = ("lru", "lfu")[ci % 2]
+        kind = kinds[(ci // 2) % 3]
+        batches = cache_case_batches(rng, kind)
+        d = int(rng.choice([1, 2, 3, 4, 8]))
+        cap = int(rng.integers(0, 40))
+        hcap = int(rng.choice([0, 1, 8, 30]))
+        use_bd = ci % 5 == 4
+        bd = [int(x) for x in rng.integers(d, size=len(batches))] if use_bd else None
+        cfg = cs.CacheConfig(device_capacity=cap, host_capacity=hcap, num_devices=d, policy=policy,
+                             feature_bytes_per_node=512)
+        state = cs.cold_state(cfg)
+        for i, b in enumerate(batches):
+            rep = cs.simulate(AccessTrace(batches=[np.asarray(b, dtype=np.int64)]), cfg,
+                              batch_devices=[bd[i] if bd else i % d], state=state, record_outcomes=True)
+            all_codes.append(np.array(["DPHM".index(c) for c in rep.outcomes[0]], dtype=np.int64))
+            all_counters.append([rep.batch_queries[0], rep.batch_own_hits[0], rep.batch_peer_hits[0],
+                                 rep.batch_host_hits[0], rep.batch_misses[0], rep.batch_insertions[0],
+                                 rep.batch_evictions[0], rep.batch_metadata_updates[0]])
+            for lv in list(state.devices) + [state.host]:
+                if policy == "lru":
+                    logs.append(np.array(list(lv.entries.keys()), dtype=np.int64))
+                    freqs.append(np.zeros(0, dtype=np.int64))
+                    ticks.append(np.zeros(0, dtype=np.int64))
+                    level_ticks.append(0)
+                else:
+                    order = sorted(lv.freq, key=lambda v: lv.tick_of[v])
+                    logs.append(np.array(order, dtype=np.int64))
+                    freqs.append(np.array([lv.freq[v] for v in order], dtype=np.int64))
+                    ticks.append(np.array([lv.tick_of[v] for v in order], dtype=np.int64))
+                    level_ticks.append(lv.tick)
+        specs.append((d, cap, hcap, len(batches), int(use_bd), kinds.index(kind), ci % 2))
+        all_batches.extend(batches)
+        out[f"bd_{ci}"] = np.array(bd if bd else [], dtype=np.int64)
+    out["specs"] = np.array(specs, dtype=np.int64)
+    put(out, "batches", all_batches)
+    put(out, "codes", all_codes, np.int8)
+    out["counters"] = np.array(all_counters, dtype=np.int64)
+    put(out, "logs", logs)
+    put(out, "freqs", freqs)
+    put(out, "ticks", ticks)
+    out["level_ticks"] = np.array(level_ticks, dtype=np.int64)
+    g = generate_power_law(5000, 10, seed=1, train_fraction=0.1, num_labels=16)
+    sched = od.proximity_schedule(g, 4, 100, seed=1)
+    trace, _ = sp.simulate_epoch(g, random_partition(g, 1, seed=0), sched,
+                                 sp.SamplingConfig(fanouts=(10, 5), seed=1))
+    put(out, "real_trace", trace.batches)
+    real = []
+    for policy in ("lru", "lfu"):
+        for d in (1, 2, 4):
+            rep = cs.simulate(trace, cs.CacheConfig(device_capacity=500 // d, host_capacity=250,
+                                                    num_devices=d, policy=policy))
+            real.append([rep.batch_queries, rep.batch_own_hits, rep.batch_peer_hits, rep.batch_host_hits,
+                         rep.batch_misses, rep.batch_insertions, rep.batch_evictions, rep.batch_metadata_updates])
+    out["real_counters"] = np.array(real, dtype=np.int64)   # [2 policies x 3 d, 8, nb]
+    np.savez_compressed(os.path.join(HERE, "ordered.npz"), **out)
+
+
 if __name__ == "__main__":
     parts = sys.argv[1:] or ["sampler", "cache", "ordering", "static", "shuffle", "graphgen", "c1", "c2", "policies",
-                             "c2_window", "sparse"]
+                             "c2_window", "sparse", "ordered"]
     gs = graphs()
     makers = {"sampler": lambda: make_sampler(gs), "cache": make_cache, "ordering": lambda: make_ordering(gs),
               "static": lambda: make_static(gs), "shuffle": lambda: make_shuffle(gs), "graphgen": make_graphgen,
               "c1": make_c1, "c2": make_c2, "policies": lambda: make_policies(gs), "c2_window": make_c2_window,
-              "sparse": make_sparse}
+              "sparse": make_sparse, "ordered": make_ordered}
     for part in parts:
         makers[part]()
         f = part + ".npz"

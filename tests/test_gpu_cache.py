@@ -96,8 +96,9 @@ def test_reference_hand_cases():
         st = cs.cold_state(cs.CacheConfig(device_capacity=2))
         st.policy = "lru"
         cs.simulate(tr([0]), cs.CacheConfig(device_capacity=2), state=st)
-    with pytest.raises(NotImplementedError):
-        cs.simulate(tr([0]), cs.CacheConfig(device_capacity=2, policy="lru"))
+    # LRU / LFU run on the device too (tests/test_gpu_ordered.py); FeatureCacheEngine stays FIFO
+    rep = cs.simulate(tr([0], [0]), cs.CacheConfig(device_capacity=2, policy="lru"), record_outcomes=True)
+    assert rep.outcomes == [["M"], ["D"]] and rep.batch_metadata_updates == [1, 1]
 
 
 @pytest.mark.parametrize("where", ["host", "hbm"])
@@ -256,9 +257,10 @@ def test_span_gather_matches_rows(dim, where):
 
 
 def test_compare_policies_and_amortized_ops_match_reference(golden):
-    """compare_policies over the device-run policies (static-degree, FIFO) and
-    amortized_update_ops equal the reference's on a sampled trace
-    (tests/golden/policies.npz; cachesim.py:366-409)."""
+    """compare_policies with the reference's default policy set (POLICIES:
+    static-degree, FIFO, LRU, LFU -- every cell on the device) and
+    amortized_update_ops of the dynamic policies equal the reference's on a
+    sampled trace (tests/golden/policies.npz; cachesim.py:366-409)."""
     from paper_2112_08541_b200 import cachesim as cs
     from paper_2112_08541_b200.sampler import AccessTrace
     from conftest import golden_graph
@@ -270,16 +272,16 @@ def test_compare_policies_and_amortized_ops_match_reference(golden):
         row_offsets, col_indices, num_nodes, train_mask = off, col, len(off) - 1, train
 
     trace = AccessTrace(batches=[b.astype(np.int64) for b in get(npz, "trace")])
-    rows = cs.compare_policies(Gr(), trace, [40, 150, 600], policies=("static-degree", "fifo"), num_devices=2,
-                               host_capacity=100)
-    got = np.array([[["static-degree", "fifo"].index(r["policy"]), r["capacity"], r["device_hits"], r["host_hits"],
+    rows = cs.compare_policies(Gr(), trace, [40, 150, 600], num_devices=2, host_capacity=100)
+    got = np.array([[list(cs.POLICIES).index(r["policy"]), r["capacity"], r["device_hits"], r["host_hits"],
                      r["misses"]] for r in rows])
     assert np.array_equal(got, npz["rows"])
     assert [r["hit_ratio"] for r in rows] == npz["hit_ratio"].tolist()
-    amort = cs.amortized_update_ops(cs.simulate(trace, cs.CacheConfig(device_capacity=150, host_capacity=100,
-                                                                      num_devices=2)))
-    assert [amort[k] for k in ("lookups_per_batch", "insertions_per_batch", "evictions_per_batch",
-                               "metadata_updates_per_batch")] == npz["amortized"].tolist()
+    for j, p in enumerate(("fifo", "lru", "lfu")):
+        amort = cs.amortized_update_ops(cs.simulate(trace, cs.CacheConfig(device_capacity=150, host_capacity=100,
+                                                                          num_devices=2, policy=p)))
+        assert [amort[k] for k in ("lookups_per_batch", "insertions_per_batch", "evictions_per_batch",
+                                   "metadata_updates_per_batch")] == npz["amortized"][j].tolist(), p
 
 
 @pytest.mark.parametrize("d,cap,hcap", [(1, 40, 0), (3, 17, 8), (4, 0, 16), (2, 64, 64)])

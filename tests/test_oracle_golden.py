@@ -146,6 +146,48 @@ def test_fifo_sparse_ids_oracle_matches_reference(golden):
     assert npz["batches__data"].max() >= 2**40 and npz["batches__data"].min() >= 0
 
 
+def _ordered_cases(npz):
+    specs = npz["specs"]
+    batches = get(npz, "batches")
+    codes = get(npz, "codes")
+    logs, freqs, ticks = get(npz, "logs"), get(npz, "freqs"), get(npz, "ticks")
+    lticks = npz["level_ticks"]
+    cnt = npz["counters"]
+    b0 = l0 = 0
+    for ci, (d, cap, hcap, nb, use_bd, kind, pol) in enumerate(specs):
+        bd = npz[f"bd_{ci}"].tolist() if use_bd else None
+        nl = nb * (d + 1)
+        yield (("lru", "lfu")[pol], int(d), int(cap), int(hcap), bd, batches[b0:b0 + nb], codes[b0:b0 + nb],
+               cnt[b0:b0 + nb], logs[l0:l0 + nl], freqs[l0:l0 + nl], ticks[l0:l0 + nl], lticks[l0:l0 + nl])
+        b0 += nb
+        l0 += nl
+
+
+def test_lru_lfu_batched_oracle_matches_reference(golden):
+    """The batch-parallel LRU / LFU closed forms (oracle/cache_oracle.py
+    OrderedLevel, what the CUDA update implements) against gnnio's
+    sequential levels (tests/golden/ordered.npz): counters incl. metadata
+    updates, codes, and every level's order / freq / ticks after every batch."""
+    npz = golden("ordered")
+    for policy, d, cap, hcap, bd, batches, codes, cnt, logs, freqs, ticks, lticks in _ordered_cases(npz):
+        state = None
+        for i, b in enumerate(batches):
+            c, cd, state = co.simulate_ordered(policy, [b], cap, hcap, d, [bd[i] if bd else i % d], state=state)
+            assert np.array_equal(cd[0], codes[i])
+            assert np.array_equal(c[0], cnt[i])
+            for y, lv in enumerate(list(state[0]) + [state[1]]):
+                k = i * (d + 1) + y
+                assert lv.log == logs[k].tolist(), (policy, i, y)
+                if policy == "lfu":
+                    assert [lv.freq[v] for v in lv.log] == freqs[k].tolist()
+                    assert [lv.tick_of[v] for v in lv.log] == ticks[k].tolist()
+                    assert lv.tick == lticks[k]
+    real = get(npz, "real_trace")
+    for j, (policy, d) in enumerate([(p, d) for p in ("lru", "lfu") for d in (1, 2, 4)]):
+        c, _, _ = co.simulate_ordered(policy, real, 500 // d, 250, d)
+        assert np.array_equal(c.T, npz["real_counters"][j])
+
+
 def test_fifo_real_trace(golden):
     npz = golden("cache")
     trace = get(npz, "real_trace")
