@@ -458,6 +458,9 @@ def dropin_e2e(args, cfg, dg, feats, order_host, max_uniq):
         qbytes += ids.size * 4
     codes_last = codes.cpu()                  # the step's result back on the host
     t2 = time.perf_counter()
+    simulate(AccessTrace(batches=trace.batches[:2]), ccfg)     # warm: first-call allocations outside the timing
+    torch.cuda.synchronize()
+    t2s = time.perf_counter()
     rep = simulate(trace, ccfg)
     t3 = time.perf_counter()
     assert rep.total_queries == sum(x.size for x in trace.batches)
@@ -466,7 +469,7 @@ def dropin_e2e(args, cfg, dg, feats, order_host, max_uniq):
                    "rows F[batch] in HBM, codes D2H at the end); wall clock, host-synchronous gnnio-style calls",
             "simulate_epoch_ms_per_batch": round(1e3 * (t1 - t0) / nb, 3),
             "retrieve_ms_per_batch": round(1e3 * (t2 - t1) / nb, 3),
-            "simulate_ms_per_batch": round(1e3 * (t3 - t2) / nb, 3),
+            "simulate_ms_per_batch": round(1e3 * (t3 - t2s) / nb, 3),   # cachesim.simulate over the trace (FIFO)
             "h2d_bytes_per_step": int(qbytes / nb + b * 8),
             "d2h_bytes_per_step": int(qbytes * 2 / nb + codes_last.numel() / nb)}
 
