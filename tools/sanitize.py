@@ -2,7 +2,9 @@
     compute-sanitizer --tool memcheck|racecheck|synccheck python tools/sanitize.py
 sampler (replay + counter), dedup/relabel, FIFO lookup/insert (pipeline,
 eager steps, host + HBM features, span and per-row miss gathers), static warm,
-BFS ordering + interleave, shuffling TV, partition/scatter, native generator."""
+BFS ordering + interleave, shuffling TV, partition/scatter, native generator;
+round 2: sparse-ID hash dedup + ring remap, LRU / LFU updates (every level
+kind, sparse IDs), the sampler timeline trace."""
 import os
 import sys
 
@@ -49,5 +51,22 @@ ops = GpuShardOps(4, 2000, 128)
 ids = torch.unique(torch.randint(0, 6000, (1500,), device="cuda")).to(torch.int32)
 part, pos, counts = ops.partition(ids)
 ops.scatter(pos, torch.zeros((len(ids), 32), device="cuda"), torch.zeros((len(ids), 32), device="cuda"))
+# round 2: sparse int64 IDs (hash dedup, home map, remap) on FIFO / LRU / LFU, static; the timeline trace
+from paper_2112_08541_b200.sampler import AccessTrace  # noqa: E402
+rng = np.random.default_rng(4)
+universe = np.unique(rng.integers(2**33, 2**40, size=300))
+for policy in ("fifo", "lru", "lfu"):
+    cfg = CacheConfig(device_capacity=40, host_capacity=25, num_devices=3, policy=policy)
+    st = bgl.cachesim.cold_state(cfg)
+    for k in range(3):
+        part = [rng.choice(universe[: 100 * (k + 1)], size=70) for _ in range(3)]
+        bgl.simulate(AccessTrace(batches=part), cfg, state=st, record_outcomes=True)
+    bgl.simulate(trace, CacheConfig(device_capacity=200, host_capacity=60, num_devices=2, policy=policy))
+from paper_2112_08541_b200 import _lib  # noqa: E402
+buf = torch.zeros(8 + 8 * 4096, dtype=torch.int64, device="cuda")
+_lib.check(_lib.load().bgl_debug_seg_trace(buf.data_ptr()))
+bgl.sample_batch(g_hub, seeds_hub, bgl.SamplingConfig(fanouts=(5, 5), seed=9), batch_seed=4)
+torch.cuda.synchronize()
+_lib.check(_lib.load().bgl_debug_seg_trace(None))
 torch.cuda.synchronize()
 print("sanitize driver done")
