@@ -12,7 +12,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libbgl_b200.so")
+# BGL_LIB_PATH: another build of the same ABI (A/B timing of two builds, tools/hop_bench.py)
+LIB_PATH = os.environ.get("BGL_LIB_PATH") or os.path.join(_HERE, "_lib", "libbgl_b200.so")
 
 PCG_TABLE_ROWS = 241   # BGL_PCG_TABLE_ROWS (include/bgl_b200.h)
 BGL_OK, BGL_EINVAL, BGL_ECUDA, BGL_ENOMEM, BGL_EUNSUPPORTED = 0, 1, 2, 3, 4

@@ -37,6 +37,14 @@
 #include "pcg64.cuh"
 #include "scan.cuh"
 
+#include <cub/block/block_radix_sort.cuh>
+
+// Build-time A/B switch of the segmented walk's candidate append (tools/ab:
+// a separate build; branch-free measured faster: hop 3 at C2 106.5 vs 108.7 us)
+#ifndef BGL_APPEND_BRANCHFREE
+#define BGL_APPEND_BRANCHFREE 1
+#endif
+
 namespace bgl {
 
 constexpr int64_t kNarrowMaxDeg = 2048;   // t fits 11 bits next to the 53-bit draw
@@ -68,6 +76,18 @@ static HopWorkspace carve_hop_ws(void* ws, int64_t max_parents) {
     p += align256(scan_state_bytes(2, w.max_tiles));
     w.heavy_count = reinterpret_cast<int64_t*>(p);   // zeroed with the scan state (contiguous)
     return w;
+}
+
+// Slice-path workspace, after the HopWorkspace: [prep scan state (4 values) |
+// heavy count | HopMeta] (one memset per hop), then the light-parent arrays.
+static int64_t prep_tiles(int64_t m) { return ceil_div(m > 0 ? m : 1, 2048); }
+static size_t hop_ws_bytes(int64_t m) { return align256(m * 8) * 2 + align256(m * 4) + align256(scan_state_bytes(2, m)) + 256; }
+static size_t slice_reset_bytes(int64_t m) { return align256(scan_state_bytes(5, prep_tiles(m))) + 256; }
+static size_t light_list_bytes(int64_t m) { return align256(m * 4) * 3 + align256(m * 8) * 4; }
+static size_t slice_ws_bytes(int64_t m) {
+    // prep state | wide list | slice map | lane list | perm | tile bases | tile counts
+    return slice_reset_bytes(m) + 2 * light_list_bytes(m) + align256((8 * m + 2) * 4) + align256(m * 4) +
+           2 * align256(prep_tiles(m) * 4);
 }
 
 // fire-and-forget (RED.OR): no dependent load of the word before the atomic
@@ -527,17 +547,17 @@ __device__ __noinline__ void seg_trace_record(unsigned long long* trace, int64_t
 
 struct SegWarp {
     uint64_t cand[kSegCap];
-    uint64_t thr[33];    // [32]: sentinel 0 (lanes past the run's draws never pass)
+    uint32_t thr[33];    // high-word thresholds; [32]: sentinel 0 (lanes past the run's draws never pass)
     int64_t gap[33];
     int32_t wst[33];
     int32_t wend[33];    // [32]: sentinel INT_MAX (ends the parent search)
-    int32_t cst[32];
+    int32_t cst[33];     // seg_post: each parent's candidate range start; [32] = list length
     uint8_t cj[kSegCap];
 };
 
 // The lane's parent bound / threshold / walk start stay in registers and are
 // reloaded only when the lane crosses into the next parent.
-__device__ __forceinline__ void seg_take(SegWarp& sw, int w, int& j, int& nb, uint64_t& th, int& ws) {
+__device__ __forceinline__ void seg_take(SegWarp& sw, int w, int& j, int& nb, uint32_t& th, int& ws) {
     if (w >= nb) {
         do {
             ++j;
@@ -548,32 +568,33 @@ __device__ __forceinline__ void seg_take(SegWarp& sw, int w, int& j, int& nb, ui
     }
 }
 
-__device__ __forceinline__ void seg_append(SegWarp& sw, bool pass, uint64_t key, int j, int& L, unsigned lt,
-                                           int cap) {
-    const unsigned bm = __ballot_sync(0xffffffffu, pass);
-    if (pass) {
-        const int pos = L + __popc(bm & lt);
-        if (pos < cap) {
-            sw.cand[pos] = key;
-            sw.cj[pos] = (uint8_t)j;
-        }
-    }
-    L += __popc(bm);
+// High word of a candidate threshold: out < (thh << 32). Rounding T << 11 up
+// to a multiple of 2^32 keeps the candidate set a threshold set (every
+// non-candidate's m is strictly above every candidate's), so the selection
+// stays exact and the walk compares one 32-bit word per draw.
+__device__ __forceinline__ uint32_t thr_hi(uint64_t tm /* T, <= 2^53 */) {
+    if (tm >= (1ull << 53)) return 0xffffffffu;   // every draw but out_hi == 2^32 - 1 (the largest m)
+    const uint64_t t = tm << 11;
+    const uint64_t h = (t >> 32) + ((t & 0xffffffffull) != 0);
+    return h > 0xffffffffull ? 0xffffffffu : (uint32_t)h;
 }
 
 // Walk the run's light draws in chunks of 32; returns the candidate count.
+// Per chunk: the 128-bit affine step, the high word of XSL-RR, one 32-bit
+// compare, a ballot; the low word and the key are formed by passing lanes only.
+// The state of walk position w (parent j) is s0 advanced by d_run + gap_j + w + 1.
 template <bool kGaps>
-__device__ __forceinline__ int seg_walk(SegWarp& sw, const PcgTable T, U128 A32, U128 C32, int64_t d_run,
+__device__ __forceinline__ int seg_walk(SegWarp& sw, const PcgTable T, U128 A32, U128 C32, U128 s0, int64_t d_run,
                                         int32_t Wtot, int lane, unsigned lt, int cap) {
     int j = 0;
     while (lane >= sw.wend[j]) ++j;
     int nb = sw.wend[j], ws = sw.wst[j];
-    uint64_t th = sw.thr[j];
+    uint32_t th = sw.thr[j];
     int64_t g = kGaps ? sw.gap[j] : 0;
-    U128 s = T.at((uint64_t)(d_run + lane + g + 1));
+    U128 s = T.adv(s0, (uint64_t)(d_run + lane + g + 1));
     int L = 0;
-    for (int W = 0; W < Wtot; W += 32) {
-        const int w = W + lane;
+    const int wlim = Wtot + lane;
+    for (int w = lane; w < wlim; w += 32) {
         if (w >= nb) {
             seg_take(sw, w, j, nb, th, ws);
             if (kGaps) {
@@ -584,12 +605,120 @@ __device__ __forceinline__ int seg_walk(SegWarp& sw, const PcgTable T, U128 A32,
                 }
             }
         }
-        // out >> 11 < T  <=>  out < T << 11 (thr holds T << 11; see the sentinel note)
-        const uint64_t out = xsl_rr_fs(s);
-        seg_append(sw, out < th, (out & ~2047ull) | (uint64_t)(w - ws), j, L, lt, cap);
+        const uint32_t hh = (uint32_t)(s.hi >> 32);
+        const uint32_t xl = (uint32_t)s.lo ^ (uint32_t)s.hi, xh = (uint32_t)(s.lo >> 32) ^ hh;
+        const uint32_t rot = hh >> 26;
+        const uint32_t a = (rot & 32u) ? xl : xh, b = (rot & 32u) ? xh : xl;
+        const uint32_t out_hi = __funnelshift_r(a, b, rot);
+        const bool pass = out_hi < th;
+        const unsigned bm = __ballot_sync(0xffffffffu, pass);
+#if BGL_APPEND_BRANCHFREE
+        // every lane forms its key, passing lanes store it
+        const int pos = L + __popc(bm & lt);
+        const uint32_t out_lo = __funnelshift_r(b, a, rot);
+        const uint64_t key = ((uint64_t)out_hi << 32) | (uint64_t)((out_lo & ~2047u) | (uint32_t)(w - ws));
+        if (pass && pos < cap) {
+            sw.cand[pos] = key;
+            sw.cj[pos] = (uint8_t)j;
+        }
+#else
+        // the low word and the key are formed by passing lanes only
+        if (pass) {
+            const int pos = L + __popc(bm & lt);
+            if (pos < cap) {
+                const uint32_t out_lo = __funnelshift_r(b, a, rot);
+                sw.cand[pos] = ((uint64_t)out_hi << 32) | (uint64_t)((out_lo & ~2047u) | (uint32_t)(w - ws));
+                sw.cj[pos] = (uint8_t)j;
+            }
+        }
+#endif
+        L += __popc(bm);
         s = affine_mad(A32, C32, s);
     }
     return L;
+}
+
+// Ranking + output of one run/group after its walk (lane i = parent i):
+// each parent's candidates are one range of the (parent-ordered) list; the
+// k smallest are written at their rank. Parents with fewer than k candidates
+// (or whose range was cut by the list's end) take an exact warp top-k over
+// all their draws (first draw's state: s0 advanced by dpos + 1).
+__device__ __forceinline__ void seg_post(SegWarp& sw, int L, int cap, int lane, int k, int64_t off, int64_t ex_k,
+                                         bool light, int64_t deg, U128 s0, uint64_t dpos, int32_t pid,
+                                         const PcgTable T, U128 A32, U128 C32,
+                                         const int32_t* __restrict__ indices, int32_t* __restrict__ out_ids,
+                                         int32_t* __restrict__ out_pidx, uint32_t* __restrict__ bitmap) {
+    const unsigned FULL = 0xffffffffu;
+    const int Ls = L < cap ? L : cap;
+    int lo = 0, hi = Ls;                    // first index with cj >= lane
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((int)sw.cj[mid] < lane) lo = mid + 1; else hi = mid;
+    }
+    const int c_st = lo;
+    const int c_end = __shfl_down_sync(FULL, c_st, 1);
+    const int c_own = lane < 31 ? c_end - c_st : Ls - c_st;
+    // a range touching the list's end is incomplete when the list overflowed
+    const bool cut = L > cap && c_st + c_own >= Ls;
+    sw.cst[lane] = c_st;
+    if (lane == 0) sw.cst[32] = Ls;
+    const bool fb = light && (c_own < k || cut);
+    __syncwarp();
+    // rank each candidate over its parent's range, write the k smallest at their rank
+    for (int b0 = 0; b0 < Ls; b0 += 32) {
+        const int i = b0 + lane;
+        const bool has = i < Ls;
+        const uint64_t key = has ? sw.cand[i] : ~0ull;
+        const int j = has ? (int)sw.cj[i] : 0;
+        const int kj = __shfl_sync(FULL, k, j);
+        const int64_t offj = __shfl_sync(FULL, off, j);
+        const int64_t oij = __shfl_sync(FULL, ex_k, j);
+        const bool fbj = __shfl_sync(FULL, (int)fb, j) != 0;
+        const int32_t pj = __shfl_sync(FULL, pid, j);
+        if (has && !fbj) {
+            const int st = sw.cst[j], e = sw.cst[j + 1];
+            int rk = 0;
+            for (int x = st; x < e; ++x) rk += sw.cand[x] < key;
+            if (rk < kj) {
+                const int32_t v = indices[offj + (int64_t)(key & 2047u)];
+                if (out_ids) out_ids[oij + rk] = v;
+                if (out_pidx) out_pidx[oij + rk] = pj;
+                if (bitmap) mark_bit(bitmap, v);
+            }
+        }
+    }
+    // fallback: exact warp top-k over all of the parent's draws
+    unsigned fm = __ballot_sync(FULL, fb);
+    while (fm) {
+        const int i = __ffs(fm) - 1;
+        fm &= fm - 1;
+        const int64_t dg = __shfl_sync(FULL, deg, i);
+        const int ki = __shfl_sync(FULL, k, i);
+        U128 s = T.adv(s0, __shfl_sync(FULL, dpos, i) + (uint64_t)lane + 1);
+        uint64_t best = ~0ull, kth = ~0ull;
+        const int nc = (int)((dg + 31) >> 5);
+        for (int c = 0; c < nc; ++c) {
+            if (c > 0) s = affine(A32, C32, s);
+            const int t = (c << 5) + lane;
+            const uint64_t cand = t < dg ? ((draw_of_state(s) << 11) | (uint64_t)t) : ~0ull;
+            if (c == 0) {
+                best = warp_bitonic_sort(cand);
+                kth = shfl(best, ki - 1);
+            } else {
+                fold_chunk(best, kth, cand, ki);
+            }
+        }
+        const int64_t oi = __shfl_sync(FULL, ex_k, i);
+        const int64_t offi = __shfl_sync(FULL, off, i);
+        const int32_t pi = __shfl_sync(FULL, pid, i);
+        if (lane < ki) {
+            const int32_t v = indices[offi + key_t(best)];
+            if (out_ids) out_ids[oi + lane] = v;
+            if (out_pidx) out_pidx[oi + lane] = pi;
+            if (bitmap) mark_bit(bitmap, v);
+        }
+    }
+    __syncwarp();
 }
 
 // WPB warps per CTA, MINB CTAs per SM: (8, 4) = 32 resident warps per SM
@@ -666,12 +795,10 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
         sw.wst[lane] = incl_l - ldeg;
         sw.wend[lane] = incl_l;
         sw.gap[lane] = (incl_d - deg) - (int64_t)(incl_l - ldeg);
-        {   // T << 11; T = 2^53 ("every draw") -> 2^64 - 1, which drops only an
-            // m = 2^53 - 1 draw: the largest possible, so either k others remain
-            // or the parent takes the exact fallback (fewer than k candidates)
-            const uint64_t tm = light ? cand_threshold(k, deg, ma, mb) : 0;
-            sw.thr[lane] = tm >= (1ull << 53) ? ~0ull : tm << 11;
-        }
+        // T = 2^53 ("every draw") -> 2^32 - 1, which drops only draws with
+        // out_hi = 2^32 - 1: the largest m, so either k others remain or the
+        // parent takes the exact fallback (fewer than k candidates)
+        sw.thr[lane] = light ? thr_hi(cand_threshold(k, deg, ma, mb)) : 0u;
         if (lane == 0) {
             sw.wend[32] = 0x7fffffff;
             sw.thr[32] = 0;
@@ -681,79 +808,435 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
         __syncwarp();
         int L = 0;
         if (trace) t_walk = gtimer();
-        if (Wtot > 0) L = hm ? seg_walk<true>(sw, T, A32, C32, D0 + pre_d, Wtot, lane, lt, cap)
-                             : seg_walk<false>(sw, T, A32, C32, D0 + pre_d, Wtot, lane, lt, cap);
+        if (Wtot > 0) L = hm ? seg_walk<true>(sw, T, A32, C32, T.state(), D0 + pre_d, Wtot, lane, lt, cap)
+                             : seg_walk<false>(sw, T, A32, C32, T.state(), D0 + pre_d, Wtot, lane, lt, cap);
         __syncwarp();
         if (trace) t_post = gtimer();
-        // each parent's candidates are one range of the (parent-ordered) list
-        const int Ls = L < cap ? L : cap;
-        int lo = 0, hi = Ls;                    // first index with cj >= lane
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if ((int)sw.cj[mid] < lane) lo = mid + 1; else hi = mid;
-        }
-        const int c_st = lo;
-        const int c_end = __shfl_down_sync(FULL, c_st, 1);
-        const int c_own = lane < 31 ? c_end - c_st : Ls - c_st;
-        // a range touching the list's end is incomplete when the list overflowed
-        const bool cut = L > cap && c_st + c_own >= Ls;
-        sw.cst[lane] = c_st;
-        const bool fb = light && (c_own < (int)k || cut);
-        __syncwarp();
-        for (int b0 = 0; b0 < Ls; b0 += 32) {
-            const int i = b0 + lane;
-            const bool has = i < Ls;
-            const uint64_t key = has ? sw.cand[i] : ~0ull;
-            const int j = has ? (int)sw.cj[i] : 0;
-            const int kj = __shfl_sync(FULL, (int)k, j);
-            const int64_t offj = __shfl_sync(FULL, off, j);
-            const int64_t oij = __shfl_sync(FULL, ex_k, j);
-            const bool fbj = __shfl_sync(FULL, (int)fb, j) != 0;
-            const int e = __shfl_sync(FULL, c_st + c_own, j);
-            if (has && !fbj) {
-                const int st = sw.cst[j];
-                int rk = 0;
-                for (int x = st; x < e; ++x) rk += sw.cand[x] < key;
-                if (rk < kj) {
-                    const int32_t v = indices[offj + (int64_t)(key & 2047u)];
-                    if (out_ids) out_ids[oij + rk] = v;
-                    if (out_pidx) out_pidx[oij + rk] = (int32_t)(r * run + j);
-                    if (bitmap) mark_bit(bitmap, v);
-                }
-            }
-        }
-        // fallback: exact warp top-k over all of the parent's draws
-        unsigned fm = __ballot_sync(FULL, fb);
-        while (fm) {
-            const int i = __ffs(fm) - 1;
-            fm &= fm - 1;
-            const int64_t dg = __shfl_sync(FULL, deg, i);
-            const int ki = __shfl_sync(FULL, (int)k, i);
-            U128 s = T.at((uint64_t)(D0 + __shfl_sync(FULL, ex_d, i) + lane + 1));
-            uint64_t best = ~0ull, kth = ~0ull;
-            const int nc = (int)((dg + 31) >> 5);
-            for (int c = 0; c < nc; ++c) {
-                if (c > 0) s = affine(A32, C32, s);
-                const int t = (c << 5) + lane;
-                const uint64_t cand = t < dg ? ((draw_of_state(s) << 11) | (uint64_t)t) : ~0ull;
-                if (c == 0) {
-                    best = warp_bitonic_sort(cand);
-                    kth = shfl(best, ki - 1);
-                } else {
-                    fold_chunk(best, kth, cand, ki);
-                }
-            }
-            const int64_t oi = __shfl_sync(FULL, ex_k, i);
-            const int64_t offi = __shfl_sync(FULL, off, i);
-            if (lane < ki) {
-                const int32_t v = indices[offi + key_t(best)];
-                if (out_ids) out_ids[oi + lane] = v;
-                if (out_pidx) out_pidx[oi + lane] = (int32_t)(r * run + i);
-                if (bitmap) mark_bit(bitmap, v);
-            }
-        }
-        __syncwarp();
+        seg_post(sw, L, cap, lane, (int)k, off, ex_k, light, deg, T.state(), (uint64_t)(D0 + ex_d),
+                 (int32_t)(r * run + lane), T, A32, C32, indices, out_ids, out_pidx, bitmap);
         if (trace && lane == 0) seg_trace_record(trace, n, r, Wtot, t_claim, t_walk, t_post);
+    }
+}
+
+// ---------------------------------------------------------------- prep + slice walk (default)
+// Two launches per hop instead of the look-back inside the walk:
+//   sample_prep_kernel  one pass over the hop's parents (1024 per CTA tile,
+//       decoupled look-back over tiles, the four prefixes resolved by four
+//       warps at once): deg/k/light-draw/light-count prefixes; the light
+//       parents compacted in order with everything the walk needs (parent
+//       index, light-draw start, heavy-draw gap, col offset, output offset,
+//       deg|k, threshold); heavy parents listed for sample_heavy_kernel; the
+//       slice map sf[s] = first light parent starting at or after light draw
+//       s*S; the hop's base PCG64 state; the chained draw base and output
+//       count. No per-run look-back is left on the walk's critical path.
+//   sample_slice_kernel persistent warps claim slices of ~S light draws
+//       (whole parents, atomic ticket), so every warp does about the same
+//       number of draws and the tail is one slice, not one 32-parent run;
+//       each group of <= 32 parents of a slice is walked with seg_walk (state
+//       jumped from the hop's base, <= 7 affine maps) and finished by seg_post.
+constexpr int kPrepThreads = 1024;
+constexpr int kPrepWarps = kPrepThreads / 32;
+constexpr int kPrepPPT = 2;                         // parents per thread
+constexpr int kPrepTile = kPrepThreads * kPrepPPT;  // parents per CTA tile
+constexpr int kSliceMin = 256;            // smallest slice: bounds the slice map at 8 entries per parent
+
+struct HopMeta {
+    uint64_t s0_hi, s0_lo;   // state after D0 steps (the hop's base)
+    int64_t nlight;          // light parents
+    int64_t ltot;            // light draws
+    int64_t nslices;         // slices = ltot / S + 1
+    unsigned ticket;         // slice / group claims (zeroed with the prep scan state)
+    unsigned ntiles;         // prep tiles of this hop
+};
+
+struct LightParents {
+    int32_t* q;        // parent position in the hop's input
+    int64_t* lp;       // first light draw (prefix over light parents)
+    int64_t* gap;      // heavy parents' draws before it (full position = lp + gap)
+    int64_t* off;      // col offset (indptr[p])
+    int64_t* kpre;     // output offset
+    int32_t* dk;       // deg | k << 16 (light: deg <= 2048, k <= 32)
+    uint32_t* thr;     // candidate threshold, high word
+    int32_t* sf;       // [nslices + 1] slice -> first light parent
+    int32_t* perm;     // lane walk: light parents of each prep tile by descending degree
+    int32_t* tbase;    // lane walk: [tile] first light index of the tile
+    int32_t* tcount;   // lane walk: [tile] light parents in the tile
+};
+
+// Parents split four ways: zero-degree (no draws), heavy (deg > 2048 or
+// k > 32: sample_heavy_kernel), lane (deg <= dlane: one lane each, the
+// tile's lane parents ordered by descending degree) and wide (the rest:
+// slices of ~S draws). dlane = 0: every light parent is wide.
+constexpr int kPrepVals = 5;   // deg, k, wide draws, wide parents, lane parents
+
+__global__ void __launch_bounds__(kPrepThreads, 1)
+sample_prep_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ parents,
+                   const int64_t* __restrict__ num_parents_dev, int32_t fanout, const uint64_t* __restrict__ table,
+                   int64_t* __restrict__ draw_base, ScanState ss, int64_t* __restrict__ deg_prefix,
+                   int64_t* __restrict__ k_prefix, int32_t* __restrict__ heavy, int64_t* __restrict__ heavy_count,
+                   LightParents lpar, LightParents lpl, HopMeta* __restrict__ meta, int64_t* __restrict__ num_out,
+                   int64_t heavy_deg, float ma, float mb, int32_t S, int32_t dlane) {
+    using Sorter = cub::BlockRadixSort<uint16_t, kPrepThreads, kPrepPPT, int16_t>;
+    __shared__ typename Sorter::TempStorage s_sort;
+    __shared__ int64_t s_tile;
+    __shared__ int64_t s_warp[kPrepVals][kPrepWarps];
+    __shared__ int64_t s_pre[kPrepVals], s_tot[kPrepVals];
+    const int64_t n = *num_parents_dev;
+    const int64_t ntiles = n > 0 ? ceil_div(n, kPrepTile) : 1;
+    const int64_t tile = claim_tile(ss, &s_tile);
+    const int lane = lane_id(), wid = warp_id();
+    if (tile >= ntiles) {
+        // the first spare CTA (grid = max tiles + 1) computes the hop's base
+        // state beside the scan: the <= 16 jump rows loaded at once by 16
+        // lanes, then applied in order from registers via shuffles
+        if (tile == ntiles && wid == 0) {
+            const PcgTable T{table};
+            const uint64_t D0 = (uint64_t)draw_base[0];
+            const int dig = (int)((D0 >> (4 * (lane & 15))) & 15u);
+            U128 A{0, 0}, C{0, 0};
+            if (lane < 16 && dig) {
+                const uint64_t* r = T.row(lane, dig);
+                A = U128{__ldg(r + 0), __ldg(r + 1)};
+                C = U128{__ldg(r + 2), __ldg(r + 3)};
+            }
+            U128 st = T.state();
+            for (int i = 0; i < 16; ++i) {
+                const int di = __shfl_sync(0xffffffffu, dig, i);
+                const U128 Ai{__shfl_sync(0xffffffffu, A.hi, i), __shfl_sync(0xffffffffu, A.lo, i)};
+                const U128 Ci{__shfl_sync(0xffffffffu, C.hi, i), __shfl_sync(0xffffffffu, C.lo, i)};
+                if (di) st = affine(Ai, Ci, st);
+            }
+            if (lane == 0) {
+                meta->s0_hi = st.hi;
+                meta->s0_lo = st.lo;
+            }
+        }
+        return;
+    }
+    // thread t holds parents 2t, 2t+1 of the tile
+    int64_t qv[kPrepPPT], offv[kPrepPPT], degv[kPrepPPT], kv[kPrepPPT];
+    int cls[kPrepPPT];   // 0 none, 1 heavy, 2 wide, 3 lane
+    int64_t v[kPrepVals] = {0, 0, 0, 0, 0};
+#pragma unroll
+    for (int e = 0; e < kPrepPPT; ++e) {
+        const int64_t q = tile * kPrepTile + kPrepPPT * threadIdx.x + e;
+        const bool valid = q < n;
+        const int32_t p = valid ? parents[q] : 0;
+        const int64_t off = valid ? indptr[p] : 0;
+        const int64_t deg = valid ? indptr[p + 1] - off : 0;
+        const int64_t k = deg < fanout ? deg : fanout;
+        qv[e] = q;
+        offv[e] = off;
+        degv[e] = deg;
+        kv[e] = k;
+        cls[e] = !valid || deg == 0 ? 0 : (k > 32 || deg > heavy_deg) ? 1 : deg <= dlane ? 3 : 2;
+        v[0] += deg;
+        v[1] += k;
+        v[2] += cls[e] == 2 ? deg : 0;
+        v[3] += cls[e] == 2 ? 1 : 0;
+        v[4] += cls[e] == 3 ? 1 : 0;
+    }
+    int64_t incl[kPrepVals];
+#pragma unroll
+    for (int c = 0; c < kPrepVals; ++c) {
+        incl[c] = warp_incl_scan(v[c]);
+        if (lane == 31) s_warp[c][wid] = incl[c];
+    }
+    __syncthreads();
+    if (wid < kPrepVals) {   // warp c: exclusive prefix of the warp totals of value c, tile total
+        const int64_t x = s_warp[wid][lane];
+        const int64_t xi = warp_incl_scan(x);
+        s_warp[wid][lane] = xi - x;
+        if (lane == 31) s_tot[wid] = xi;
+    }
+    __syncthreads();
+    if (threadIdx.x < kPrepVals) {
+        const uint64_t w = (tile == 0 ? kFlagInc : kFlagAgg) | ((uint64_t)s_tot[threadIdx.x] & kValMask);
+        atomicExch((unsigned long long*)&ss.status[threadIdx.x * ss.max_tiles + tile], (unsigned long long)w);
+        if (tile == 0) s_pre[threadIdx.x] = 0;
+    }
+    __syncthreads();   // aggregates published before anyone reads
+    if (tile > 0 && wid < kPrepVals) {   // the prefixes at once: every predecessor's aggregate, read directly
+        const uint64_t* st = ss.status + wid * ss.max_tiles;
+        int64_t acc = 0;
+        for (int64_t j = lane; j < tile; j += 32) {
+            uint64_t w;
+            do { w = ld_volatile(st + j); } while ((w >> 62) == 0);
+            acc += (int64_t)(w & kValMask);
+        }
+        acc = warp_sum_i64(acc);
+        if (lane == 0) s_pre[wid] = acc;
+    }
+    __syncthreads();
+    int64_t ex[kPrepVals];
+#pragma unroll
+    for (int c = 0; c < kPrepVals; ++c) ex[c] = s_warp[c][wid] + incl[c] - v[c];   // tile-relative
+    if (dlane > 0) {   // the tile's lane parents by descending degree
+        uint16_t key[kPrepPPT];
+        int16_t val[kPrepPPT];
+        int64_t r = ex[4];
+#pragma unroll
+        for (int e = 0; e < kPrepPPT; ++e) {
+            key[e] = cls[e] == 3 ? (uint16_t)(kNarrowMaxDeg - degv[e]) : (uint16_t)4095;
+            val[e] = (int16_t)r;
+            r += cls[e] == 3 ? 1 : 0;
+        }
+        Sorter(s_sort).Sort(key, val, 0, 12);
+        const int64_t lb = s_pre[4], lc = s_tot[4];
+#pragma unroll
+        for (int e = 0; e < kPrepPPT; ++e) {
+            const int64_t pos = (int64_t)kPrepPPT * threadIdx.x + e;
+            if (pos < lc) lpl.perm[lb + pos] = (int32_t)(lb + val[e]);
+        }
+        if (threadIdx.x == 0) {
+            lpl.tbase[tile] = (int32_t)lb;
+            lpl.tcount[tile] = (int32_t)lc;
+        }
+    }
+    int64_t dpre = s_pre[0] + ex[0], kpre = s_pre[1] + ex[1], wpre = s_pre[2] + ex[2];
+    int64_t wi = s_pre[3] + ex[3], ni = s_pre[4] + ex[4];
+#pragma unroll
+    for (int e = 0; e < kPrepPPT; ++e) {
+        const int64_t q = qv[e], deg = degv[e], k = kv[e];
+        const bool hv = cls[e] == 1;
+        const unsigned hm = __ballot_sync(0xffffffffu, hv);
+        if (hm) {
+            int64_t slot = 0;
+            if (lane == 0) slot = (int64_t)atomicAdd((unsigned long long*)heavy_count, (unsigned long long)__popc(hm));
+            slot = __shfl_sync(0xffffffffu, slot, 0);
+            if (hv) {
+                heavy[slot + __popc(hm & ((1u << lane) - 1u))] = (int32_t)q;
+                deg_prefix[q] = dpre;
+                k_prefix[q] = kpre;
+            }
+        }
+        if (cls[e] >= 2) {
+            const bool wide = cls[e] == 2;
+            LightParents& L = wide ? lpar : lpl;
+            const int64_t i = wide ? wi : ni;
+            L.q[i] = (int32_t)q;
+            L.lp[i] = wide ? wpre : dpre;
+            L.gap[i] = wide ? dpre - wpre : 0;
+            L.off[i] = offv[e];
+            L.kpre[i] = kpre;
+            L.dk[i] = (int32_t)(deg | (k << 16));
+            L.thr[i] = thr_hi(cand_threshold(k, deg, ma, mb));
+            // slices whose start s*S lies in (wpre, wpre + deg] begin at the next wide parent
+            if (wide)
+                for (int64_t sl = wpre / S + 1; sl * S <= wpre + deg; ++sl) lpar.sf[sl] = (int32_t)(wi + 1);
+        }
+        dpre += deg;
+        kpre += k;
+        wpre += cls[e] == 2 ? deg : 0;
+        wi += cls[e] == 2 ? 1 : 0;
+        ni += cls[e] == 3 ? 1 : 0;
+    }
+    if (tile == ntiles - 1 && threadIdx.x == 0) {
+        const int64_t D0 = draw_base[0];
+        const int64_t ltot = s_pre[2] + s_tot[2], nl = s_pre[3] + s_tot[3];
+        const int64_t ns = ltot / S + 1;
+        draw_base[1] = D0 + s_pre[0] + s_tot[0];
+        *num_out = s_pre[1] + s_tot[1];
+        meta->nlight = nl;
+        meta->ltot = ltot;
+        meta->nslices = ns;
+        meta->ntiles = (unsigned)ntiles;
+        lpar.sf[0] = 0;
+        lpar.sf[ns] = (int32_t)nl;
+    }
+}
+
+// One slice of the wide list: groups of <= `group` parents walked with
+// seg_walk (state jumped from the hop's base) and finished by seg_post.
+// Per-group values that live across the walk are re-read after it (light
+// list / hop meta, L1/L2 hits) instead of being held in registers.
+__device__ __forceinline__ void slice_one(SegWarp& sw, int i0, int i1, const LightParents& lpar,
+                                          const HopMeta* meta, const PcgTable T, U128 A32, U128 C32,
+                                          const int32_t* __restrict__ indices, int32_t* __restrict__ out_ids,
+                                          int32_t* __restrict__ out_pidx, uint32_t* __restrict__ bitmap, int group,
+                                          int cap, int lane, unsigned lt) {
+    const unsigned FULL = 0xffffffffu;
+    for (int ib = i0; ib < i1; ib += group) {
+        const int ie = ib + group < i1 ? ib + group : i1;
+        int L, Wtot;
+        {
+            const int i = ib + lane;
+            const bool valid = lane < ie - ib;
+            const int64_t lp = valid ? lpar.lp[i] : 0;
+            const int64_t gap = valid ? lpar.gap[i] : 0;
+            const int deg = valid ? (lpar.dk[i] & 0xffff) : 0;
+            const int64_t LB = __shfl_sync(FULL, lp, 0);
+            const int64_t LE = ie < meta->nlight ? lpar.lp[ie] : meta->ltot;   // same address on every lane
+            Wtot = (int32_t)(LE - LB);
+            sw.wst[lane] = valid ? (int32_t)(lp - LB) : Wtot;
+            sw.wend[lane] = valid ? (int32_t)(lp - LB) + deg : Wtot;
+            const int64_t G0 = __shfl_sync(FULL, gap, 0);   // gaps relative to the group's first parent
+            sw.gap[lane] = valid ? gap - G0 : 0;
+            sw.thr[lane] = valid ? lpar.thr[i] : 0u;
+            if (lane == 0) {
+                sw.wend[32] = 0x7fffffff;
+                sw.thr[32] = 0;
+                sw.gap[32] = 0;
+                sw.wst[32] = 0;
+            }
+            const bool gaps = G0 != __shfl_sync(FULL, gap, ie - ib - 1);
+            const U128 s0{meta->s0_hi, meta->s0_lo};
+            __syncwarp();
+            L = gaps ? seg_walk<true>(sw, T, A32, C32, s0, LB + G0, Wtot, lane, lt, cap)
+                     : seg_walk<false>(sw, T, A32, C32, s0, LB + G0, Wtot, lane, lt, cap);
+        }
+        __syncwarp();
+        const int i = ib + lane;
+        const bool valid = lane < ie - ib;
+        const int dk = valid ? lpar.dk[i] : 0;
+        const int64_t dpos = valid ? lpar.lp[i] + lpar.gap[i] : 0;
+        const int64_t off = valid ? lpar.off[i] : 0;
+        const int64_t kpre = valid ? lpar.kpre[i] : 0;
+        const int32_t q = valid ? lpar.q[i] : 0;
+        const U128 s0{meta->s0_hi, meta->s0_lo};
+        seg_post(sw, L, cap, lane, dk >> 16, off, kpre, valid, dk & 0xffff, s0, (uint64_t)dpos, q, T, A32, C32,
+                 indices, out_ids, out_pidx, bitmap);
+    }
+}
+
+// ---------------------------------------------------------------- lane walk
+// One lane per low-degree parent (deg <= dlane): the lane replays its
+// parent's own draws with the 1-step map (no cross-lane hand-off), keeps
+// the draws below the parent's threshold in its own shared-memory column
+// (high word + position) and selects the k smallest by an in-place
+// selection sort over the column: no ballot, no cross-lane compaction, no
+// ranking against other lanes' candidates (47 SASS instructions per draw
+// against ~69 in the segmented walk). sample_prep_kernel orders each tile's
+// lane parents by descending degree, so a warp's lanes walk about as many
+// draws each, and dlane bounds the serial chain of one lane. Candidate-set
+// exactness as in the segmented walk (out < thh * 2^32 is a threshold
+// set). Parents with fewer than k candidates, a full column, or two
+// candidates with equal high words (their order needs the low word) take
+// the exact CTA kernel (sample_heavy_kernel) through the heavy list.
+constexpr int kLaneCap = 32;
+
+struct LaneCols {
+    uint32_t hi[kLaneCap][32];
+    uint16_t t[kLaneCap][32];
+};
+
+__device__ __forceinline__ void lane_one(LaneCols& cl, int g, const LightParents& lpl, const HopMeta* meta,
+                                         int ntiles, const PcgTable T, U128 A1, U128 C1,
+                                         const int32_t* __restrict__ indices, int64_t* __restrict__ deg_prefix,
+                                         int64_t* __restrict__ k_prefix, int32_t* __restrict__ heavy,
+                                         int64_t* __restrict__ heavy_count, int32_t* __restrict__ out_ids,
+                                         int32_t* __restrict__ out_pidx, uint32_t* __restrict__ bitmap, int capl,
+                                         int lane) {
+    const int tile = g % ntiles, grp = g / ntiles;
+    const int lc = lpl.tcount[tile];
+    if (32 * grp >= lc) return;
+    const int lb = lpl.tbase[tile];
+    const bool valid = 32 * grp + lane < lc;
+    const int li = valid ? lpl.perm[lb + 32 * grp + lane] : 0;
+    const int dk = valid ? lpl.dk[li] : 0;
+    const int deg = dk & 0xffff, k = dk >> 16;
+    const uint32_t th = valid ? lpl.thr[li] : 0u;
+    const int64_t dpos = valid ? lpl.lp[li] : 0;   // the lane list holds the full draw offset
+    U128 s = T.adv(U128{meta->s0_hi, meta->s0_lo}, (uint64_t)dpos + 1);
+    int c = 0;
+    for (int t = 0; t < deg; ++t) {
+        const uint32_t hh = (uint32_t)(s.hi >> 32);
+        const uint32_t xl = (uint32_t)s.lo ^ (uint32_t)s.hi, xh = (uint32_t)(s.lo >> 32) ^ hh;
+        const uint32_t rot = hh >> 26;
+        const uint32_t a = (rot & 32u) ? xl : xh, b = (rot & 32u) ? xh : xl;
+        const uint32_t out_hi = __funnelshift_r(a, b, rot);
+        if (out_hi < th) {
+            if (c < capl) {
+                cl.hi[c][lane] = out_hi;
+                cl.t[c][lane] = (uint16_t)t;
+            }
+            ++c;
+        }
+        s = affine_mad(A1, C1, s);
+    }
+    // selection sort of the column's k smallest into its first k slots
+    bool fb = valid && (c < k || c > capl);
+    const int kk = fb ? 0 : k;
+    for (int r = 0; r < kk; ++r) {
+        uint32_t best = cl.hi[r][lane];
+        int bi = r;
+        for (int x = r + 1; x < c; ++x) {
+            const uint32_t h = cl.hi[x][lane];
+            fb |= h == best;
+            if (h < best) {
+                best = h;
+                bi = x;
+            }
+        }
+        const uint16_t tb = cl.t[bi][lane];
+        cl.hi[bi][lane] = cl.hi[r][lane];
+        cl.t[bi][lane] = cl.t[r][lane];
+        cl.hi[r][lane] = best;
+        cl.t[r][lane] = tb;
+    }
+    const int64_t off = valid ? lpl.off[li] : 0;
+    const int64_t kpre = valid ? lpl.kpre[li] : 0;
+    const int32_t q = valid ? lpl.q[li] : 0;
+    if (fb) {   // exact CTA kernel (runs after this one)
+        const int64_t slot = (int64_t)atomicAdd((unsigned long long*)heavy_count, 1ull);
+        heavy[slot] = q;
+        deg_prefix[q] = dpos;
+        k_prefix[q] = kpre;
+    }
+    const int ko = fb ? 0 : kk;
+    for (int r0 = 0; r0 < ko; r0 += 4) {   // four column reads in flight before their stores
+        int32_t v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (r0 + u < ko) v[u] = indices[off + cl.t[r0 + u][lane]];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (r0 + u < ko) {
+                if (out_ids) out_ids[kpre + r0 + u] = v[u];
+                if (out_pidx) out_pidx[kpre + r0 + u] = q;
+                if (bitmap) mark_bit(bitmap, v[u]);
+            }
+        }
+    }
+    __syncwarp();
+}
+
+union WalkSmem {
+    SegWarp seg;
+    LaneCols lane;
+};
+
+// Persistent warps over one claim counter: the wide list's slices first
+// (the long work starts early), then the lane groups, heaviest first
+// (group j of every prep tile before group j + 1 of any).
+template <int WPB, int MINB>
+__global__ void __launch_bounds__(WPB * 32, MINB)
+sample_walk_kernel(const int32_t* __restrict__ indices, const uint64_t* __restrict__ table, LightParents lpar,
+                   LightParents lpl, HopMeta* __restrict__ meta, int64_t* __restrict__ deg_prefix,
+                   int64_t* __restrict__ k_prefix, int32_t* __restrict__ heavy, int64_t* __restrict__ heavy_count,
+                   int32_t* __restrict__ out_ids, int32_t* __restrict__ out_pidx, uint32_t* __restrict__ bitmap,
+                   int group, int cap, int capl, int lanes_on) {
+    __shared__ WalkSmem s_walk[WPB];
+    WalkSmem& ws = s_walk[warp_id()];
+    const int lane = lane_id();
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned FULL = 0xffffffffu;
+    const PcgTable T{table};
+    const int nslices = (int)meta->nslices;
+    const int ntiles = (int)meta->ntiles;
+    const int nclaims = nslices + (lanes_on ? ntiles * (kPrepTile / 32) : 0);
+    while (true) {
+        int g = 0;
+        if (lane == 0) g = (int)atomicAdd(&meta->ticket, 1u);
+        g = __shfl_sync(FULL, g, 0);
+        if (g >= nclaims) break;
+        if (g < nslices) {
+            slice_one(ws.seg, lpar.sf[g], lpar.sf[g + 1], lpar, meta, T, T.A(5), T.C(5), indices, out_ids, out_pidx,
+                      bitmap, group, cap, lane, lt);
+        } else {
+            lane_one(ws.lane, g - nslices, lpl, meta, ntiles, T, T.A(0), T.C(0), indices, deg_prefix, k_prefix,
+                     heavy, heavy_count, out_ids, out_pidx, bitmap, capl, lane);
+        }
     }
 }
 
@@ -877,7 +1360,7 @@ int bgl_debug_seg_trace(void* buf) {
 
 size_t bgl_sample_hop_workspace(int64_t max_parents) {
     int64_t m = max_parents > 0 ? max_parents : 1;
-    return align256(m * 8) * 2 + align256(m * 4) + align256(scan_state_bytes(2, m)) + 256;
+    return hop_ws_bytes(m) + slice_ws_bytes(m);
 }
 
 int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t* parents,
@@ -892,9 +1375,6 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
                   "bgl_sample_hop: null pointer");
     cudaStream_t st = as_stream(stream);
     HopWorkspace w = carve_hop_ws(workspace, max_parents);
-    // scan state + heavy counter are contiguous: one memset
-    BGL_TRY(cuda_status(cudaMemsetAsync(w.scan, 0, align256(scan_state_bytes(2, w.max_tiles)) + 8, st),
-                        "hop workspace reset"));
     uint32_t* bm = reinterpret_cast<uint32_t*>(mark_bitmap);
     // fused scan + sample over runs of `run` parents: short runs when the hop is
     // small (enough warps for hop 1), up to kRun (one per lane) when it is large
@@ -914,9 +1394,15 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
         const char* e = getenv("BGL_SAMPLER");
         if (e && std::string(e) == "fused") return 0;
         if (e && std::string(e) == "cand") return 1;
+        if (e && std::string(e) == "slice") return 3;
+        if (e && std::string(e) == "hybrid") return 4;
         return 2;
     }();
     const int mode = fanout <= 32 ? mode_env : 0;
+    if (mode >= 3) run = kRun;                 // a slice's parents are walked 32 at a time
+    else   // scan state + heavy counter are contiguous: one memset
+        BGL_TRY(cuda_status(cudaMemsetAsync(w.scan, 0, align256(scan_state_bytes(2, w.max_tiles)) + 8, st),
+                            "hop workspace reset"));
     // candidate threshold keeps ~k + 2 sqrt(k) + 1 draws per parent (a sweep of
     // the margin at C2: (1, 1) 4027, (1.5, 1) 4079, (2, 1) 4102, (2.5, 2) 4046,
     // (3, 3) 4032 b/s with HBM features -- a few % either way; the segmented
@@ -929,7 +1415,7 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
         const int c = e ? atoi(e) : kSegCap;
         return c < 1 ? 1 : (c > kSegCap ? kSegCap : c);
     }();
-    if (mode == 2 && seg_cap == kSegCap) {   // a run's expected candidates stay well inside the list
+    if (mode >= 2 && seg_cap == kSegCap) {   // a run's expected candidates stay well inside the list
         const double mu = fanout + mar[0] * std::sqrt((double)fanout) + mar[1];
         const int64_t rmax = std::max<int64_t>(1, (int64_t)(kSegCap / (1.5 * mu)));
         run = std::min<int64_t>(run, rmax);
@@ -949,7 +1435,74 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     const unsigned cap_blocks = (unsigned)kNumSMs * 8;
     if (blocks > cap_blocks) blocks = cap_blocks;               // runs are claimed dynamically
     if (max_ctas > 0 && blocks > (unsigned)max_ctas) blocks = (unsigned)max_ctas;
-    if (mode == 2) {
+    if (mode >= 3) {
+        // wide parents: slices of ~S light draws, ~1.5 per resident warp at
+        // the expected hop size (max_parents x BGL_SLICE_DEG, default 128
+        // draws per parent; BGL_SLICE_DRAWS overrides), never below kSliceMin;
+        // lane parents (mode 4, k <= 10): deg <= BGL_LANE_DEG (default 64)
+        static const int64_t slice_env = [] {
+            const char* e = getenv("BGL_SLICE_DRAWS");
+            return (int64_t)(e ? atoll(e) : 0);
+        }();
+        static const int64_t deg_hint = [] {
+            const char* e = getenv("BGL_SLICE_DEG");
+            return (int64_t)(e ? atoll(e) : 128);
+        }();
+        static const int lane_deg = [] {
+            const char* e = getenv("BGL_LANE_DEG");
+            return e ? std::max(0, std::min(atoi(e), (int)kNarrowMaxDeg)) : 64;
+        }();
+        // column length per lane (BGL_LANE_CAP < kLaneCap: tests force full columns)
+        static const int lane_cap = [] {
+            const char* e = getenv("BGL_LANE_CAP");
+            return e ? std::max(1, std::min(atoi(e), kLaneCap)) : kLaneCap;
+        }();
+        const int dlane = (mode == 4 && fanout <= 10) ? lane_deg : 0;
+        int64_t S = slice_env;
+        if (S <= 0) {   // ~1.5 slices per resident warp (32 per SM)
+            const int64_t want = (int64_t)kNumSMs * 48;
+            S = kSliceMin;
+            while (S < 8192 && 2 * S * want <= max_parents * deg_hint) S *= 2;
+        }
+        S = std::max<int64_t>(S, kSliceMin);
+        const int64_t m = std::max<int64_t>(max_parents, 1);
+        char* base = reinterpret_cast<char*>(workspace) + hop_ws_bytes(m);
+        const int64_t ptiles = prep_tiles(m);
+        BGL_TRY(cuda_status(cudaMemsetAsync(base, 0, slice_reset_bytes(m), st), "walk workspace reset"));
+        ScanState ps = make_scan_state(base, kPrepVals, ptiles);
+        char* r = base + align256(scan_state_bytes(kPrepVals, ptiles));
+        int64_t* hcount = reinterpret_cast<int64_t*>(r);
+        HopMeta* meta = reinterpret_cast<HopMeta*>(r + 64);
+        char* a = base + slice_reset_bytes(m);
+        auto carve_list = [&](LightParents& L) {
+            L.q = reinterpret_cast<int32_t*>(a); a += align256(m * 4);
+            L.dk = reinterpret_cast<int32_t*>(a); a += align256(m * 4);
+            L.thr = reinterpret_cast<uint32_t*>(a); a += align256(m * 4);
+            L.lp = reinterpret_cast<int64_t*>(a); a += align256(m * 8);
+            L.gap = reinterpret_cast<int64_t*>(a); a += align256(m * 8);
+            L.off = reinterpret_cast<int64_t*>(a); a += align256(m * 8);
+            L.kpre = reinterpret_cast<int64_t*>(a); a += align256(m * 8);
+            L.sf = L.perm = L.tbase = L.tcount = nullptr;
+        };
+        LightParents wl, ll;
+        carve_list(wl);
+        wl.sf = reinterpret_cast<int32_t*>(a); a += align256((8 * m + 2) * 4);
+        carve_list(ll);
+        ll.perm = reinterpret_cast<int32_t*>(a); a += align256(m * 4);
+        ll.tbase = reinterpret_cast<int32_t*>(a); a += align256(ptiles * 4);
+        ll.tcount = reinterpret_cast<int32_t*>(a);
+        sample_prep_kernel<<<(unsigned)ptiles + 1, kPrepThreads, 0, st>>>(
+            indptr, parents, num_parents_dev, fanout, table, draw_base, ps, w.deg_prefix, w.k_prefix, w.heavy, hcount,
+            wl, ll, meta, num_out_dev, heavy_deg, mar[0], mar[1], (int32_t)S, dlane);
+        BGL_TRY(launch_status("sample_prep_kernel"));
+        unsigned sblocks = (unsigned)kNumSMs * 4;
+        if (max_ctas > 0 && sblocks > (unsigned)max_ctas) sblocks = (unsigned)max_ctas;
+        sample_walk_kernel<8, 4><<<sblocks, 8 * 32, 0, st>>>(indices, table, wl, ll, meta, w.deg_prefix, w.k_prefix,
+                                                             w.heavy, hcount, out_ids, out_parent_idx, bm,
+                                                             (int32_t)run, seg_cap, lane_cap, dlane > 0 ? 1 : 0);
+        BGL_TRY(launch_status("sample_walk_kernel"));
+        w.heavy_count = hcount;
+    } else if (mode == 2) {
         auto kern = wpb == 6 ? sample_seg_kernel<6, 6> : sample_seg_kernel<8, 4>;
         kern<<<blocks, wpb * 32, 0, st>>>(
             indptr, indices, parents, num_parents_dev, fanout, table, draw_base, ss, w.deg_prefix, w.k_prefix,

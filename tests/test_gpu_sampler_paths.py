@@ -1,7 +1,8 @@
 """GPU parity for the sampler's rare paths: hubs mixed into long runs (heavy
 gaps), candidate-list overflow and the exact top-k fallback (forced with a
-tiny list), and the A/B kernels (BGL_SAMPLER=cand|fused) — all bit-exact
-against the oracle on the same hub graph."""
+tiny list), the A/B walks (BGL_SAMPLER=slice|hybrid: prep kernel + slice /
+lane walk, slice sizes and lane degrees at both extremes; cand|fused) — all bit-exact against the oracle on the same
+hub graph."""
 import os
 import subprocess
 import sys
@@ -27,12 +28,22 @@ def test_hubs_inside_long_runs(ref_path):
 
 
 @pytest.mark.parametrize("env", [
-    {"BGL_SEG_CAP": "24", "BGL_RUNS_PER_SM": "1"},     # every run 32 parents, lists overflow
+    {"BGL_SEG_CAP": "24", "BGL_RUNS_PER_SM": "1"},     # look-back walk: every run 32 parents, lists overflow
     {"BGL_SEG_CAP": "1"},                              # almost every parent takes the fallback
+    {"BGL_SEG_OCC": "6x6"},                            # 6 warps x 6 CTAs per SM walk
+    {"BGL_SAMPLER": "hybrid"},                         # lane walk (deg <= 64) + slices
+    {"BGL_SAMPLER": "hybrid", "BGL_LANE_CAP": "12"},   # full lane columns -> exact CTA kernel
+    {"BGL_SAMPLER": "hybrid", "BGL_LANE_CAP": "1"},    # almost every lane parent takes the exact kernel
+    {"BGL_SAMPLER": "hybrid", "BGL_LANE_DEG": "2048"},  # every light parent walked by one lane
+    {"BGL_SAMPLER": "hybrid", "BGL_LANE_DEG": "3", "BGL_SLICE_DRAWS": "256"},
+    {"BGL_SAMPLER": "slice"},
+    {"BGL_SAMPLER": "slice", "BGL_SEG_CAP": "24"},     # slice walk: lists overflow
+    {"BGL_SAMPLER": "slice", "BGL_SEG_CAP": "1"},      # almost every parent takes the fallback
+    {"BGL_SAMPLER": "slice", "BGL_SLICE_DRAWS": "256"},      # smallest slices: many empty ones behind long parents
+    {"BGL_SAMPLER": "slice", "BGL_SLICE_DRAWS": "1000000"},  # one slice per hop: many 32-parent groups per slice
+    {"BGL_SAMPLER": "slice", "BGL_SLICE_DRAWS": "300", "BGL_SEG_CAP": "24"},
     {"BGL_SAMPLER": "cand"},
     {"BGL_SAMPLER": "fused", "BGL_RUNS_PER_SM": "2"},
-    {"BGL_SEG_OCC": "6x6"},                            # 6 warps x 6 CTAs per SM walk
-    {"BGL_SEG_OCC": "6x6", "BGL_SEG_CAP": "24", "BGL_RUNS_PER_SM": "1"},
 ])
 def test_rare_paths_under_env(env, ref_path):
     e = dict(os.environ, **env)

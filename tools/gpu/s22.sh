@@ -1,0 +1,11 @@
+# Slice sampler round 2: parity, A/B timing (back-to-back), launch list, ncu source of the hop-3 slice walk
+mkdir -p gpurun_out/s22
+timeout 1200 python -m pytest tests/test_gpu_sampler.py tests/test_gpu_sampler_paths.py tests/test_gpu_c2.py tests/test_gpu_c1.py -q > gpurun_out/s22/pytest_sampler.log 2>&1; echo "pytest rc=$?" >> gpurun_out/s22/pytest_sampler.log
+tail -3 gpurun_out/s22/pytest_sampler.log
+BGL_SAMPLER=seg timeout 600 python tools/hop_bench.py --config c2 --batches 40 --out gpurun_out/s22/hop_seg.json 2> gpurun_out/s22/hop.err
+for S in auto 1024 4096 8192; do if [ $S = auto ]; then unset BGL_SLICE_DRAWS; else export BGL_SLICE_DRAWS=$S; fi; timeout 600 python tools/hop_bench.py --config c2 --batches 40 --out gpurun_out/s22/hop_slice_$S.json 2>> gpurun_out/s22/hop.err; done
+unset BGL_SLICE_DRAWS
+timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum,smsp__inst_executed.sum,sm__warps_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active --clock-control none --csv --log-file gpurun_out/s22/launches_hbm.csv python tools/profile_step.py --steps 3 --features hbm > gpurun_out/s22/prof_hbm.log 2>&1
+timeout 900 ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:"sample_slice|sample_prep" -c 6 -o gpurun_out/s22/full_slice python tools/profile_step.py --steps 1 --features hbm > gpurun_out/s22/full.log 2>&1
+timeout 600 python bench.py --features hbm --steps 100 --warmup 10 --no-cpu-baseline > gpurun_out/s22/c2_hbm.json 2> gpurun_out/s22/c2_hbm.err
+python -c "import json; d=json.loads(open('gpurun_out/s22/c2_hbm.json').read().strip().splitlines()[-1]); print('c2_hbm', d['value'], d['e2e']['value'], d['roofline']['frac'])"
