@@ -31,6 +31,21 @@ __host__ __device__ __forceinline__ U128 add128(U128 a, U128 b) {
 // s -> A*s + C
 __host__ __device__ __forceinline__ U128 affine(U128 A, U128 C, U128 s) { return add128(mul128(A, s), C); }
 
+// affine() with the 128-bit add as one add.cc/addc chain (no compare-and-
+// select carry): the walk's per-draw step (~2 SASS instructions fewer than
+// affine(), ~4 fewer than affine_mad() in the walk loop, sm_100a)
+__device__ __forceinline__ U128 affine_cc(U128 A, U128 C, U128 s) {
+    const U128 p = mul128(A, s);
+    uint32_t r0 = (uint32_t)p.lo, r1 = (uint32_t)(p.lo >> 32), r2 = (uint32_t)p.hi, r3 = (uint32_t)(p.hi >> 32);
+    asm("add.cc.u32  %0, %0, %4;\n\t"
+        "addc.cc.u32 %1, %1, %5;\n\t"
+        "addc.cc.u32 %2, %2, %6;\n\t"
+        "addc.u32    %3, %3, %7;"
+        : "+r"(r0), "+r"(r1), "+r"(r2), "+r"(r3)
+        : "r"((uint32_t)C.lo), "r"((uint32_t)(C.lo >> 32)), "r"((uint32_t)C.hi), "r"((uint32_t)(C.hi >> 32)));
+    return U128{((uint64_t)r3 << 32) | r2, ((uint64_t)r1 << 32) | r0};
+}
+
 // affine() as one 32-bit-limb multiply-accumulate chain: acc = C, then
 // acc += A * s (mod 2^128) row by row (lo parts, then hi parts, each a carry
 // chain): 16 mad instructions instead of the 64-bit emulation's ~30.
