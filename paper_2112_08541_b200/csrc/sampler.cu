@@ -633,7 +633,7 @@ __device__ __forceinline__ int seg_walk(SegWarp& sw, const PcgTable T, U128 A32,
         }
 #endif
         L += __popc(bm);
-        s = affine_mad(A32, C32, s);
+        s = affine_cc(A32, C32, s);
     }
     return L;
 }
@@ -1152,7 +1152,7 @@ __device__ __forceinline__ void lane_one(LaneCols& cl, int g, const LightParents
             }
             ++c;
         }
-        s = affine_mad(A1, C1, s);
+        s = affine_cc(A1, C1, s);
     }
     // selection sort of the column's k smallest into its first k slots
     bool fb = valid && (c < k || c > capl);
