@@ -80,6 +80,8 @@ class MiniBatchPipeline:
         self.order = order.to(device="cuda", dtype=torch.int32).contiguous()
         total = int(self.order.numel())
         self.num_batches = check_num_batches(num_batches, total, self.b)
+        if not sampler_ctas:   # BGL_SAMPLER_CTAS: cap the sampler's CTAs so other branches co-run (A/B)
+            sampler_ctas = int(os.environ.get("BGL_SAMPLER_CTAS", "0"))
         self.samplers = [BatchSampler(dg, fanouts, self.b, max_ctas=sampler_ctas, rng=rng, frontier_outputs=False)
                          for _ in range(NS)]
         self.max_uniq = self.samplers[0].max_uniq
