@@ -521,20 +521,30 @@ sample_cand_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
 constexpr int kSegCap = 512;
 
 // Diagnostics (tools/seg_timeline.py, bgl_debug_seg_trace): when set, lane 0
-// of every run appends {n, r, smid, Wtot, t_claim, t_walk, t_post, t_end}
-// (globaltimer ns) -- the per-run timeline behind DESIGN.md's sampler notes.
+// of every run appends a 16-word record {n, r, smid, Wtot, t_claim, t_walk,
+// t_post, t_end, t_loaded, t_prefix, 0...} (globaltimer ns; t_loaded once
+// the run's degrees are in registers, t_prefix once both look-backs are
+// done) -- the per-run timeline behind DESIGN.md's sampler notes.
 __device__ unsigned long long* g_seg_trace = nullptr;
+constexpr int kSegTraceWords = 16;
 __device__ __forceinline__ uint64_t gtimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+// globaltimer read after `dep` is available (the asm consumes it)
+__device__ __forceinline__ uint64_t gtimer_after(int64_t dep) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) : "l"(dep));
+    return t;
+}
 __device__ __noinline__ void seg_trace_record(unsigned long long* trace, int64_t n, int64_t r, int32_t Wtot,
-                                              uint64_t t_claim, uint64_t t_walk, uint64_t t_post) {
+                                              uint64_t t_claim, uint64_t t_walk, uint64_t t_post, uint64_t t_loaded,
+                                              uint64_t t_prefix) {
     unsigned sm;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
     const unsigned long long slot = atomicAdd(trace, 1ull);
-    unsigned long long* rec = trace + 8 + 8 * slot;
+    unsigned long long* rec = trace + kSegTraceWords + kSegTraceWords * slot;
     rec[0] = (unsigned long long)n;
     rec[1] = (unsigned long long)r;
     rec[2] = sm;
@@ -543,6 +553,8 @@ __device__ __noinline__ void seg_trace_record(unsigned long long* trace, int64_t
     rec[5] = t_walk;
     rec[6] = t_post;
     rec[7] = gtimer();
+    rec[8] = t_loaded;
+    rec[9] = t_prefix;
 }
 
 struct SegWarp {
@@ -749,7 +761,7 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
         if (lane == 0) r = (int64_t)atomicAdd(ss.ticket, 1u);
         r = __shfl_sync(FULL, r, 0);
         if (r >= nruns) break;
-        uint64_t t_claim = 0, t_walk = 0, t_post = 0;
+        uint64_t t_claim = 0, t_walk = 0, t_post = 0, t_loaded = 0, t_prefix = 0;
         if (trace) t_claim = gtimer();
         const int64_t q = r * run + lane;
         const bool valid = lane < run && q < n;
@@ -761,6 +773,7 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
         const int64_t incl_k = warp_incl_scan(k);
         const int64_t agg_d = __shfl_sync(FULL, incl_d, 31);
         const int64_t agg_k = __shfl_sync(FULL, incl_k, 31);
+        if (trace) t_loaded = gtimer_after(agg_k);
         if (lane == 0) {
             const uint64_t f = r == 0 ? kFlagInc : kFlagAgg;
             atomicExch((unsigned long long*)(ss.status + r), (unsigned long long)(f | ((uint64_t)agg_d & kValMask)));
@@ -769,6 +782,7 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
         }
         const int64_t pre_d = warp_lookback1(ss.status, r, agg_d);
         const int64_t pre_k = warp_lookback1(ss.status + ss.max_tiles, r, agg_k);
+        if (trace) t_prefix = gtimer_after(pre_d + pre_k);
         const int64_t ex_d = pre_d + incl_d - deg;
         const int64_t ex_k = pre_k + incl_k - k;
         const bool hv = valid && (k > 32 || deg > heavy_deg);
@@ -814,7 +828,7 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
         if (trace) t_post = gtimer();
         seg_post(sw, L, cap, lane, (int)k, off, ex_k, light, deg, T.state(), (uint64_t)(D0 + ex_d),
                  (int32_t)(r * run + lane), T, A32, C32, indices, out_ids, out_pidx, bitmap);
-        if (trace && lane == 0) seg_trace_record(trace, n, r, Wtot, t_claim, t_walk, t_post);
+        if (trace && lane == 0) seg_trace_record(trace, n, r, Wtot, t_claim, t_walk, t_post, t_loaded, t_prefix);
     }
 }
 

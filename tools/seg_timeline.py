@@ -40,14 +40,15 @@ for _ in range(a.warm):
     pipe.step()
 torch.cuda.synchronize()
 cap = 1 << 20
-buf = torch.zeros(8 + 8 * cap, dtype=torch.int64, device="cuda")
+W = 16   # words per record (csrc/sampler.cu kSegTraceWords)
+buf = torch.zeros(W + W * cap, dtype=torch.int64, device="cuda")
 lib = _lib.load()
 _lib.check(lib.bgl_debug_seg_trace(buf.data_ptr()))
 pipe.step_eager()
 torch.cuda.synchronize()
 _lib.check(lib.bgl_debug_seg_trace(None))
 nrec = int(buf[0].item())
-rec = buf[8:8 + 8 * nrec].view(nrec, 8).cpu().numpy()
+rec = buf[W:W + W * nrec].view(nrec, W).cpu().numpy()
 report = {"config": a.config, "features": a.features, "hops": []}
 for n in sorted(set(rec[:, 0].tolist())):
     r = rec[rec[:, 0] == n]
@@ -55,13 +56,19 @@ for n in sorted(set(rec[:, 0].tolist())):
     claim, walk, post, end = (r[:, 4] - t0) / 1e3, (r[:, 5] - t0) / 1e3, (r[:, 6] - t0) / 1e3, (r[:, 7] - t0) / 1e3
     span = end.max()
     setup_us, walk_us, post_us = walk - claim, post - walk, end - post
+    loaded, prefix = (r[:, 8] - t0) / 1e3, (r[:, 9] - t0) / 1e3
     draws = r[:, 3].astype(np.float64)
     # busy runs over time (1 us bins)
     bins = np.arange(0, span + 1.0, 1.0)
     busy = [int(((claim <= b) & (end > b)).sum()) for b in bins]
     late = int((claim > 0.25 * span).sum())
     h = {"parents": int(n), "runs": int(len(r)), "span_us": round(float(span), 2),
-         "setup_us_mean": round(float(setup_us.mean()), 2), "walk_us_mean": round(float(walk_us.mean()), 2),
+         "setup_us_mean": round(float(setup_us.mean()), 2),
+         "setup_split_us_mean": {"loads": round(float((loaded - claim).mean()), 2),
+                                 "lookback": round(float((prefix - loaded).mean()), 2),
+                                 "layout": round(float((walk - prefix).mean()), 2)},
+         "lookback_us_p50_p90_max": [round(float(np.percentile(prefix - loaded, q)), 2) for q in (50, 90, 100)],
+         "walk_us_mean": round(float(walk_us.mean()), 2),
          "post_us_mean": round(float(post_us.mean()), 2), "run_us_mean": round(float((end - claim).mean()), 2),
          "run_us_p50_p90_max": [round(float(np.percentile(end - claim, q)), 2) for q in (50, 90, 100)],
          "draws_mean": round(float(draws.mean()), 1), "draws_p90_max": [float(np.percentile(draws, 90)), float(draws.max())],
