@@ -57,6 +57,9 @@ struct HopWorkspace {
     int64_t* heavy_count;  // [1]
     void* scan;            // scan state for 2 values
     int64_t max_tiles;
+    int32_t* split_ctr;    // [3] split queue: pushed, claimed, runs that have decided (after heavy_count)
+    int32_t* split_ready;  // [max_tiles] entry published
+    int64_t* split_ent;    // [max_tiles] run << 8 | first parent of the split-off part
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -75,13 +78,21 @@ static HopWorkspace carve_hop_ws(void* ws, int64_t max_parents) {
     w.scan = p;
     p += align256(scan_state_bytes(2, w.max_tiles));
     w.heavy_count = reinterpret_cast<int64_t*>(p);   // zeroed with the scan state (contiguous)
+    w.split_ctr = reinterpret_cast<int32_t*>(p + 64);
+    p += 256;
+    w.split_ready = reinterpret_cast<int32_t*>(p);   // zeroed too
+    p += align256(m * 4);
+    w.split_ent = reinterpret_cast<int64_t*>(p);
     return w;
 }
 
 // Slice-path workspace, after the HopWorkspace: [prep scan state (4 values) |
 // heavy count | HopMeta] (one memset per hop), then the light-parent arrays.
 static int64_t prep_tiles(int64_t m) { return ceil_div(m > 0 ? m : 1, 2048); }
-static size_t hop_ws_bytes(int64_t m) { return align256(m * 8) * 2 + align256(m * 4) + align256(scan_state_bytes(2, m)) + 256; }
+// [deg prefix | k prefix | heavy list | scan state | counters (256) | split ready | split entries];
+// scan state, counters and split-ready flags are zeroed per hop (one memset)
+static size_t hop_reset_bytes(int64_t m) { return align256(scan_state_bytes(2, m)) + 256 + align256(m * 4); }
+static size_t hop_ws_bytes(int64_t m) { return align256(m * 8) * 2 + align256(m * 4) + hop_reset_bytes(m) + align256(m * 8); }
 static size_t slice_reset_bytes(int64_t m) { return align256(scan_state_bytes(5, prep_tiles(m))) + 256; }
 static size_t light_list_bytes(int64_t m) { return align256(m * 4) * 3 + align256(m * 8) * 4; }
 static size_t slice_ws_bytes(int64_t m) {
@@ -733,9 +744,54 @@ __device__ __forceinline__ void seg_post(SegWarp& sw, int L, int cap, int lane, 
     __syncwarp();
 }
 
+// One part of a run (lane i = parent i of the part; invalid lanes take no
+// part): walk layout of its light parents, the walk from the part's first
+// draw (D0 + ex_d of lane 0), ranking/output and fallbacks.
+__device__ __forceinline__ void seg_part(SegWarp& sw, bool valid, int64_t off, int64_t deg, int64_t k, int64_t ex_d,
+                                         int64_t ex_k, bool hv, int32_t pid, int64_t D0, const PcgTable T, U128 A32,
+                                         U128 C32, int lane, unsigned lt, int cap, float ma, float mb,
+                                         const int32_t* __restrict__ indices, int32_t* __restrict__ out_ids,
+                                         int32_t* __restrict__ out_pidx, uint32_t* __restrict__ bitmap,
+                                         bool trace, uint64_t& t_walk, uint64_t& t_post, int32_t& Wtot_out) {
+    const unsigned FULL = 0xffffffffu;
+    const int64_t ex0 = __shfl_sync(FULL, ex_d, 0);
+    const bool light = valid && !hv && deg > 0;
+    const int32_t ldeg = light ? (int32_t)deg : 0;
+    const int32_t incl_l = warp_incl_scan(ldeg);
+    const int32_t Wtot = __shfl_sync(FULL, incl_l, 31);
+    sw.wst[lane] = incl_l - ldeg;
+    sw.wend[lane] = incl_l;
+    sw.gap[lane] = (ex_d - ex0) - (int64_t)(incl_l - ldeg);
+    // T = 2^53 ("every draw") -> 2^32 - 1, which drops only draws with
+    // out_hi = 2^32 - 1: the largest m, so either k others remain or the
+    // parent takes the exact fallback (fewer than k candidates)
+    sw.thr[lane] = light ? thr_hi(cand_threshold(k, deg, ma, mb)) : 0u;
+    if (lane == 0) {
+        sw.wend[32] = 0x7fffffff;
+        sw.thr[32] = 0;
+        sw.gap[32] = 0;
+        sw.wst[32] = 0;
+    }
+    const unsigned hm = __ballot_sync(FULL, valid && hv);
+    __syncwarp();
+    int L = 0;
+    if (trace) t_walk = gtimer();
+    if (Wtot > 0) L = hm ? seg_walk<true>(sw, T, A32, C32, T.state(), D0 + ex0, Wtot, lane, lt, cap)
+                         : seg_walk<false>(sw, T, A32, C32, T.state(), D0 + ex0, Wtot, lane, lt, cap);
+    __syncwarp();
+    if (trace) t_post = gtimer();
+    seg_post(sw, L, cap, lane, (int)k, off, ex_k, light, deg, T.state(), (uint64_t)(D0 + ex_d), pid, T, A32, C32,
+             indices, out_ids, out_pidx, bitmap);
+    Wtot_out = Wtot;
+}
+
 // WPB warps per CTA, MINB CTAs per SM: (8, 4) = 32 resident warps per SM
 // (64 registers); (6, 6) = 36 (56 registers), enough for the largest hop's
 // runs to start in one wave (153.6K parents / 32 = 4800 runs vs 4736 / 5328).
+// split_min > 0: a run whose light draws reach split_min hands the parents
+// past its walk's midpoint to a queue (their offsets in deg_prefix /
+// k_prefix); warps that find no run left take them, so the longest runs no
+// longer set the kernel's tail alone.
 template <int WPB, int MINB>
 __global__ void __launch_bounds__(WPB * 32, MINB)
 sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
@@ -744,7 +800,9 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
                   ScanState ss, int64_t* __restrict__ deg_prefix, int64_t* __restrict__ k_prefix,
                   int32_t* __restrict__ heavy, int64_t* __restrict__ heavy_count,
                   int32_t* __restrict__ out_ids, int32_t* __restrict__ out_pidx, int64_t* __restrict__ num_out,
-                  uint32_t* __restrict__ bitmap, int32_t run, int64_t heavy_deg, float ma, float mb, int cap) {
+                  uint32_t* __restrict__ bitmap, int32_t run, int64_t heavy_deg, float ma, float mb, int cap,
+                  int32_t split_min, int32_t* __restrict__ split_ctr, int32_t* __restrict__ split_ready,
+                  int64_t* __restrict__ split_ent) {
     __shared__ SegWarp s_seg[WPB];
     SegWarp& sw = s_seg[warp_id()];
     const int64_t n = *num_parents_dev;
@@ -801,34 +859,82 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
             draw_base[1] = D0 + pre_d + incl_d;
             *num_out = pre_k + incl_k;
         }
-        // walk layout of the run's light parents
-        const bool light = valid && !hv && deg > 0;
-        const int32_t ldeg = light ? (int32_t)deg : 0;
-        const int32_t incl_l = warp_incl_scan(ldeg);
-        const int32_t Wtot = __shfl_sync(FULL, incl_l, 31);
-        sw.wst[lane] = incl_l - ldeg;
-        sw.wend[lane] = incl_l;
-        sw.gap[lane] = (incl_d - deg) - (int64_t)(incl_l - ldeg);
-        // T = 2^53 ("every draw") -> 2^32 - 1, which drops only draws with
-        // out_hi = 2^32 - 1: the largest m, so either k others remain or the
-        // parent takes the exact fallback (fewer than k candidates)
-        sw.thr[lane] = light ? thr_hi(cand_threshold(k, deg, ma, mb)) : 0u;
-        if (lane == 0) {
-            sw.wend[32] = 0x7fffffff;
-            sw.thr[32] = 0;
-            sw.gap[32] = 0;
-            sw.wst[32] = 0;
+        int jend = 32;
+        if (split_min > 0) {
+            const bool light = valid && !hv && deg > 0;
+            const int32_t incl_l = warp_incl_scan(light ? (int32_t)deg : 0);
+            const int32_t Wt = __shfl_sync(FULL, incl_l, 31);
+            if (Wt >= split_min) {
+                // part A: parents up to the one crossing the walk's midpoint; part B: the rest
+                const unsigned cross = __ballot_sync(FULL, valid && 2 * incl_l >= Wt);
+                const int j1 = cross ? __ffs(cross) : 32;
+                const int cnt = (int)(n - r * run < run ? n - r * run : run);
+                const int32_t before = j1 > 0 && j1 < 32 ? __shfl_sync(FULL, incl_l, j1 - 1) : Wt;
+                if (j1 < cnt && Wt - before > 0) {
+                    if (valid && lane >= j1) {
+                        deg_prefix[q] = ex_d;
+                        k_prefix[q] = ex_k;
+                    }
+                    __threadfence();
+                    __syncwarp();
+                    if (lane == 0) {
+                        const int slot = atomicAdd(split_ctr + 0, 1);
+                        split_ent[slot] = (r << 8) | j1;
+                        __threadfence();
+                        atomicExch(split_ready + slot, 1);
+                    }
+                    jend = j1;
+                }
+            }
+            if (lane == 0) {
+                __threadfence();
+                atomicAdd(split_ctr + 2, 1);
+            }
         }
-        __syncwarp();
-        int L = 0;
-        if (trace) t_walk = gtimer();
-        if (Wtot > 0) L = hm ? seg_walk<true>(sw, T, A32, C32, T.state(), D0 + pre_d, Wtot, lane, lt, cap)
-                             : seg_walk<false>(sw, T, A32, C32, T.state(), D0 + pre_d, Wtot, lane, lt, cap);
-        __syncwarp();
-        if (trace) t_post = gtimer();
-        seg_post(sw, L, cap, lane, (int)k, off, ex_k, light, deg, T.state(), (uint64_t)(D0 + ex_d),
-                 (int32_t)(r * run + lane), T, A32, C32, indices, out_ids, out_pidx, bitmap);
+        int32_t Wtot = 0;
+        seg_part(sw, valid && lane < jend, off, deg, k, ex_d, ex_k, hv, (int32_t)q, D0, T, A32, C32, lane, lt, cap,
+                 ma, mb, indices, out_ids, out_pidx, bitmap, trace != nullptr, t_walk, t_post, Wtot);
         if (trace && lane == 0) seg_trace_record(trace, n, r, Wtot, t_claim, t_walk, t_post, t_loaded, t_prefix);
+    }
+    if (split_min <= 0) return;
+    // no run left: take split-off parts until every run has decided and the queue is drained
+    while (true) {
+        int64_t idx = 0;
+        if (lane == 0) {
+            idx = atomicAdd(split_ctr + 1, 1);
+            if (idx >= nruns) {
+                idx = -1;   // never valid: at most one part per run
+            } else {
+                unsigned ns = 64;
+                while (!ld_volatile(split_ready + idx)) {
+                    if (ld_volatile(split_ctr + 2) >= nruns && ld_volatile(split_ctr + 0) <= idx) {
+                        idx = -1;
+                        break;
+                    }
+                    __nanosleep(ns);
+                    ns = ns < 1024 ? 2 * ns : ns;
+                }
+            }
+        }
+        idx = __shfl_sync(FULL, idx, 0);
+        if (idx < 0) break;
+        __threadfence();
+        const int64_t e = ld_volatile(split_ent + idx);
+        const int64_t r = e >> 8;
+        const int j1 = (int)(e & 255);
+        const int64_t q = r * run + j1 + lane;
+        const bool valid = j1 + lane < run && q < n;
+        const int32_t p = valid ? parents[q] : 0;
+        const int64_t off = valid ? indptr[p] : 0;
+        const int64_t deg = valid ? indptr[p + 1] - off : 0;
+        const int64_t k = deg < fanout ? deg : fanout;
+        const int64_t ex_d = valid ? ld_volatile(deg_prefix + q) : 0;
+        const int64_t ex_k = valid ? ld_volatile(k_prefix + q) : 0;
+        const bool hv = valid && (k > 32 || deg > heavy_deg);
+        uint64_t t_walk = 0, t_post = 0;
+        int32_t Wtot = 0;
+        seg_part(sw, valid, off, deg, k, ex_d, ex_k, hv, (int32_t)q, D0, T, A32, C32, lane, lt, cap, ma, mb, indices,
+                 out_ids, out_pidx, bitmap, false, t_walk, t_post, Wtot);
     }
 }
 
@@ -1414,8 +1520,8 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     }();
     const int mode = fanout <= 32 ? mode_env : 0;
     if (mode >= 3) run = kRun;                 // a slice's parents are walked 32 at a time
-    else   // scan state + heavy counter are contiguous: one memset
-        BGL_TRY(cuda_status(cudaMemsetAsync(w.scan, 0, align256(scan_state_bytes(2, w.max_tiles)) + 8, st),
+    else   // scan state + counters + split-ready flags are contiguous: one memset
+        BGL_TRY(cuda_status(cudaMemsetAsync(w.scan, 0, hop_reset_bytes(std::max<int64_t>(max_parents, 1)), st),
                             "hop workspace reset"));
     // candidate threshold keeps ~k + 2 sqrt(k) + 1 draws per parent (a sweep of
     // the margin at C2: (1, 1) 4027, (1.5, 1) 4079, (2, 1) 4102, (2.5, 2) 4046,
@@ -1517,11 +1623,22 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
         BGL_TRY(launch_status("sample_walk_kernel"));
         w.heavy_count = hcount;
     } else if (mode == 2) {
+        // BGL_SEG_SPLIT=D: runs of >= 16 parents whose light draws reach D hand
+        // their second half to warps that find no run left (C2 hop 3 warm,
+        // graph replays: 112.9 -> 105.9 us at D = 3072; 2048: 106.2, 4096:
+        // 109.2, 6144: 114.6). Off by default: the pipelined C2 HBM line is
+        // unchanged (5225 vs 5215) and hop 3 under ncu's serialised, cold-cache
+        // replay takes 63.5 M instead of 56 M instructions and 105-113 us.
+        static const int32_t split_env = [] {
+            const char* e = getenv("BGL_SEG_SPLIT");
+            return (int32_t)(e ? atoi(e) : 0);
+        }();
+        const int32_t split_min = run >= 16 ? split_env : 0;
         auto kern = wpb == 6 ? sample_seg_kernel<6, 6> : sample_seg_kernel<8, 4>;
         kern<<<blocks, wpb * 32, 0, st>>>(
             indptr, indices, parents, num_parents_dev, fanout, table, draw_base, ss, w.deg_prefix, w.k_prefix,
             w.heavy, w.heavy_count, out_ids, out_parent_idx, num_out_dev, bm, (int32_t)run, heavy_deg, mar[0], mar[1],
-            seg_cap);
+            seg_cap, split_min, w.split_ctr, w.split_ready, w.split_ent);
         BGL_TRY(launch_status("sample_seg_kernel"));
     } else if (mode == 1) {
         sample_cand_kernel<<<blocks, kWarpsPerBlock * 32, 0, st>>>(

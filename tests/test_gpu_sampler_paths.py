@@ -31,6 +31,9 @@ def test_hubs_inside_long_runs(ref_path):
     {"BGL_SEG_CAP": "24", "BGL_RUNS_PER_SM": "1"},     # look-back walk: every run 32 parents, lists overflow
     {"BGL_SEG_CAP": "1"},                              # almost every parent takes the fallback
     {"BGL_SEG_OCC": "6x6"},                            # 6 warps x 6 CTAs per SM walk
+    {"BGL_SEG_SPLIT": "16", "BGL_RUNS_PER_SM": "1"},   # every 32-parent run hands its second half to idle warps
+    {"BGL_SEG_SPLIT": "16", "BGL_SEG_CAP": "24", "BGL_RUNS_PER_SM": "1"},
+    {"BGL_SEG_SPLIT": "0"},                            # no split-off
     {"BGL_SAMPLER": "hybrid"},                         # lane walk (deg <= 64) + slices
     {"BGL_SAMPLER": "hybrid", "BGL_LANE_CAP": "12"},   # full lane columns -> exact CTA kernel
     {"BGL_SAMPLER": "hybrid", "BGL_LANE_CAP": "1"},    # almost every lane parent takes the exact kernel
