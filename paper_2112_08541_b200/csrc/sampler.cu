@@ -90,7 +90,7 @@ static HopWorkspace carve_hop_ws(void* ws, int64_t max_parents) {
 // heavy count | HopMeta] (one memset per hop), then the light-parent arrays.
 static int64_t prep_tiles(int64_t m) { return ceil_div(m > 0 ? m : 1, 2048); }
 // [deg prefix | k prefix | heavy list | scan state | counters (256) | split ready | split entries];
-// scan state, counters and split-ready flags are zeroed per hop (one memset)
+// scan state and counters are zeroed per hop, the split-ready flags when the hop splits
 static size_t hop_reset_bytes(int64_t m) { return align256(scan_state_bytes(2, m)) + 256 + align256(m * 4); }
 static size_t hop_ws_bytes(int64_t m) { return align256(m * 8) * 2 + align256(m * 4) + hop_reset_bytes(m) + align256(m * 8); }
 static size_t slice_reset_bytes(int64_t m) { return align256(scan_state_bytes(5, prep_tiles(m))) + 256; }
@@ -1520,8 +1520,8 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
     }();
     const int mode = fanout <= 32 ? mode_env : 0;
     if (mode >= 3) run = kRun;                 // a slice's parents are walked 32 at a time
-    else   // scan state + counters + split-ready flags are contiguous: one memset
-        BGL_TRY(cuda_status(cudaMemsetAsync(w.scan, 0, hop_reset_bytes(std::max<int64_t>(max_parents, 1)), st),
+    else   // scan state + counters are contiguous: one memset (the split-ready flags only when splitting)
+        BGL_TRY(cuda_status(cudaMemsetAsync(w.scan, 0, align256(scan_state_bytes(2, w.max_tiles)) + 256, st),
                             "hop workspace reset"));
     // candidate threshold keeps ~k + 2 sqrt(k) + 1 draws per parent (a sweep of
     // the margin at C2: (1, 1) 4027, (1.5, 1) 4079, (2, 1) 4102, (2.5, 2) 4046,
@@ -1634,6 +1634,8 @@ int bgl_sample_hop(const int64_t* indptr, const int32_t* indices, const int32_t*
             return (int32_t)(e ? atoi(e) : 0);
         }();
         const int32_t split_min = run >= 16 ? split_env : 0;
+        if (split_min > 0)
+            BGL_TRY(cuda_status(cudaMemsetAsync(w.split_ready, 0, (size_t)w.max_tiles * 4, st), "split flags reset"));
         auto kern = wpb == 6 ? sample_seg_kernel<6, 6> : sample_seg_kernel<8, 4>;
         kern<<<blocks, wpb * 32, 0, st>>>(
             indptr, indices, parents, num_parents_dev, fanout, table, draw_base, ss, w.deg_prefix, w.k_prefix,
