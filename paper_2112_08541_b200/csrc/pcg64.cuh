@@ -32,8 +32,9 @@ __host__ __device__ __forceinline__ U128 add128(U128 a, U128 b) {
 __host__ __device__ __forceinline__ U128 affine(U128 A, U128 C, U128 s) { return add128(mul128(A, s), C); }
 
 // affine() with the 128-bit add as one add.cc/addc chain (no compare-and-
-// select carry): the walk's per-draw step (~2 SASS instructions fewer than
-// affine(), ~4 fewer than affine_mad() in the walk loop, sm_100a)
+// select carry): the walk's per-draw step. In the walk loop it compiles to
+// ~8 SASS instructions fewer than a 16-mad 32-bit-limb chain (whose ptxas
+// expansion zeroes addends for every mad.hi) and ~2 fewer than affine().
 __device__ __forceinline__ U128 affine_cc(U128 A, U128 C, U128 s) {
     const U128 p = mul128(A, s);
     uint32_t r0 = (uint32_t)p.lo, r1 = (uint32_t)(p.lo >> 32), r2 = (uint32_t)p.hi, r3 = (uint32_t)(p.hi >> 32);
@@ -43,34 +44,6 @@ __device__ __forceinline__ U128 affine_cc(U128 A, U128 C, U128 s) {
         "addc.u32    %3, %3, %7;"
         : "+r"(r0), "+r"(r1), "+r"(r2), "+r"(r3)
         : "r"((uint32_t)C.lo), "r"((uint32_t)(C.lo >> 32)), "r"((uint32_t)C.hi), "r"((uint32_t)(C.hi >> 32)));
-    return U128{((uint64_t)r3 << 32) | r2, ((uint64_t)r1 << 32) | r0};
-}
-
-// affine() as one 32-bit-limb multiply-accumulate chain: acc = C, then
-// acc += A * s (mod 2^128) row by row (lo parts, then hi parts, each a carry
-// chain): 16 mad instructions instead of the 64-bit emulation's ~30.
-__device__ __forceinline__ U128 affine_mad(U128 A, U128 C, U128 s) {
-    const uint32_t a0 = (uint32_t)A.lo, a1 = (uint32_t)(A.lo >> 32), a2 = (uint32_t)A.hi, a3 = (uint32_t)(A.hi >> 32);
-    const uint32_t s0 = (uint32_t)s.lo, s1 = (uint32_t)(s.lo >> 32), s2 = (uint32_t)s.hi, s3 = (uint32_t)(s.hi >> 32);
-    uint32_t r0 = (uint32_t)C.lo, r1 = (uint32_t)(C.lo >> 32), r2 = (uint32_t)C.hi, r3 = (uint32_t)(C.hi >> 32);
-    asm("mad.lo.cc.u32  %0, %4, %8, %0;\n\t"
-        "madc.lo.cc.u32 %1, %4, %9, %1;\n\t"
-        "madc.lo.cc.u32 %2, %4, %10, %2;\n\t"
-        "madc.lo.u32    %3, %4, %11, %3;\n\t"
-        "mad.hi.cc.u32  %1, %4, %8, %1;\n\t"
-        "madc.hi.cc.u32 %2, %4, %9, %2;\n\t"
-        "madc.hi.u32    %3, %4, %10, %3;\n\t"
-        "mad.lo.cc.u32  %1, %5, %8, %1;\n\t"
-        "madc.lo.cc.u32 %2, %5, %9, %2;\n\t"
-        "madc.lo.u32    %3, %5, %10, %3;\n\t"
-        "mad.hi.cc.u32  %2, %5, %8, %2;\n\t"
-        "madc.hi.u32    %3, %5, %9, %3;\n\t"
-        "mad.lo.cc.u32  %2, %6, %8, %2;\n\t"
-        "madc.lo.u32    %3, %6, %9, %3;\n\t"
-        "mad.hi.u32     %3, %6, %8, %3;\n\t"
-        "mad.lo.u32     %3, %7, %8, %3;"
-        : "+r"(r0), "+r"(r1), "+r"(r2), "+r"(r3)
-        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(s0), "r"(s1), "r"(s2), "r"(s3));
     return U128{((uint64_t)r3 << 32) | r2, ((uint64_t)r1 << 32) | r0};
 }
 

@@ -39,11 +39,6 @@
 
 #include <cub/block/block_radix_sort.cuh>
 
-// Build-time A/B switch of the segmented walk's candidate append (tools/ab:
-// a separate build; branch-free measured faster: hop 3 at C2 106.5 vs 108.7 us)
-#ifndef BGL_APPEND_BRANCHFREE
-#define BGL_APPEND_BRANCHFREE 1
-#endif
 
 namespace bgl {
 
@@ -603,8 +598,10 @@ __device__ __forceinline__ uint32_t thr_hi(uint64_t tm /* T, <= 2^53 */) {
 }
 
 // Walk the run's light draws in chunks of 32; returns the candidate count.
-// Per chunk: the 128-bit affine step, the high word of XSL-RR, one 32-bit
-// compare, a ballot; the low word and the key are formed by passing lanes only.
+// Per chunk: the 128-bit affine step (affine_cc), the high word of XSL-RR,
+// one 32-bit compare, a ballot and a branch-free append (every lane forms its
+// key, passing lanes store it: faster than a branch around the append, whose
+// body runs in ~97% of chunks anyway).
 // The state of walk position w (parent j) is s0 advanced by d_run + gap_j + w + 1.
 template <bool kGaps>
 __device__ __forceinline__ int seg_walk(SegWarp& sw, const PcgTable T, U128 A32, U128 C32, U128 s0, int64_t d_run,
@@ -635,7 +632,6 @@ __device__ __forceinline__ int seg_walk(SegWarp& sw, const PcgTable T, U128 A32,
         const uint32_t out_hi = __funnelshift_r(a, b, rot);
         const bool pass = out_hi < th;
         const unsigned bm = __ballot_sync(0xffffffffu, pass);
-#if BGL_APPEND_BRANCHFREE
         // every lane forms its key, passing lanes store it
         const int pos = L + __popc(bm & lt);
         const uint32_t out_lo = __funnelshift_r(b, a, rot);
@@ -644,17 +640,6 @@ __device__ __forceinline__ int seg_walk(SegWarp& sw, const PcgTable T, U128 A32,
             sw.cand[pos] = key;
             sw.cj[pos] = (uint8_t)j;
         }
-#else
-        // the low word and the key are formed by passing lanes only
-        if (pass) {
-            const int pos = L + __popc(bm & lt);
-            if (pos < cap) {
-                const uint32_t out_lo = __funnelshift_r(b, a, rot);
-                sw.cand[pos] = ((uint64_t)out_hi << 32) | (uint64_t)((out_lo & ~2047u) | (uint32_t)(w - ws));
-                sw.cj[pos] = (uint8_t)j;
-            }
-        }
-#endif
         L += __popc(bm);
         s = affine_cc(A32, C32, s);
     }
