@@ -24,7 +24,7 @@ import bench  # noqa: E402
 from paper_2112_08541_b200.cachesim import CacheConfig, simulate  # noqa: E402
 from paper_2112_08541_b200.features import FeatureCacheEngine  # noqa: E402
 from paper_2112_08541_b200.ordering import BatchSchedule  # noqa: E402
-from paper_2112_08541_b200.sampler import AccessTrace, SamplingConfig, simulate_epoch  # noqa: E402
+from paper_2112_08541_b200.sampler import SamplingConfig, simulate_epoch  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--batches", type=int, default=25)

@@ -24,7 +24,6 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 from paper_2112_08541_b200.cachesim import CacheConfig, compare_policies, simulate  # noqa: E402
-from paper_2112_08541_b200.graph import generate_power_law_device  # noqa: E402
 from paper_2112_08541_b200.ordering import BatchSchedule, proximity_schedule_device  # noqa: E402
 from paper_2112_08541_b200.sampler import SamplingConfig, simulate_epoch  # noqa: E402
 
