@@ -545,8 +545,8 @@ __device__ __forceinline__ uint64_t gtimer_after(int64_t dep) {
     return t;
 }
 __device__ __noinline__ void seg_trace_record(unsigned long long* trace, int64_t n, int64_t r, int32_t Wtot,
-                                              uint64_t t_claim, uint64_t t_walk, uint64_t t_post, uint64_t t_loaded,
-                                              uint64_t t_prefix) {
+                                              const uint64_t* ts) {
+    const uint64_t t_claim = ts[0], t_loaded = ts[1], t_prefix = ts[2], t_walk = ts[3], t_post = ts[4];
     unsigned sm;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
     const unsigned long long slot = atomicAdd(trace, 1ull);
@@ -571,6 +571,7 @@ struct SegWarp {
     int32_t wend[33];    // [32]: sentinel INT_MAX (ends the parent search)
     int32_t cst[33];     // seg_post: each parent's candidate range start; [32] = list length
     uint8_t cj[kSegCap];
+    uint64_t ts[6];      // diagnostics: claim, loaded, prefix, walk, post (lane 0; kept out of registers)
 };
 
 // The lane's parent bound / threshold / walk start stay in registers and are
@@ -737,7 +738,7 @@ __device__ __forceinline__ void seg_part(SegWarp& sw, bool valid, int64_t off, i
                                          U128 C32, int lane, unsigned lt, int cap, float ma, float mb,
                                          const int32_t* __restrict__ indices, int32_t* __restrict__ out_ids,
                                          int32_t* __restrict__ out_pidx, uint32_t* __restrict__ bitmap,
-                                         bool trace, uint64_t& t_walk, uint64_t& t_post, int32_t& Wtot_out) {
+                                         bool trace, int32_t& Wtot_out) {
     const unsigned FULL = 0xffffffffu;
     const int64_t ex0 = __shfl_sync(FULL, ex_d, 0);
     const bool light = valid && !hv && deg > 0;
@@ -760,11 +761,11 @@ __device__ __forceinline__ void seg_part(SegWarp& sw, bool valid, int64_t off, i
     const unsigned hm = __ballot_sync(FULL, valid && hv);
     __syncwarp();
     int L = 0;
-    if (trace) t_walk = gtimer();
+    if (trace && lane == 0) sw.ts[3] = gtimer();
     if (Wtot > 0) L = hm ? seg_walk<true>(sw, T, A32, C32, T.state(), D0 + ex0, Wtot, lane, lt, cap)
                          : seg_walk<false>(sw, T, A32, C32, T.state(), D0 + ex0, Wtot, lane, lt, cap);
     __syncwarp();
-    if (trace) t_post = gtimer();
+    if (trace && lane == 0) sw.ts[4] = gtimer();
     seg_post(sw, L, cap, lane, (int)k, off, ex_k, light, deg, T.state(), (uint64_t)(D0 + ex_d), pid, T, A32, C32,
              indices, out_ids, out_pidx, bitmap);
     Wtot_out = Wtot;
@@ -804,8 +805,7 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
         if (lane == 0) r = (int64_t)atomicAdd(ss.ticket, 1u);
         r = __shfl_sync(FULL, r, 0);
         if (r >= nruns) break;
-        uint64_t t_claim = 0, t_walk = 0, t_post = 0, t_loaded = 0, t_prefix = 0;
-        if (trace) t_claim = gtimer();
+        if (trace && lane == 0) sw.ts[0] = gtimer();
         const int64_t q = r * run + lane;
         const bool valid = lane < run && q < n;
         const int32_t p = valid ? parents[q] : 0;
@@ -816,7 +816,7 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
         const int64_t incl_k = warp_incl_scan(k);
         const int64_t agg_d = __shfl_sync(FULL, incl_d, 31);
         const int64_t agg_k = __shfl_sync(FULL, incl_k, 31);
-        if (trace) t_loaded = gtimer_after(agg_k);
+        if (trace && lane == 0) sw.ts[1] = gtimer_after(agg_k);
         if (lane == 0) {
             const uint64_t f = r == 0 ? kFlagInc : kFlagAgg;
             atomicExch((unsigned long long*)(ss.status + r), (unsigned long long)(f | ((uint64_t)agg_d & kValMask)));
@@ -825,7 +825,7 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
         }
         const int64_t pre_d = warp_lookback1(ss.status, r, agg_d);
         const int64_t pre_k = warp_lookback1(ss.status + ss.max_tiles, r, agg_k);
-        if (trace) t_prefix = gtimer_after(pre_d + pre_k);
+        if (trace && lane == 0) sw.ts[2] = gtimer_after(pre_d + pre_k);
         const int64_t ex_d = pre_d + incl_d - deg;
         const int64_t ex_k = pre_k + incl_k - k;
         const bool hv = valid && (k > 32 || deg > heavy_deg);
@@ -878,8 +878,8 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
         }
         int32_t Wtot = 0;
         seg_part(sw, valid && lane < jend, off, deg, k, ex_d, ex_k, hv, (int32_t)q, D0, T, A32, C32, lane, lt, cap,
-                 ma, mb, indices, out_ids, out_pidx, bitmap, trace != nullptr, t_walk, t_post, Wtot);
-        if (trace && lane == 0) seg_trace_record(trace, n, r, Wtot, t_claim, t_walk, t_post, t_loaded, t_prefix);
+                 ma, mb, indices, out_ids, out_pidx, bitmap, trace != nullptr, Wtot);
+        if (trace && lane == 0) seg_trace_record(trace, n, r, Wtot, sw.ts);
     }
     if (split_min <= 0) return;
     // no run left: take split-off parts until every run has decided and the queue is drained
@@ -916,10 +916,9 @@ sample_seg_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict_
         const int64_t ex_d = valid ? ld_volatile(deg_prefix + q) : 0;
         const int64_t ex_k = valid ? ld_volatile(k_prefix + q) : 0;
         const bool hv = valid && (k > 32 || deg > heavy_deg);
-        uint64_t t_walk = 0, t_post = 0;
         int32_t Wtot = 0;
         seg_part(sw, valid, off, deg, k, ex_d, ex_k, hv, (int32_t)q, D0, T, A32, C32, lane, lt, cap, ma, mb, indices,
-                 out_ids, out_pidx, bitmap, false, t_walk, t_post, Wtot);
+                 out_ids, out_pidx, bitmap, false, Wtot);
     }
 }
 
