@@ -57,6 +57,16 @@ __device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
 template <typename T>
 __device__ __forceinline__ T ld_volatile(const T* p) { return *(const volatile T*)p; }
 
+// Poll of a look-back status word (flag and value packed in one 64-bit word,
+// published by device-scope atomics): a relaxed load at GPU scope. A volatile
+// load compiles to LDG.E.STRONG.SYS (system scope) on sm_100a, which costs
+// more than an L2 round trip on every window of a look-back chain.
+__device__ __forceinline__ uint64_t ld_status(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

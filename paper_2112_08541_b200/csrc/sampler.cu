@@ -209,7 +209,7 @@ __device__ __forceinline__ int64_t warp_lookback1(uint64_t* status, int64_t r, i
             const int64_t idx = j - lane;
             uint64_t w = kFlagInc;
             if (idx >= 0) {
-                do { w = ld_volatile(status + idx); } while ((w >> 62) == 0);
+                do { w = ld_status(status + idx); } while ((w >> 62) == 0);
             }
             const unsigned inc = __ballot_sync(0xffffffffu, (w >> 62) == 2);
             const int stop = inc ? __ffs(inc) - 1 : 31;
@@ -1065,7 +1065,7 @@ sample_prep_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict
         int64_t acc = 0;
         for (int64_t j = lane; j < tile; j += 32) {
             uint64_t w;
-            do { w = ld_volatile(st + j); } while ((w >> 62) == 0);
+            do { w = ld_status(st + j); } while ((w >> 62) == 0);
             acc += (int64_t)(w & kValMask);
         }
         acc = warp_sum_i64(acc);

@@ -123,7 +123,7 @@ sample_counter_kernel(const int64_t* __restrict__ indptr, const int32_t* __restr
                 const int64_t idx = j - lane;
                 uint64_t w = kFlagInc;
                 if (idx >= 0) {
-                    do { w = ld_volatile(ss.status + idx); } while ((w >> 62) == 0);
+                    do { w = ld_status(ss.status + idx); } while ((w >> 62) == 0);
                 }
                 const unsigned inc = __ballot_sync(0xffffffffu, (w >> 62) == 2);
                 const int stop = inc ? __ffs(inc) - 1 : 31;
@@ -221,7 +221,7 @@ sample_counter_group_kernel(const int64_t* __restrict__ indptr, const int32_t* _
                 const int64_t idx = j - lane;
                 uint64_t w = kFlagInc;
                 if (idx >= 0) {
-                    do { w = ld_volatile(ss.status + idx); } while ((w >> 62) == 0);
+                    do { w = ld_status(ss.status + idx); } while ((w >> 62) == 0);
                 }
                 const unsigned inc = __ballot_sync(FULL, (w >> 62) == 2);
                 const int stop = inc ? __ffs(inc) - 1 : 31;

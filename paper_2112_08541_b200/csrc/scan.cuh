@@ -66,7 +66,7 @@ __device__ __forceinline__ void lookback(const ScanState& s, int64_t tile, const
                 int64_t idx = j - lane;
                 uint64_t w = kFlagInc;   // before tile 0: inclusive zero
                 if (idx >= 0) {
-                    do { w = ld_volatile(st + idx); } while ((w >> 62) == 0);
+                    do { w = ld_status(st + idx); } while ((w >> 62) == 0);
                 }
                 unsigned inc = __ballot_sync(0xffffffffu, (w >> 62) == 2);
                 int stop = inc ? __ffs(inc) - 1 : 31;
